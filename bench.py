@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""BAGEL hot-path benchmark (BASELINE.json metric: trajectory-steps/sec (fwd+bwd) and
+policy-grad iters/sec).
+
+One "step" = one policy-gradient iteration = rollout_cost_and_grad over the rank's
+trajectories (forward T steps through the LOVE-GP model + reverse pass) plus the single
+gradient all_reduce when N > 1.  Workload: BASELINE.json configs[1] ("C2": GP N=5,000 on
+(pos, vel, valve cmd), LOVE rank 256, policy MLP 4-64-64-1, B=1,024, T=100), synthetic
+boom-plant data (workloads/), B=1,024 trajectories per GPU (weak scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+Prints ONE JSON line on rank 0.  Timing: CUDA events on the context stream around each
+timed iteration, L2 flushed (256 MiB write) between iterations outside the events,
+barrier + synchronize on both sides of the timed region, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "trajectory-steps/sec (fwd+bwd)"
+UNIT = "traj-steps/s"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def flops_per_traj_step(wl):
+    """Algorithmic tensor-eligible flops of the GP contraction:
+    pass 1 (a3): 2 p N (1 + d + k); pass 2 (a5): 2 p N k + 2 p N (1 + d)."""
+    p, N, d, k = wl.p, wl.N, wl.d, wl.rank
+    return 2 * p * N * (1 + d + k), 2 * p * N * k + 2 * p * N * (1 + d)
+
+
+def cpu_baseline(wl, budget_s=20.0, max_traj=256):
+    """Oracle (float64 C, OpenMP over trajectories) on a bounded trajectory subset, full N, k, T."""
+    import oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    O.set_num_threads(cores)
+    t0 = time.perf_counter()
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    build_s = time.perf_counter() - t0
+    phi = "xg" if wl.sizes[0] == 2 * wl.p else "xgd"
+    n, total_t, total_steps = 8, 0.0, 0
+    while True:
+        n = min(n, max_traj, wl.B)
+        t0 = time.perf_counter()
+        O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[:n], wl.goals[:n], wl.T,
+                  W.rollout_seed(0), B_global=wl.B)
+        dt = time.perf_counter() - t0
+        total_t += dt
+        total_steps += n * wl.T
+        if total_t >= budget_s / 2 or n >= max_traj or n >= wl.B:
+            break
+        n *= 2
+    return {"value": total_steps / total_t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{total_steps // wl.T} trajectories x T={wl.T} (full N={wl.N}, k={wl.rank}) fwd+bwd in "
+                      f"{total_t:.1f} s; oracle cache build {build_s:.1f} s excluded"}
+
+
+def run_reference(args, wl, rank):
+    if rank != 0:
+        return
+    import oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    O.set_num_threads(cores)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    phi = "xg" if wl.sizes[0] == 2 * wl.p else "xgd"
+    n = min(wl.B, args.ref_traj)
+    for i in range(args.warmup):
+        O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[:n], wl.goals[:n], wl.T,
+                  W.rollout_seed(i), B_global=wl.B)
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[:n], wl.goals[:n], wl.T,
+                  W.rollout_seed(args.warmup + i), B_global=wl.B)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * wl.T * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(args, wl, n_traj=n),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} of {wl.B} trajectories per step, full N={wl.N}, k={wl.rank}, T={wl.T}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, wl, n_traj=None):
+    return {"workload": f"{args.config}: GP N={wl.N} d={wl.d} p={wl.p}, LOVE rank {wl.rank}, "
+                        f"MLP {'-'.join(map(str, wl.sizes))}, B={wl.B} per GPU, T={wl.T}",
+            "global_batch": wl.B * args.gpus if n_traj is None else n_traj, "horizon": wl.T,
+            "parallelism": f"dp{args.gpus}", "l2": "flushed (256 MiB write) between timed iterations"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="bagel", choices=["bagel", "reference"])
+    ap.add_argument("--ref-traj", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = W.config(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, wl, rank)
+        return
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2202_13638_b200 import bagel
+    from paper_2202_13638_b200.dist import allreduce_cost_grad, shard
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    # weak scaling: B trajectories per GPU, global ids contiguous per rank
+    B_local = wl.B
+    B_global = wl.B * world
+    x0g, gg = W.sample_states_goals(wl.X, wl.p, B_global)
+    off, bl = shard(B_global, world, rank)
+    assert bl == B_local
+
+    ctx = bagel.setup(wl, device=local)
+    cache_s = ctx.cache_seconds
+    theta = torch.from_numpy(wl.theta).to(dev)
+    x0 = torch.from_numpy(x0g[off:off + bl]).to(dev)
+    goals = torch.from_numpy(gg[off:off + bl]).to(dev)
+    grad = torch.empty(ctx.n_params, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def iteration(i):
+        cost, g = ctx.rollout_cost_and_grad(theta, x0, goals, wl.T, W.rollout_seed(i), traj_offset=off,
+                                            B_global=B_global, grad=grad)
+        return allreduce_cost_grad(cost, g)
+
+    for i in range(args.warmup):
+        iteration(i)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device-resident inputs)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            iteration(args.warmup + i)
+            ev[i][1].record(stream)
+            launches += ctx.last_launch_count()
+        torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    prof = ctx.profile_get()
+    ctx.profile(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = B_global * wl.T * args.steps / (tot_ms / 1e3)
+
+    # ---------------- end-to-end: host (pinned) buffers through the C ABI, copies inside the timing
+    th_h = torch.from_numpy(wl.theta).pin_memory()
+    x0_h = torch.from_numpy(x0g[off:off + bl]).pin_memory()
+    g_h = torch.from_numpy(gg[off:off + bl]).pin_memory()
+    grad_h = torch.empty(ctx.n_params).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(e2e_steps):
+        cost, g = ctx.rollout_cost_and_grad(th_h, x0_h, g_h, wl.T, W.rollout_seed(1000 + i), traj_offset=off,
+                                            B_global=B_global, grad=grad if world > 1 else grad_h)
+        if world > 1:
+            cost, g = allreduce_cost_grad(cost, g)
+            grad_h.copy_(g, non_blocking=True)
+            stream.synchronize()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(e2e_ms, op=tdist.ReduceOp.MAX)
+    e2e_value = B_global * wl.T * e2e_steps / (float(e2e_ms.item()) / 1e3)
+    h2d = (ctx.n_params + 2 * bl * wl.p) * 4
+    d2h = ctx.n_params * 4 + 8
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        f1, f2 = flops_per_traj_step(wl)
+        names = {"gp_pass1": f1, "gp_pass2": f2}
+        dom = max(names, key=lambda n: prof[n][0])
+        dom_ms, dom_n = prof[dom]
+        per_launch_s = dom_ms / 1e3 / dom_n
+        flops_launch = names[dom] * B_local
+        achieved = flops_launch / per_launch_s / 1e12
+        peak = pk.get("bf16_tflops_sustained", 1363.2)
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+            except (OSError, ValueError):
+                traffic = None
+        step_share = {k: round(v[0] / max(1e-9, sum(x[0] for x in prof.values())), 4) for k, v in prof.items()}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (boom-plant transitions, workloads/)",
+            "config": config_dict(args, wl),
+            "policy_grad_iters_per_s": 1e3 / ms_per_step,
+            "cache_build_s": cache_s,
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"{pk_kind} bf16_tflops_sustained (fp16 kind::f16 at the bf16 rate)",
+                         "algorithmic_flops_per_launch": flops_launch},
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "kernel_share": step_share,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(wl)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

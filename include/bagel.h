@@ -1,0 +1,195 @@
+/*
+ * bagel.h -- C ABI of libbagel.so, the B200 (sm_100a) hot path of BAGEL
+ * (arXiv 2202.13638, "Policy optimization via Batch Automatic differentiation
+ * of Gaussian process Evaluations using Lanczos variance estimates").
+ *
+ * Citations: PAPER.md line numbers are written P:NN, SPEC.md lines S:NN,
+ * equations follow the paper's label order (Eq.1 dynamics ... Eq.11 batched
+ * objective); readings are written R<n>.
+ *
+ * Conventions (all entry points):
+ *   - return 0 on success, else one of the BAGEL_E_* codes below; no C++
+ *     exception crosses the ABI; bagel_last_error() holds a one-line message
+ *     naming the argument, its shape, or (step, row) for numerical faults.
+ *   - array arguments are row-major float32 unless stated.  Pointers marked
+ *     [dev|host] may be device memory or host memory (pageable or pinned);
+ *     host buffers are staged through library-owned device memory with
+ *     cudaMemcpyAsync on the context stream.  Pointers marked [dev] must be
+ *     device memory, [host] host memory.
+ *   - everything is enqueued on the stream given to bagel_create (or
+ *     bagel_set_stream); calls that return host values synchronise it.
+ *   - the library owns every internal buffer; caller buffers are never kept.
+ *   - one context per GPU / rank; a context is not thread-safe.
+ *   - no global state: two contexts never share memory.
+ */
+#ifndef BAGEL_H
+#define BAGEL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bagel_ctx bagel_ctx;
+
+/* Error classes mirror the specification's exit codes: 1 usage/config,
+ * 2 numerical, 3 I/O or device.  BAGEL_E_STATE is a usage error (class 1). */
+#define BAGEL_OK 0
+#define BAGEL_E_ARG 1     /* bad argument value or shape                      */
+#define BAGEL_E_NUMERIC 2 /* pivot <= 0, T not PD, non-finite state    */
+#define BAGEL_E_CUDA 3    /* CUDA runtime failure or out of device memory      */
+#define BAGEL_E_STATE 4   /* call out of order (no gp_load / cache / policy)   */
+
+/* ------------------------------------------------------------------ context */
+
+/* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
+ * (NULL = legacy default stream), typically torch.cuda.current_stream().
+ * *out receives the context.  Errors: E_ARG (out NULL), E_CUDA. */
+int bagel_create(bagel_ctx** out, int device, void* cuda_stream);
+
+/* Free every library buffer.  NULL is accepted. */
+int bagel_destroy(bagel_ctx* ctx);
+
+/* Re-target subsequent work to another stream on the same device. */
+int bagel_set_stream(bagel_ctx* ctx, void* cuda_stream);
+
+/* Message of the last failing call on this context ("" if none).  The pointer
+ * stays valid until the next call on the context. */
+const char* bagel_last_error(const bagel_ctx* ctx);
+
+/* --------------------------------------------------------------- GP model */
+
+/* gp_load -- the GP transition model of Eq.1-4: one independent
+ * SE-ARD GP per state dimension m = 0..p-1 (reading R7, R8), prior mean
+ * 0 (R4), Delta targets (R6).
+ *   X            [dev|host] N x d training inputs (x_k, u_k), d = p + q, already
+ *                normalised by the caller (R22).
+ *   y            [dev|host] N x p targets; column m is Delta x_m.
+ *   lengthscales [dev|host] p x d, l_mc > 0; Lambda = diag(l^-2) (R1).
+ *   outputscale  [dev|host] p, signal VARIANCE s_m = alpha^2 of Eq.4 (R2).
+ *   noise        [dev|host] p, observation-noise VARIANCE sigma_n^2 >= 1e-8 (R3).
+ * Copies everything into library memory; invalidates any LOVE cache.
+ * Errors: E_ARG for N < 1, d < 2, p < 1, p >= d, p > 4, non-finite or
+ * non-positive l or s, noise < 1e-8, non-finite X or y. */
+int gp_load(bagel_ctx* ctx, const float* X, const float* y, int N, int d, int p,
+            const float* lengthscales, const float* outputscale, const float* noise);
+
+/* love_cache_build -- the one-time LOVE cache ("one-time caching
+ * operation ... ~0.6s"), for every output m, in float64 on the GPU:
+ *   alpha_m = Khat_m^-1 y_m by blocked Cholesky (Khat = K + sigma_n^2 I; R21),
+ *   Lanczos(Khat_m, q1 = y_m/||y_m||, `rank` steps, classical Gram-Schmidt
+ *   twice, Philox restart on breakdown; R20) -> Q, T;  R_m = L_T^-1 Q^T;
+ *   then packs V_m = s_m [alpha_m | alpha_m o X | R_m^T] for the hot path.
+ * Synchronous.  seconds_out [host, nullable] receives the wall time.
+ * Errors: E_STATE without gp_load; E_ARG for rank < 1 or rank > N or rank >
+ * 768; E_NUMERIC if a Cholesky pivot <= 0 (message carries the pivot index)
+ * or T is not positive definite; E_CUDA (incl. out of memory). */
+int love_cache_build(bagel_ctx* ctx, int rank, double* seconds_out);
+
+/* ------------------------------------------------------- policy / reward */
+
+/* policy_configure -- tanh MLP policy u = pi_theta(x, g) (P:104, P:129,
+ * P:149 "bounded in [-1,1] using a saturating function"; R13).
+ *   sizes [host] n_sizes = L + 1 layer widths (in, h1, ..., q).  in = 2p selects
+ *   phi = [x, g], in = 3p selects phi = [x, g, g - x] (R14).  Last width = q = d - p.
+ * theta layout (rollout_cost_and_grad): per layer l, W_l [out x in] row-major
+ * then b_l [out] (PyTorch nn.Sequential(Linear, Tanh, ...) order).
+ * Errors: E_STATE without gp_load; E_ARG for n_sizes < 2, a width < 1 or > 256,
+ * in not in {2p, 3p}, q != d - p. */
+int policy_configure(bagel_ctx* ctx, const int* sizes, int n_sizes);
+
+/* reward_configure -- Eq.8: r = exp(-(1/(2 sigma_r^2)) (x-g)^T Q (x-g)).
+ *   Q_diag [host] p non-negative weights (default diag{10, 0.1} for p = 2, P:149;
+ *   R12 for other p); sigma_r > 0 (default 1, R11).
+ * Errors: E_STATE without gp_load; E_ARG for negative/non-finite Q or sigma_r <= 0. */
+int reward_configure(bagel_ctx* ctx, const float* Q_diag, float sigma_r);
+
+/* ------------------------------------------------------------ hot path */
+
+/* rollout_cost_and_grad -- one BAGEL iteration's forward + backward pass
+ * (Alg.1 lines P:101-109, Eq.9-11):
+ *   G_b = r(x0_b, g_b);  for t = 0..T-1: u = pi(x_t, g); x* = [x_t, u];
+ *   mu_m = k(x*,X) alpha_m (Eq.2), v_m = s_m - ||R_m k(x*,X)||^2 (LOVE, Eq.3),
+ *   x_{t+1,m} = x_{t,m} + mu_m + sqrt(max(v_m, 1e-12)) eps_{b,t,m} (Eq.9-10, R6, R19),
+ *   G_b += r(x_{t+1}, g_b);
+ *   L = -(1/B_global) sum_b G_b (R9), and dL/dtheta by reverse mode
+ *   through the whole horizon (pathwise, R18).
+ *   eps_{b,t,m} = BoxMuller(Philox4x32-10(key = (seed lo, seed hi),
+ *   ctr = (traj_offset + b, t, m >> 2, 0)))[m & 3].
+ * Arguments:
+ *   policy_params [dev|host] |theta| floats, layout of policy_configure.
+ *   x0, goals     [dev|host] B x p (normalised units; goals are constants, R23).
+ *   B >= 1 trajectories on this rank; T >= 0 steps.
+ *   seed          64-bit Philox key for this iteration (fresh per iteration, R17).
+ *   traj_offset   global id of row 0 (rank r of G: r*B/G, P:142 batches sharded).
+ *   B_global      the 1/b of Eq.11 (total trajectories over all ranks), >= B.
+ *   mean_cost     [host] receives this rank's share of L (already / B_global).
+ *   grad          [dev|host] |theta| floats, overwritten with this rank's dL/dtheta.
+ * Synchronises the stream before returning.  T = 0 returns -mean r(x0) share
+ * and a zero gradient.
+ * Errors: E_STATE without cache or policy; E_ARG (B < 1, T < 0, B_global < B,
+ * B or T beyond the workspace limits); E_NUMERIC on a non-finite state (message
+ * "step t, row b"); E_CUDA. */
+int rollout_cost_and_grad(bagel_ctx* ctx, const float* policy_params, const float* x0,
+                          const float* goals, int B, int T, uint64_t seed, long long traj_offset,
+                          long long B_global, double* mean_cost, float* grad);
+
+/* Number of kernel launches the last rollout_cost_and_grad enqueued (host int). */
+int bagel_last_launch_count(const bagel_ctx* ctx, int* launches);
+
+/* Per-kernel device timing for the roofline report (bench.py).  While enabled,
+ * every hot-path launch is bracketed by cudaEvents on the context stream and
+ * its duration is accumulated per kernel class:
+ *   0 gp_pass1 (a2+a3 contraction), 1 gp_reduce1 (a4), 2 gp_pass2 (a5),
+ *   3 step_epilogue (a6-a8 + next a1), 4 init (a1 + a7 at t = 0),
+ *   5 reverse (a9), 6 reduce (a10).
+ * bagel_profile(ctx, 1) enables and clears, bagel_profile(ctx, 0) disables.
+ * bagel_profile_get: total_ms [host] and launches [host] of class `kernel`
+ * since the last enable (synchronises the stream).  Errors: E_ARG. */
+#define BAGEL_PROFILE_CLASSES 7
+int bagel_profile(bagel_ctx* ctx, int enable);
+int bagel_profile_get(bagel_ctx* ctx, int kernel, double* total_ms, long long* launches);
+
+/* ------------------------------------------------------- test-only exports */
+
+/* One GP query per row of xstar [dev] M x d with the LOVE variance and input
+ * Jacobians (Appendix B of SURVEY.md; the autodiff of Eq.2-3):
+ *   mean, var [dev] M x p; dmean, dvar [dev] M x p x d (dvar uses the unclamped v).
+ * Runs the same kernels as the rollout's GP step. */
+int bagel_gp_predict(bagel_ctx* ctx, const float* xstar, int M, float* mean, float* var,
+                     float* dmean, float* dvar);
+
+/* Forward rollout with per-step traces (same kernels as rollout_cost_and_grad):
+ *   x [dev] (T+1) x B x p states, mu / var [dev] T x B x p GP moments,
+ *   ret [dev] B returns G_b.  Any trace pointer may be NULL. */
+int bagel_rollout_trace(bagel_ctx* ctx, const float* policy_params, const float* x0,
+                        const float* goals, int B, int T, uint64_t seed, long long traj_offset,
+                        float* x, float* mu, float* var, float* ret);
+
+/* Raw Philox4x32-10: ctr [dev] n x 4 u32, key [host] 2 u32, out [dev] n x 4 u32. */
+int bagel_philox4x32_10(bagel_ctx* ctx, const uint32_t* ctr, const uint32_t* key, int n,
+                        uint32_t* out);
+
+/* Rollout noise as the rollout draws it: out [dev] T x B x p floats,
+ * out[t][b][m] = eps_{traj_offset + b, t, m} for `seed`. */
+int bagel_philox_normals(bagel_ctx* ctx, uint64_t seed, long long traj_offset, int B, int T,
+                         int p, float* out);
+
+/* LOVE cache of output m as float64 device arrays: alpha [dev] N, R [dev] rank x N.
+ * bagel_cache_rank returns the rank k (0 if no cache). */
+int bagel_cache_rank(const bagel_ctx* ctx, int* rank);
+int bagel_cache_get(bagel_ctx* ctx, int m, double* alpha, double* R);
+
+/* Install an externally computed cache (isolates hot-path parity from the
+ * cache build).  Call once per output m = 0..p-1 with the same rank; the
+ * packed hot-path operand V_m is rebuilt for that output.
+ *   alpha [dev] N float64, R [dev] rank x N float64.
+ * Errors: E_STATE without gp_load; E_ARG for m out of range, rank change. */
+int bagel_cache_set(bagel_ctx* ctx, int m, int rank, const double* alpha, const double* R);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BAGEL_H */

@@ -64,8 +64,10 @@ void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint3
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* 24-bit uniform strictly inside (0,1): ((o >> 8) + 0.5) * 2^-24 (exact in fp32 and fp64). */
-static double orc_uniform(uint32_t o) { return ((double)(o >> 8) + 0.5) * (1.0 / 16777216.0); }
+/* 23-bit uniform strictly inside (0,1): ((o >> 9) + 0.5) * 2^-23.  Every value
+ * has at most 24 significant bits, so it is exact in fp32 and fp64 alike
+ * (reading R29). */
+static double orc_uniform(uint32_t o) { return ((double)(o >> 9) + 0.5) * (1.0 / 8388608.0); }
 
 /* Box-Muller on the four uniforms of one Philox call (fp64). */
 void orc_box_muller4(const uint32_t o[4], double eps[4])

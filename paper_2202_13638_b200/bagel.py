@@ -1,0 +1,245 @@
+"""Thin ctypes binding of libbagel.so (include/bagel.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only
+turns torch tensors / numpy arrays into pointers, sizes and the current CUDA
+stream.  There is no CPU fallback: if libbagel.so is missing or fails to load,
+``lib()`` raises.  Method names follow the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+import torch
+
+from .build import LIB
+
+_lock = threading.Lock()
+_lib = None
+
+E_ARG, E_NUMERIC, E_CUDA, E_STATE = 1, 2, 3, 4
+_vp = C.c_void_p
+
+
+class BagelError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[bagel error {code}] {msg}")
+        self.code = code
+
+
+def lib() -> C.CDLL:
+    """Load libbagel.so (built in-tree by __graft_entry__.build()); never falls back."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB):
+                raise RuntimeError(f"{LIB} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = C.CDLL(LIB)
+            L.bagel_create.argtypes = [C.POINTER(_vp), C.c_int, _vp]
+            L.bagel_destroy.argtypes = [_vp]
+            L.bagel_set_stream.argtypes = [_vp, _vp]
+            L.bagel_last_error.argtypes = [_vp]
+            L.bagel_last_error.restype = C.c_char_p
+            L.gp_load.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp]
+            L.love_cache_build.argtypes = [_vp, C.c_int, C.POINTER(C.c_double)]
+            L.policy_configure.argtypes = [_vp, C.POINTER(C.c_int), C.c_int]
+            L.reward_configure.argtypes = [_vp, C.POINTER(C.c_float), C.c_float]
+            L.rollout_cost_and_grad.argtypes = [_vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_uint64, C.c_longlong,
+                                                C.c_longlong, C.POINTER(C.c_double), _vp]
+            L.bagel_last_launch_count.argtypes = [_vp, C.POINTER(C.c_int)]
+            L.bagel_gp_predict.argtypes = [_vp, _vp, C.c_int, _vp, _vp, _vp, _vp]
+            L.bagel_rollout_trace.argtypes = [_vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_uint64, C.c_longlong,
+                                              _vp, _vp, _vp, _vp]
+            L.bagel_philox4x32_10.argtypes = [_vp, _vp, C.POINTER(C.c_uint32), C.c_int, _vp]
+            L.bagel_philox_normals.argtypes = [_vp, C.c_uint64, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp]
+            L.bagel_cache_rank.argtypes = [_vp, C.POINTER(C.c_int)]
+            L.bagel_cache_get.argtypes = [_vp, C.c_int, _vp, _vp]
+            L.bagel_cache_set.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
+            L.bagel_profile.argtypes = [_vp, C.c_int]
+            L.bagel_profile_get.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
+            _lib = L
+    return _lib
+
+
+EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_error", "gp_load", "love_cache_build",
+           "policy_configure", "reward_configure", "rollout_cost_and_grad", "bagel_last_launch_count",
+           "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
+           "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get"]
+
+PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce"]
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def _f32(a, device=None):
+    """Contiguous float32 tensor (kept on its device unless `device` is given)."""
+    if isinstance(a, np.ndarray):
+        a = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+    t = a.to(dtype=torch.float32) if a.dtype != torch.float32 else a
+    if device is not None:
+        t = t.to(device)
+    return t.contiguous()
+
+
+class Context:
+    """One bagel_ctx per GPU / rank (not thread-safe)."""
+
+    def __init__(self, device: int | None = None, stream: torch.cuda.Stream | None = None):
+        self.L = lib()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.dev = torch.device("cuda", self.device)
+        self.stream = stream or torch.cuda.current_stream(self.dev)
+        h = _vp()
+        self._check(self.L.bagel_create(C.byref(h), self.device, _vp(self.stream.cuda_stream)), ctx=None)
+        self.h = h
+        self.p = self.d = self.N = 0
+        self.n_params = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.bagel_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, ctx=True):
+        if rc != 0:
+            msg = self.L.bagel_last_error(self.h).decode() if ctx and self.h else "bagel_create failed"
+            raise BagelError(rc, msg)
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        self._check(self.L.bagel_set_stream(self.h, _vp(stream.cuda_stream)))
+
+    # ------------------------------------------------------------ model
+    def gp_load(self, X, Y, lengthscales, outputscale, noise):
+        X, Y = _f32(X, self.dev), _f32(Y, self.dev)
+        ell, s, sn = _f32(lengthscales, self.dev), _f32(outputscale, self.dev), _f32(noise, self.dev)
+        N, d = X.shape
+        p = Y.shape[1]
+        self._check(self.L.gp_load(self.h, _ptr(X), _ptr(Y), N, d, p, _ptr(ell), _ptr(s), _ptr(sn)))
+        self.N, self.d, self.p = N, d, p
+
+    def love_cache_build(self, rank: int) -> float:
+        sec = C.c_double(0.0)
+        self._check(self.L.love_cache_build(self.h, int(rank), C.byref(sec)))
+        return sec.value
+
+    def policy_configure(self, sizes):
+        arr = (C.c_int * len(sizes))(*[int(s) for s in sizes])
+        self._check(self.L.policy_configure(self.h, arr, len(sizes)))
+        self.n_params = int(sum((sizes[i] + 1) * sizes[i + 1] for i in range(len(sizes) - 1)))
+
+    def reward_configure(self, Q, sigma_r: float = 1.0):
+        q = np.ascontiguousarray(Q, dtype=np.float32)
+        self._check(self.L.reward_configure(self.h, q.ctypes.data_as(C.POINTER(C.c_float)), float(sigma_r)))
+
+    # ------------------------------------------------------------ hot path
+    def rollout_cost_and_grad(self, theta, x0, goals, T: int, seed: int, traj_offset: int = 0,
+                              B_global: int | None = None, grad=None):
+        """Returns (this rank's share of L, dL/dtheta).  Tensors may live on the GPU or on the host
+        (host buffers are staged by the library); `grad` (optional) is written in place."""
+        B = int(x0.shape[0])
+        if B_global is None:
+            B_global = B
+        if grad is None:
+            grad = torch.empty(self.n_params, dtype=torch.float32, device=self.dev)
+        cost = C.c_double(0.0)
+        self._check(self.L.rollout_cost_and_grad(self.h, _ptr(theta), _ptr(x0), _ptr(goals), B, int(T),
+                                                 int(seed) & 0xFFFFFFFFFFFFFFFF, int(traj_offset), int(B_global),
+                                                 C.byref(cost), _ptr(grad)))
+        return cost.value, grad
+
+    def last_launch_count(self) -> int:
+        n = C.c_int(0)
+        self._check(self.L.bagel_last_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def profile(self, enable: bool):
+        self._check(self.L.bagel_profile(self.h, int(bool(enable))))
+
+    def profile_get(self) -> dict:
+        """{kernel class: (total device ms, launches)} since profile(True)."""
+        out = {}
+        for i, name in enumerate(PROFILE_CLASSES):
+            ms, n = C.c_double(0.0), C.c_longlong(0)
+            self._check(self.L.bagel_profile_get(self.h, i, C.byref(ms), C.byref(n)))
+            out[name] = (ms.value, n.value)
+        return out
+
+    # ------------------------------------------------------------ test exports
+    def gp_predict(self, xstar):
+        xs = _f32(xstar, self.dev)
+        M = xs.shape[0]
+        mean = torch.empty(M, self.p, device=self.dev)
+        var = torch.empty(M, self.p, device=self.dev)
+        dmean = torch.empty(M, self.p, self.d, device=self.dev)
+        dvar = torch.empty(M, self.p, self.d, device=self.dev)
+        self._check(self.L.bagel_gp_predict(self.h, _ptr(xs), M, _ptr(mean), _ptr(var), _ptr(dmean), _ptr(dvar)))
+        return mean, var, dmean, dvar
+
+    def rollout_trace(self, theta, x0, goals, T: int, seed: int, traj_offset: int = 0):
+        th, x0d, gd = _f32(theta, self.dev), _f32(x0, self.dev), _f32(goals, self.dev)
+        B = x0d.shape[0]
+        x = torch.empty(T + 1, B, self.p, device=self.dev)
+        mu = torch.empty(max(T, 1), B, self.p, device=self.dev)
+        var = torch.empty(max(T, 1), B, self.p, device=self.dev)
+        ret = torch.empty(B, device=self.dev)
+        self._check(self.L.bagel_rollout_trace(self.h, _ptr(th), _ptr(x0d), _ptr(gd), B, int(T), int(seed),
+                                               int(traj_offset), _ptr(x), _ptr(mu), _ptr(var), _ptr(ret)))
+        return dict(x=x, mu=mu[:T], var=var[:T], ret=ret)
+
+    def philox4x32_10(self, ctr, key):
+        c = torch.as_tensor(np.ascontiguousarray(ctr, dtype=np.uint32).view(np.int32)).to(self.dev)
+        n = c.numel() // 4
+        out = torch.empty_like(c)
+        k = (C.c_uint32 * 2)(*[int(v) for v in key])
+        self._check(self.L.bagel_philox4x32_10(self.h, _ptr(c), k, n, _ptr(out)))
+        return out.cpu().numpy().view(np.uint32).reshape(-1, 4)
+
+    def philox_normals(self, seed: int, traj_offset: int, B: int, T: int, p: int):
+        out = torch.empty(T, B, p, device=self.dev)
+        self._check(self.L.bagel_philox_normals(self.h, int(seed), int(traj_offset), B, T, p, _ptr(out)))
+        return out
+
+    def cache_rank(self) -> int:
+        k = C.c_int(0)
+        self._check(self.L.bagel_cache_rank(self.h, C.byref(k)))
+        return k.value
+
+    def cache_get(self, m: int):
+        k = self.cache_rank()
+        alpha = torch.empty(self.N, dtype=torch.float64, device=self.dev)
+        R = torch.empty(k, self.N, dtype=torch.float64, device=self.dev)
+        self._check(self.L.bagel_cache_get(self.h, int(m), _ptr(alpha), _ptr(R)))
+        return alpha, R
+
+    def cache_set(self, m: int, alpha, R):
+        a = torch.as_tensor(alpha, dtype=torch.float64).to(self.dev).contiguous()
+        r = torch.as_tensor(R, dtype=torch.float64).to(self.dev).contiguous()
+        self._check(self.L.bagel_cache_set(self.h, int(m), int(r.shape[0]), _ptr(a), _ptr(r)))
+
+
+def setup(wl, rank: int | None = None, device: int | None = None, build_cache: bool = True) -> Context:
+    """Context with the workload's GP, LOVE cache, policy and reward configured."""
+    ctx = Context(device)
+    ctx.gp_load(wl.X, wl.Y, wl.ell, wl.s, wl.noise)
+    if build_cache:
+        ctx.cache_seconds = ctx.love_cache_build(wl.rank if rank is None else rank)
+    ctx.policy_configure(wl.sizes)
+    ctx.reward_configure(wl.Q, wl.sigma_r)
+    return ctx

@@ -1,0 +1,157 @@
+// bagel_internal.h -- context layout and launcher prototypes shared by the
+// CUDA translation units of libbagel.so.  Not part of the ABI (see include/bagel.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#define BAGEL_MAX_P 4        // one Philox call per (b, t) carries the p <= 4 normals
+#define BAGEL_MAX_D 8        // d = p + q <= 8
+#define BAGEL_MAX_WIDTH 256  // widest MLP layer
+#define BAGEL_MAX_LAYERS 8
+#define BAGEL_MAX_RANK 768
+#define BAGEL_VAR_FLOOR 1e-12f  // S:252 clamp (reading R19)
+
+// sqrt(0.5 * log2(e)): x_hat = x * KAPPA / l so that exp(-1/2 sum (dx/l)^2) = exp2(-||x_hat - X_hat||^2)
+#define BAGEL_KAPPA 0.84932180028801907f
+
+struct PolicyDesc {
+  int n_layers;
+  int sizes[BAGEL_MAX_LAYERS + 1];
+  int w_off[BAGEL_MAX_LAYERS];  // offset of W_l in theta
+  int b_off[BAGEL_MAX_LAYERS];  // offset of b_l in theta
+  int phi_mode;                 // 0: [x, g]; 1: [x, g, g - x]
+  int n_params;
+  int max_width;
+  int act_total;                // sum of all layer widths (activations per row)
+};
+
+struct RewardDesc {
+  float Q[BAGEL_MAX_P];
+  float inv_two_sr2;  // 1 / (2 sigma_r^2)
+};
+
+// Problem geometry of one GP step, passed by value to kernels.
+struct GpDesc {
+  int N, d, p, k;
+  int C;     // 1 + d + k columns of V = [s alpha | s alpha o X | s R^T]
+  int Cld;   // leading dimension of V rows (C rounded up to the column tile)
+  float ell2inv[BAGEL_MAX_P][BAGEL_MAX_D];  // 1 / l_mc^2
+  float qscale[BAGEL_MAX_P][BAGEL_MAX_D];   // KAPPA / l_mc
+  float s[BAGEL_MAX_P];
+};
+
+struct Workspace {
+  int B = 0, T = 0;         // capacity
+  int S1 = 0, S2 = 0;       // N-splits of pass 1 / pass 2
+  float* xstar = nullptr;   // B x d
+  float* P1 = nullptr;      // S1 x p x B x Cld partial [mu | k a X | z]
+  float* Z = nullptr;       // p x B x k
+  float* P2 = nullptr;      // S2 x p x B x (1 + MAX_D) partial [sum w k | sum w k X_c]
+  float* mu = nullptr;      // p x B  (step moments)
+  float* var = nullptr;     // p x B
+  // tape (a8): x (T+1) x B x p, sig T x B x p (negative = clamped), Jmu / Jv T x B x p x d
+  float* tape_x = nullptr;
+  float* tape_sig = nullptr;
+  float* tape_jmu = nullptr;
+  float* tape_jv = nullptr;
+  double* G = nullptr;      // B returns
+  float* theta_part = nullptr;  // nblk x n_params reverse partials
+  int theta_part_cap = 0;
+  float* grad_tmp = nullptr;    // n_params (host-grad staging)
+  double* cost_dev = nullptr;   // 1
+  int* err_flag = nullptr;      // first (t * B + b) + 1 with a non-finite state, else 0
+  // host staging of [dev|host] inputs
+  float* stage = nullptr;
+  size_t stage_cap = 0;
+};
+
+struct bagel_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // GP data (gp_load)
+  int N = 0, d = 0, p = 0;
+  float* X = nullptr;   // N x d
+  float* Y = nullptr;   // N x p
+  std::vector<float> ell, s, noise;
+  // LOVE cache
+  int k = 0;
+  std::vector<int> cache_ok;
+  double* alpha64 = nullptr;  // p x N
+  double* R64 = nullptr;      // p x k x N
+  float* V = nullptr;         // p x N x Cld (fp32 packed hot-path operand)
+  float* Xs = nullptr;        // p x N x d   (X * KAPPA / l)
+  GpDesc gp{};
+  // policy / reward
+  bool policy_ok = false, reward_ok = false;
+  PolicyDesc pol{};
+  RewardDesc rw{};
+  Workspace ws;
+  int last_launches = 0;
+  int num_sms = 148;
+  // per-kernel-class event timing (bagel_profile)
+  struct ProfEvent {
+    cudaEvent_t a, b;
+    int cls;
+  };
+  bool prof_on = false;
+  std::vector<ProfEvent> prof_pending;
+  std::vector<cudaEvent_t> prof_pool;
+  double prof_ms[8] = {};
+  long long prof_n[8] = {};
+};
+
+// ----------------------------------------------------------------- launchers
+// Every launcher returns the number of kernels it enqueued (for gpu_launches).
+
+// cache_build.cu
+int cb_build_khat(const float* X, int N, int d, const float* ell_dev, double s, double noise,
+                  double* K, cudaStream_t st);
+// blocked Cholesky in place (lower); pivot_flag[0] = first failing pivot + 1 (0 if ok)
+int cb_cholesky(double* K, int N, int* pivot_flag, cudaStream_t st);
+// alpha = L^-T L^-1 y  (y float32 column, stride ystride)
+int cb_cholesky_solve(const double* L, int N, const float* y, int ystride, double* alpha,
+                      double* tmp, cudaStream_t st);
+// Lanczos pieces (fp64)
+int cb_symv(const double* K, int N, const double* q, double* v, cudaStream_t st);
+int cb_dot(const double* a, const double* b, int N, double* out, cudaStream_t st);
+int cb_gemv_t(const double* Q, int nq, int N, const double* v, double* c, cudaStream_t st);  // c = Q v
+int cb_gemv_sub(const double* Q, int nq, int N, const double* c, double* v, cudaStream_t st); // v -= Q^T c
+int cb_scale_copy(const double* v, double scale_inv, double* q, int N, cudaStream_t st);
+int cb_probe_from_y(const float* Y, int ystride, int N, double* v, cudaStream_t st);
+int cb_restart_vector(uint32_t restart_idx, int m, int N, double* v, cudaStream_t st);
+int cb_love_R(const double* Q, const double* ld, const double* le, int k, int N, double* R,
+              cudaStream_t st);
+int cb_pack(const float* X, const double* alpha, const double* R, int N, int d, int k, float s,
+            const float* qscale_host, int Cld, float* V, float* Xs, cudaStream_t st);
+
+// gp_step.cu
+int gs_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);
+int gs_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out,
+               cudaStream_t st);
+int gs_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);
+int gs_finish_predict(const bagel_ctx* c, const float* xstar, int B, float* mean, float* var,
+                      float* dmean, float* dvar, cudaStream_t st);
+void gs_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2);
+
+// rollout.cu
+int ro_init(const bagel_ctx* c, const float* theta, const float* x0, const float* goals, int B,
+            cudaStream_t st);
+int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals, int B, int t,
+                     int T, uint64_t seed, long long traj_offset, bool policy_next,
+                     float* trace_mu, float* trace_var, cudaStream_t st);
+int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B, int T,
+               uint64_t seed, long long traj_offset, long long B_global, int* nblk_out,
+               cudaStream_t st);
+int ro_reduce(const bagel_ctx* c, int nblk, int B, long long B_global, float* grad,
+              cudaStream_t st);
+int ro_copy_returns(const bagel_ctx* c, int B, float* ret, cudaStream_t st);
+int ro_philox_raw(const uint32_t* ctr, uint32_t k0, uint32_t k1, int n, uint32_t* out,
+                  cudaStream_t st);
+int ro_philox_normals(uint64_t seed, long long traj_offset, int B, int T, int p, float* out,
+                      cudaStream_t st);
+int ro_reverse_block_rows();

@@ -1,0 +1,81 @@
+"""No-GPU checks of the boundary: libbagel.so loads, exports every symbol that
+include/bagel.h declares, the binding exposes the same names, and the product
+package never imports the oracle."""
+import ast
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "bagel.h")
+PKG = os.path.join(ROOT, "paper_2202_13638_b200")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2202_13638_b200 import build
+
+    return build.build_library()
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ("gp_load", "love_cache_build", "rollout_cost_and_grad", "policy_configure", "reward_configure",
+              "bagel_create", "bagel_destroy", "bagel_last_error"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", libpath], text=True)
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, missing
+
+
+def test_library_loads_and_binding_names_match(libpath):
+    from paper_2202_13638_b200 import bagel
+
+    L = bagel.lib()
+    for n in declared_functions():
+        assert hasattr(L, n), n
+    assert sorted(bagel.EXPORTS) == sorted(declared_functions())
+
+
+def test_library_is_sm100a_and_uses_no_cuda_fallback(libpath):
+    out = subprocess.check_output(["cuobjdump", "--list-elf", libpath], text=True)
+    assert "sm_100a" in out
+
+
+def test_product_never_imports_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if not f.endswith(".py"):
+                continue
+            tree = ast.parse(open(os.path.join(dirpath, f)).read())
+            for node in ast.walk(tree):
+                if isinstance(node, ast.Import):
+                    assert all(not a.name.startswith("oracle") for a in node.names), f
+                if isinstance(node, ast.ImportFrom):
+                    assert not (node.module or "").startswith("oracle"), f
+    for dirpath, _, files in os.walk(os.path.join(PKG, "csrc")):
+        for f in files:
+            src = open(os.path.join(dirpath, f)).read()
+            assert "bagel_oracle" not in src and "orc_" not in src, f
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    from paper_2202_13638_b200 import bagel
+
+    monkeypatch.setattr(bagel, "_lib", None)
+    monkeypatch.setattr(bagel, "LIB", str(tmp_path / "nope.so"))
+    with pytest.raises(RuntimeError, match="missing"):
+        bagel.lib()

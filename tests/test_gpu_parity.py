@@ -1,0 +1,344 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle.
+
+Tolerances (the north star's numbers read so that an
+fp32-accurate implementation can meet them):
+  mean      |d mu| <= 1e-4 |mu| + 32 u sum_n |k_n alpha_n|
+  variance  |d v|  <= 1e-4 |v|  + 32 u 2 sum_j |z_j| sum_n |R_jn k_n|
+  Jacobians |d J|  <= 1e-3 |J|  + 64 u (conditioning term) (|x*_c| + max|X_c|) / l_c^2
+  cost      |d L|  <= 1e-3 |L|;  gradient ||d g|| <= 1e-3 ||g||
+  eps       raw Philox u32 bit-identical; eps within 1e-6 (1 + |eps|)
+with u = 2^-24 (fp32 path)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+U32 = 2.0 ** -24
+
+
+@pytest.fixture(scope="module")
+def bagel():
+    from paper_2202_13638_b200 import bagel as b
+
+    assert torch.cuda.is_available()
+    b.lib()
+    return b
+
+
+def _ctx(bagel, wl, build_cache=True):
+    return bagel.setup(wl, device=0, build_cache=build_cache)
+
+
+def _inject(ctx, mdl):
+    for m in range(mdl.p):
+        ctx.cache_set(m, mdl.alpha[m], mdl.R[m])
+
+
+@pytest.fixture(scope="module")
+def small(bagel):
+    """Ragged sizes: N=700 (not a multiple of the 32/64 N tiles), k=100, C=104 (2 column tiles)."""
+    wl = W.make_workload(plant="boom", N=700, rank=100, hidden=(32, 32), B=150, T=10)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    return wl, mdl
+
+
+# ------------------------------------------------------------------ Philox
+def test_philox_kat_and_random_counters_bitexact(bagel):
+    from conftest import read_golden
+
+    ctx = bagel.Context(0)
+    for row in read_golden("philox_kat.txt"):
+        v = [int(x, 16) for x in row.split()]
+        out = ctx.philox4x32_10(np.array(v[0:4], dtype=np.uint32), v[4:6])
+        assert list(out[0]) == v[6:10]
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2 ** 32, size=(4096, 4), dtype=np.uint64).astype(np.uint32)
+    key = [0x5EED0001, 0x12345678]
+    out = ctx.philox4x32_10(ctr, key)
+    for i in range(0, 4096, 97):
+        assert list(out[i]) == list(O.philox4x32_10(ctr[i], key))
+
+
+def test_rollout_normals_match_oracle(bagel):
+    ctx = bagel.Context(0)
+    seed, off, B, T, p = 0x5EED0007, 1000, 37, 5, 4
+    eps = ctx.philox_normals(seed, off, B, T, p).cpu().numpy()
+    for t in range(T):
+        for b in range(0, B, 3):
+            for m in range(p):
+                ref = O.rollout_eps(seed, off + b, t, m)
+                assert abs(eps[t, b, m] - ref) <= 1e-6 * (1 + abs(ref))
+
+
+# ------------------------------------------------------------------ GP query (a2-a5)
+def _check_predict(wl, mdl, mean, var, dmean, dvar, xs):
+    om, ov, ojm, ojv, mb, vb = mdl.predict(xs)
+    mean, var, dmean, dvar = [t.double().cpu().numpy() for t in (mean, var, dmean, dvar)]
+    tol_m = 1e-4 * np.abs(om) + 32 * U32 * mb
+    tol_v = 1e-4 * np.abs(ov) + 32 * U32 * vb
+    em = np.abs(mean - om)
+    ev = np.abs(var - ov)
+    assert np.all(em <= tol_m), f"mean: worst ratio {np.max(em / tol_m):.3g}"
+    assert np.all(ev <= tol_v), f"var: worst ratio {np.max(ev / tol_v):.3g}"
+    xmax = np.abs(wl.X).max(axis=0).astype(np.float64)
+    il2 = 1.0 / wl.ell.astype(np.float64) ** 2  # p x d
+    geo = (np.abs(xs)[:, None, :] + xmax[None, None, :]) * il2[None, :, :]
+    tol_jm = 1e-3 * np.abs(ojm) + 64 * U32 * mb[:, :, None] * geo
+    tol_jv = 1e-3 * np.abs(ojv) + 64 * U32 * vb[:, :, None] * geo
+    ejm, ejv = np.abs(dmean - ojm), np.abs(dvar - ojv)
+    assert np.all(ejm <= tol_jm), f"dmean: worst ratio {np.max(ejm / tol_jm):.3g}"
+    assert np.all(ejv <= tol_jv), f"dvar: worst ratio {np.max(ejv / tol_jv):.3g}"
+    return dict(mean=np.max(em / tol_m), var=np.max(ev / tol_v), dmean=np.max(ejm / tol_jm),
+                dvar=np.max(ejv / tol_jv))
+
+
+def test_gp_predict_with_oracle_cache(bagel, small):
+    wl, mdl = small
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    rng = np.random.default_rng(1)
+    xs = np.concatenate([wl.X[rng.integers(0, wl.N, 150)] + rng.normal(0, 0.05, (150, 3)),
+                         rng.uniform(-2.5, 2.5, (150, 3))]).astype(np.float32)  # M = 300 (ragged)
+    out = ctx.gp_predict(torch.from_numpy(xs).cuda())
+    ratios = _check_predict(wl, mdl, *out, xs.astype(np.float64))
+    print("worst error / tolerance:", ratios)
+
+
+def test_gp_predict_single_point_and_far_field(bagel, small):
+    wl, mdl = small
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    xs = np.array([[50.0, -50.0, 50.0]], dtype=np.float32)  # far field: mean 0, var s
+    mean, var, dm, dv = ctx.gp_predict(torch.from_numpy(xs).cuda())
+    assert np.all(np.abs(mean.cpu().numpy()) < 1e-12)
+    assert np.allclose(var.cpu().numpy()[0], wl.s, rtol=1e-6)
+
+
+# ------------------------------------------------------------------ cache build (a0)
+def test_love_cache_build_matches_oracle(bagel, small):
+    wl, mdl = small
+    ctx = _ctx(bagel, wl)
+    assert ctx.cache_rank() == wl.rank
+    xs = np.random.default_rng(2).uniform(-2, 2, (64, 3))
+    for m in range(wl.p):
+        a, R = [t.cpu().numpy() for t in ctx.cache_get(m)]
+        # alpha: exact solve, compared through the mean it produces (cancellation-aware)
+        kx = O.kernel_matrix(xs, wl.X, wl.ell[m], wl.s[m])
+        mu_g, mu_o = kx @ a, kx @ mdl.alpha[m]
+        assert np.all(np.abs(mu_g - mu_o) <= 1e-9 * np.abs(kx) @ np.abs(mdl.alpha[m]))
+        # R: compared through the LOVE variance (R unique up to Lanczos roundoff, reading R26)
+        vg = wl.s[m] - np.sum((kx @ R.T) ** 2, axis=1)
+        vo = wl.s[m] - np.sum((kx @ mdl.R[m].T) ** 2, axis=1)
+        assert np.max(np.abs(vg - vo)) <= 1e-8 * wl.s[m]
+
+
+def test_love_cache_full_rank_is_exact_on_gpu(bagel):
+    wl = W.make_workload(plant="boom", N=150, rank=150, hidden=(8,), B=4, T=2)
+    ctx = _ctx(bagel, wl)
+    xs = np.random.default_rng(3).uniform(-2, 2, (40, 3))
+    for m in range(wl.p):
+        a, R = [t.cpu().numpy() for t in ctx.cache_get(m)]
+        alpha, L = O.exact_fit(wl.X, wl.Y[:, m], wl.ell[m], wl.s[m], wl.noise[m])
+        _, ev = O.exact_predict(wl.X, wl.ell[m], wl.s[m], L, alpha, xs)
+        kx = O.kernel_matrix(xs, wl.X, wl.ell[m], wl.s[m])
+        vl = wl.s[m] - np.sum((kx @ R.T) ** 2, axis=1)
+        assert np.max(np.abs(vl - ev)) < 1e-9 * wl.s[m]
+
+
+# ------------------------------------------------------------------ rollout (a1-a10)
+def _rollout_gpu(ctx, wl, goals, seed, B=None, off=0, B_global=None, T=None):
+    B = wl.B if B is None else B
+    th = torch.from_numpy(wl.theta).cuda()
+    x0 = torch.from_numpy(wl.x0[off:off + B]).cuda()
+    g = torch.from_numpy(goals[off:off + B]).cuda()
+    cost, grad = ctx.rollout_cost_and_grad(th, x0, g, wl.T if T is None else T, seed, traj_offset=off,
+                                           B_global=B if B_global is None else B_global)
+    return cost, grad.double().cpu().numpy()
+
+
+def _rollout_oracle(mdl, wl, goals, seed, B=None, off=0, B_global=None, T=None):
+    B = wl.B if B is None else B
+    phi = "xg" if wl.sizes[0] == 2 * wl.p else "xgd"
+    return O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[off:off + B], goals[off:off + B],
+                     wl.T if T is None else T, seed, traj_offset=off, B_global=B if B_global is None else B_global)
+
+
+def _assert_cost_grad(cost, grad, ref, tag=""):
+    rel_c = abs(cost - ref["cost"]) / abs(ref["cost"])
+    rel_g = np.linalg.norm(grad - ref["grad"]) / np.linalg.norm(ref["grad"])
+    print(f"{tag} cost rel {rel_c:.2e}  grad rel L2 {rel_g:.2e}")
+    assert rel_c <= 1e-3 and rel_g <= 1e-3, (rel_c, rel_g)
+
+
+def test_rollout_cost_grad_oracle_cache(bagel, small):
+    wl, mdl = small
+    goals = (wl.x0 + np.array([0.5, -0.3], dtype=np.float32)).astype(np.float32)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    seed = W.rollout_seed(3)
+    cost, grad = _rollout_gpu(ctx, wl, goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "small/oracle-cache")
+
+
+def test_rollout_cost_grad_gpu_cache(bagel, small):
+    wl, mdl = small
+    goals = (wl.x0 + np.array([0.5, -0.3], dtype=np.float32)).astype(np.float32)
+    ctx = _ctx(bagel, wl)
+    seed = W.rollout_seed(4)
+    cost, grad = _rollout_gpu(ctx, wl, goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "small/gpu-cache")
+
+
+def test_rollout_trace_matches_oracle(bagel, small):
+    wl, mdl = small
+    goals = wl.goals
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    seed = W.rollout_seed(5)
+    tr = ctx.rollout_trace(wl.theta, wl.x0, goals, wl.T, seed)
+    ref = O.rollout(mdl, wl.sizes, "xg", wl.theta, wl.Q, wl.sigma_r, wl.x0, goals, wl.T, seed, trace=True)
+    x = tr["x"].double().cpu().numpy()
+    assert np.max(np.abs(x - ref["x"])) < 1e-3
+    ret = tr["ret"].double().cpu().numpy()
+    assert np.allclose(ret, ref["ret"], rtol=1e-4, atol=1e-6)
+
+
+def test_c1_config_parity(bagel):
+    wl = W.config("C1")
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl)
+    for goals in (wl.goals, (wl.x0 + 0.6).astype(np.float32)):
+        seed = W.rollout_seed(0)
+        cost, grad = _rollout_gpu(ctx, wl, goals, seed)
+        _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "C1")
+
+
+def test_horizon_zero_and_single_trajectory(bagel, small):
+    wl, mdl = small
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    cost, grad = _rollout_gpu(ctx, wl, wl.goals, 1, T=0)
+    ref = _rollout_oracle(mdl, wl, wl.goals, 1, T=0)
+    assert cost == pytest.approx(ref["cost"], rel=1e-6)
+    assert np.all(grad == 0.0)
+    goals = (wl.x0 + 0.4).astype(np.float32)
+    cost, grad = _rollout_gpu(ctx, wl, goals, 9, B=1, off=77, B_global=150)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, 9, B=1, off=77, B_global=150), "B=1")
+
+
+def test_determinism_and_host_buffers(bagel, small):
+    wl, mdl = small
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    seed = W.rollout_seed(6)
+    c1, g1 = _rollout_gpu(ctx, wl, wl.goals, seed)
+    c2, g2 = _rollout_gpu(ctx, wl, wl.goals, seed)
+    assert c1 == c2 and np.array_equal(g1, g2)
+    # host (pageable numpy / pinned torch) buffers through the same C-ABI call
+    grad_host = torch.empty(ctx.n_params, dtype=torch.float32).pin_memory()
+    c3, g3 = ctx.rollout_cost_and_grad(wl.theta, wl.x0, wl.goals, wl.T, seed, grad=grad_host)
+    assert c3 == c1 and np.array_equal(g3.double().numpy(), g1)
+
+
+def test_shards_sum_to_full_batch(bagel, small):
+    wl, mdl = small
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    seed = W.rollout_seed(7)
+    c, g = _rollout_gpu(ctx, wl, wl.goals, seed)
+    cs, gs = 0.0, np.zeros_like(g)
+    for off, n in ((0, 50), (50, 64), (114, 36)):
+        ci, gi = _rollout_gpu(ctx, wl, wl.goals, seed, B=n, off=off, B_global=wl.B)
+        cs += ci
+        gs += gi
+    assert cs == pytest.approx(c, rel=1e-6)
+    assert np.linalg.norm(gs - g) <= 1e-5 * np.linalg.norm(g)
+
+
+def test_errors_are_reported(bagel, small):
+    wl, mdl = small
+    ctx = bagel.Context(0)
+    with pytest.raises(bagel.BagelError) as e:
+        ctx.love_cache_build(10)
+    assert e.value.code == bagel.E_STATE
+    ctx = _ctx(bagel, wl, build_cache=False)
+    with pytest.raises(bagel.BagelError) as e:
+        ctx.rollout_cost_and_grad(wl.theta, wl.x0, wl.goals, 3, 1)
+    assert e.value.code == bagel.E_STATE
+    _inject(ctx, mdl)
+    x0 = wl.x0.copy()
+    x0[5, 1] = np.nan
+    with pytest.raises(bagel.BagelError) as e:
+        ctx.rollout_cost_and_grad(wl.theta, x0, wl.goals, 3, 1)
+    assert e.value.code == bagel.E_NUMERIC and "step 0, row 5" in str(e.value)
+    with pytest.raises(bagel.BagelError) as e:
+        ctx.policy_configure((5, 8, 1))
+    assert e.value.code == bagel.E_ARG
+    with pytest.raises(bagel.BagelError) as e:
+        ctx.love_cache_build(wl.N + 1)
+    assert e.value.code == bagel.E_ARG
+
+
+# ------------------------------------------------------------------ full-size C2
+@pytest.fixture(scope="module")
+def c2(bagel):
+    wl = W.config("C2")
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl)
+    return wl, mdl, ctx
+
+
+def test_c2_cache_build_matches_oracle(c2):
+    wl, mdl, ctx = c2
+    xs = np.random.default_rng(4).uniform(-2, 2, (64, 3))
+    for m in range(wl.p):
+        a, R = [t.cpu().numpy() for t in ctx.cache_get(m)]
+        kx = O.kernel_matrix(xs, wl.X, wl.ell[m], wl.s[m])
+        assert np.all(np.abs(kx @ a - kx @ mdl.alpha[m]) <= 1e-8 * np.abs(kx) @ np.abs(mdl.alpha[m]))
+        vg = wl.s[m] - np.sum((kx @ R.T) ** 2, axis=1)
+        vo = wl.s[m] - np.sum((kx @ mdl.R[m].T) ** 2, axis=1)
+        assert np.max(np.abs(vg - vo)) <= 1e-7 * wl.s[m]
+
+
+def test_c2_predict_full_size(c2):
+    wl, mdl, ctx = c2
+    rng = np.random.default_rng(5)
+    xs = np.concatenate([wl.X[rng.integers(0, wl.N, 200)], rng.uniform(-2, 2, (56, 3))]).astype(np.float32)
+    out = ctx.gp_predict(torch.from_numpy(xs).cuda())
+    # compare against the oracle evaluated with the GPU-independent oracle cache
+    ratios = _check_predict(wl, mdl, *out, xs.astype(np.float64))
+    print("C2 worst error / tolerance:", ratios)
+
+
+def test_c2_trajectory_subset_full_horizon(c2):
+    """Full N, k, T; a subset of 16 trajectories (global ids 500..515, exact by Philox indexing)."""
+    wl, mdl, ctx = c2
+    seed = W.rollout_seed(0)
+    cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed, B=16, off=500, B_global=wl.B)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed, B=16, off=500, B_global=wl.B),
+                      "C2 subset")
+
+
+def test_c2_full_batch_sampled_rows(c2):
+    """Bench launch configuration (B = 1024, T = 100): sampled per-trajectory returns vs the oracle,
+    and the full-batch gradient equals the sum of its shards (any size property)."""
+    wl, mdl, ctx = c2
+    seed = W.rollout_seed(1)
+    tr = ctx.rollout_trace(wl.theta, wl.x0, wl.goals, wl.T, seed)
+    ret = tr["ret"].double().cpu().numpy()
+    rows = [0, 1, 511, 777, 1023]
+    for b in rows:
+        ref = _rollout_oracle(mdl, wl, wl.goals, seed, B=1, off=b, B_global=1)
+        assert abs(ret[b] - ref["ret"][0]) <= 1e-3 * abs(ref["ret"][0])
+    c, g = _rollout_gpu(ctx, wl, wl.goals, seed)
+    assert c == pytest.approx(-ret.sum() / wl.B, rel=1e-6)
+    cs, gs = 0.0, np.zeros_like(g)
+    for off in range(0, wl.B, 256):
+        ci, gi = _rollout_gpu(ctx, wl, wl.goals, seed, B=256, off=off, B_global=wl.B)
+        cs += ci
+        gs += gi
+    assert cs == pytest.approx(c, rel=1e-6)
+    assert np.linalg.norm(gs - g) <= 1e-5 * np.linalg.norm(g)

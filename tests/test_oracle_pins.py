@@ -22,13 +22,13 @@ def test_philox_kat():
 
 
 def test_box_muller_convention_and_statistics():
-    # u = ((o >> 8) + 0.5) 2^-24 lies strictly in (0,1) for the extreme words.
+    # u = ((o >> 9) + 0.5) 2^-23 lies strictly in (0,1) for the extreme words.
     e = O.box_muller4([0, 0xFFFFFFFF, 0xFFFFFFFF, 0])
     assert np.all(np.isfinite(e))
-    bound = math.sqrt(-2.0 * math.log(0.5 * 2.0 ** -24))  # max |eps| ~ 5.89
+    bound = math.sqrt(-2.0 * math.log(0.5 * 2.0 ** -23))  # max |eps| ~ 5.77
     assert np.all(np.abs(e) <= bound + 1e-12)
-    # u0 = (0 + .5) 2^-24, u1 -> (2^24 - .5) 2^-24: eps0 = r cos(2 pi u1) ~ r, eps1 ~ 0-
-    assert e[0] == pytest.approx(bound * math.cos(2 * math.pi * (2 ** 24 - 0.5) / 2 ** 24), rel=1e-12)
+    # u0 = (0 + .5) 2^-23, u1 = (2^23 - .5) 2^-23: eps0 = r cos(2 pi u1) ~ r, eps1 ~ 0-
+    assert e[0] == pytest.approx(bound * math.cos(2 * math.pi * (2 ** 23 - 0.5) / 2 ** 23), rel=1e-12)
     # moments of 4 * 50_000 draws (3-sigma bounds)
     n = 50_000
     draws = np.array([O.rollout_eps(1234, b, 0, m) for b in range(n // 4) for m in range(4)])

@@ -51,7 +51,7 @@ def test_scalar_rollout_closed_form():
     G = math.exp(-0.5 * 10.0 * (x - 0.4) ** 2)
     for t in range(T):
         o = O.philox4x32_10([b, t, 0, 0], key)
-        u0, u1 = [((int(v) >> 8) + 0.5) * 2.0 ** -24 for v in o[:2]]
+        u0, u1 = [((int(v) >> 9) + 0.5) * 2.0 ** -23 for v in o[:2]]
         eps = math.sqrt(-2.0 * math.log(u0)) * math.cos(2.0 * math.pi * u1)
         k = s * math.exp(-0.5 * (((x - 0.3) / 0.8) ** 2 + ((0.0 + 0.2) / 0.6) ** 2))
         mu = k * 0.05 / (s + sn2)
