@@ -188,6 +188,22 @@ int bagel_cache_get(bagel_ctx* ctx, int m, double* alpha, double* R);
  * Errors: E_STATE without gp_load; E_ARG for m out of range, rank change. */
 int bagel_cache_set(bagel_ctx* ctx, int m, int rank, const double* alpha, const double* R);
 
+/* GP-step implementation selector (bench / A-B parity tests):
+ *   1 (default) tcgen05 tensor-core kernels (csrc/gp_step_tc.cu),
+ *   0 the v0 CUDA-core FFMA kernels (csrc/gp_step.cu), kept as a reference.
+ * bagel_get_gp_kernel reports the path the next call will take (1 only if the
+ * problem fits the tensor-core kernels' shared-memory budget).  Errors: E_ARG. */
+int bagel_set_gp_kernel(bagel_ctx* ctx, int version);
+int bagel_get_gp_kernel(const bagel_ctx* ctx, int* version);
+
+/* Tensor-core probe: one CTA computes D[128 x N] = A[128 x K] . B[N x K]^T with
+ * fp16 operands (tcgen05.mma kind::f16, fp32 accumulate in TMEM).  A and B are
+ * [dev] fp16 arrays in the canonical no-swizzle K-major packing of
+ * csrc/tc.cuh (element (r, k) at ((r/8)(K/8) + k/8) 64 + (r%8) 8 + k%8);
+ * D [dev] row-major 128 x N float32.  N in {16, 32, ..., 256}, K in {16, 32, ...},
+ * (128 + N) K 2 bytes <= 200 KB.  Errors: E_ARG, E_CUDA. */
+int bagel_tc_selftest(bagel_ctx* ctx, const void* A, const void* B, int N, int K, float* D);
+
 #ifdef __cplusplus
 }
 #endif

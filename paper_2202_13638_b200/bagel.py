@@ -59,6 +59,9 @@ def lib() -> C.CDLL:
             L.bagel_cache_set.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
             L.bagel_profile.argtypes = [_vp, C.c_int]
             L.bagel_profile_get.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
+            L.bagel_tc_selftest.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, _vp]
+            L.bagel_set_gp_kernel.argtypes = [_vp, C.c_int]
+            L.bagel_get_gp_kernel.argtypes = [_vp, C.POINTER(C.c_int)]
             _lib = L
     return _lib
 
@@ -66,7 +69,8 @@ def lib() -> C.CDLL:
 EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_error", "gp_load", "love_cache_build",
            "policy_configure", "reward_configure", "rollout_cost_and_grad", "bagel_last_launch_count",
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
-           "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get"]
+           "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
+           "bagel_set_gp_kernel", "bagel_get_gp_kernel"]
 
 PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce"]
 
@@ -215,6 +219,20 @@ class Context:
         out = torch.empty(T, B, p, device=self.dev)
         self._check(self.L.bagel_philox_normals(self.h, int(seed), int(traj_offset), B, T, p, _ptr(out)))
         return out
+
+    def set_gp_kernel(self, version: int):
+        """1: tcgen05 tensor-core GP step (default); 0: v0 CUDA-core FFMA reference."""
+        self._check(self.L.bagel_set_gp_kernel(self.h, int(version)))
+
+    def gp_kernel(self) -> int:
+        v = C.c_int(0)
+        self._check(self.L.bagel_get_gp_kernel(self.h, C.byref(v)))
+        return v.value
+
+    def tc_selftest(self, A_packed: torch.Tensor, B_packed: torch.Tensor, N: int, K: int) -> torch.Tensor:
+        D = torch.empty(128, N, dtype=torch.float32, device=self.dev)
+        self._check(self.L.bagel_tc_selftest(self.h, _ptr(A_packed), _ptr(B_packed), int(N), int(K), _ptr(D)))
+        return D
 
     def cache_rank(self) -> int:
         k = C.c_int(0)

@@ -19,6 +19,7 @@
 size_t gs_pass2_smem(int k, int d);
 size_t ro_reverse_smem(const PolicyDesc& P);
 size_t ro_epilogue_smem(const PolicyDesc& P);
+int tc_selftest_launch(const void* A, const void* B, int N, int K, float* D, cudaStream_t st);
 
 namespace {
 
@@ -131,6 +132,11 @@ void free_cache(bagel_ctx* c) {
   dev_free(c->R64);
   dev_free(c->V);
   dev_free(c->Xs);
+  dev_free(c->tcs.tiles1);
+  dev_free(c->tcs.tiles2);
+  dev_free(c->tcs.colscale);
+  dev_free(c->tcs.colscale_inv);
+  dev_free(c->tcs.qscale);
   c->k = 0;
   c->cache_ok.assign(c->p, 0);
 }
@@ -140,6 +146,7 @@ void free_workspace(bagel_ctx* c) {
   dev_free(w.xstar); dev_free(w.P1); dev_free(w.Z); dev_free(w.P2); dev_free(w.mu); dev_free(w.var);
   dev_free(w.tape_x); dev_free(w.tape_sig); dev_free(w.tape_jmu); dev_free(w.tape_jv); dev_free(w.G);
   dev_free(w.theta_part); dev_free(w.grad_tmp); dev_free(w.cost_dev); dev_free(w.err_flag);
+  dev_free(c->tcs.P1z); dev_free(c->tcs.P1h); dev_free(c->tcs.Zp); dev_free(c->tcs.zrow_inv);
   w.B = w.T = 0;
   w.S1 = w.S2 = 0;
   w.theta_part_cap = 0;
@@ -171,7 +178,11 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
   Workspace& w = c->ws;
   int S1, S2;
   gs_choose_splits(c, B, &S1, &S2);
-  const bool same = w.B >= B && w.T >= T && w.B > 0 && w.S1 == S1 && w.S2 == S2 && w.B == B;
+  int S1t = 0, S2t = 0, tps1 = 0, tps2 = 0;
+  const bool tc = tc_supported(c);
+  if (tc) tc_choose_splits(c, B, &S1t, &S2t, &tps1, &tps2);
+  const bool same = w.B >= B && w.T >= T && w.B > 0 && w.S1 == S1 && w.S2 == S2 && w.B == B && w.S1tc == S1t &&
+                    w.S2tc == S2t;
   const int nblk = (B + ro_reverse_block_rows() - 1) / ro_reverse_block_rows();
   if (!same) {
     free_workspace(c);
@@ -180,7 +191,15 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
     dev_alloc(c, w.xstar, Bs * d);
     dev_alloc(c, w.P1, (size_t)S1 * p * Bs * c->gp.Cld);
     dev_alloc(c, w.Z, (size_t)p * Bs * c->gp.k);
-    dev_alloc(c, w.P2, (size_t)S2 * p * Bs * (1 + BAGEL_MAX_D));
+    const size_t s2max = std::max((size_t)S2, (size_t)S2t * (tc ? tc_njt(c) : 1));
+    dev_alloc(c, w.P2, s2max * p * Bs * (1 + BAGEL_MAX_D));
+    if (tc) {
+      dev_alloc(c, c->tcs.P1z, tc_p1z_floats(c, B, S1t));
+      dev_alloc(c, c->tcs.P1h, (size_t)S1t * p * Bs * (1 + d));
+      dev_alloc(c, c->tcs.Zp, tc_zp_bytes(c, B));
+      CK(cudaMemsetAsync(c->tcs.Zp, 0, tc_zp_bytes(c, B), c->stream));  // padding rows / j stay zero
+      dev_alloc(c, c->tcs.zrow_inv, (size_t)p * Bs);
+    }
     dev_alloc(c, w.mu, (size_t)p * Bs);
     dev_alloc(c, w.var, (size_t)p * Bs);
     dev_alloc(c, w.tape_x, (Ts + 1) * Bs * p);
@@ -194,6 +213,10 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
     w.T = std::max(T, 1);
     w.S1 = S1;
     w.S2 = S2;
+    w.S1tc = S1t;
+    w.S2tc = S2t;
+    w.tps1 = tps1;
+    w.tps2 = tps2;
   }
   if (c->policy_ok) {
     const int need = nblk * c->pol.n_params;
@@ -265,6 +288,8 @@ void prof_drain(bagel_ctx* c) {
   c->prof_pending.clear();
 }
 
+bool use_tc(const bagel_ctx* c) { return c->gp_kernel == 1 && tc_supported(c); }
+
 // Forward rollout (shared by rollout_cost_and_grad and bagel_rollout_trace).
 int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goals, int B, int T,
             uint64_t seed, long long traj_offset, float* trace_mu, float* trace_var) {
@@ -274,12 +299,16 @@ int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goal
   int launches = 0;
   CK(cudaMemsetAsync(w.err_flag, 0x7f, sizeof(int), st));
   launches += timed(c, PC_INIT, [&] { return ro_init(c, theta, x0, goals, B, st); });
+  const bool tc = use_tc(c);
+  w.S2eff = tc ? w.S2tc * tc_njt(c) : w.S2;
   for (int t = 0; t < T; ++t) {
-    launches += timed(c, PC_PASS1, [&] { return gs_pass1(c, w.xstar, B, st); });
+    launches += timed(c, PC_PASS1, [&] { return tc ? tc_pass1(c, w.xstar, B, st) : gs_pass1(c, w.xstar, B, st); });
     launches += timed(c, PC_REDUCE1, [&] {
-      return gs_reduce1(c, w.xstar, B, w.tape_jmu + (size_t)t * B * p * d, w.tape_sig + (size_t)t * B * p, st);
+      float* jm = w.tape_jmu + (size_t)t * B * p * d;
+      float* sg = w.tape_sig + (size_t)t * B * p;
+      return tc ? tc_reduce1(c, w.xstar, B, jm, sg, st) : gs_reduce1(c, w.xstar, B, jm, sg, st);
     });
-    launches += timed(c, PC_PASS2, [&] { return gs_pass2(c, w.xstar, B, st); });
+    launches += timed(c, PC_PASS2, [&] { return tc ? tc_pass2(c, w.xstar, B, st) : gs_pass2(c, w.xstar, B, st); });
     launches += timed(c, PC_EPI, [&] {
       return ro_step_epilogue(c, theta, goals, B, t, T, seed, traj_offset, t + 1 < T,
                               trace_mu ? trace_mu + (size_t)t * B * p : nullptr,
@@ -406,6 +435,15 @@ void alloc_cache(bagel_ctx* c, int k) {
   dev_alloc(c, c->V, (size_t)c->p * c->N * c->gp.Cld);
   dev_alloc(c, c->Xs, (size_t)c->p * c->N * c->d);
   c->k = k;
+  if (tc_supported(c)) {
+    c->tcs.t1_stride = tc_tiles1_bytes(c);
+    c->tcs.t2_stride = tc_tiles2_bytes(c);
+    dev_alloc(c, c->tcs.tiles1, (size_t)c->p * c->tcs.t1_stride);
+    dev_alloc(c, c->tcs.tiles2, (size_t)c->p * c->tcs.t2_stride);
+    dev_alloc(c, c->tcs.colscale, (size_t)c->p * k);
+    dev_alloc(c, c->tcs.colscale_inv, (size_t)c->p * k);
+    dev_alloc(c, c->tcs.qscale, (size_t)c->p * BAGEL_MAX_D);
+  }
   c->cache_ok.assign(c->p, 0);
 }
 
@@ -413,6 +451,7 @@ void pack_output(bagel_ctx* c, int m) {
   cb_pack(c->X, c->alpha64 + (size_t)m * c->N, c->R64 + (size_t)m * c->k * c->N, c->N, c->d, c->k, c->s[m],
           c->gp.qscale[m], c->gp.Cld, c->V + (size_t)m * c->N * c->gp.Cld, c->Xs + (size_t)m * c->N * c->d,
           c->stream);
+  if (tc_supported(c)) tc_pack(c, m, c->stream);
   CK(cudaGetLastError());
 }
 
@@ -632,10 +671,12 @@ extern "C" int bagel_gp_predict(bagel_ctx* c, const float* xstar, int M, float* 
     ensure_workspace(c, M, 1);
     cudaStream_t st = c->stream;
     float* jmu = dmean ? dmean : c->ws.tape_jmu;
+    const bool tc = use_tc(c);
+    c->ws.S2eff = tc ? c->ws.S2tc * tc_njt(c) : c->ws.S2;
     int n = 0;
-    n += gs_pass1(c, xstar, M, st);
-    n += gs_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st);
-    n += gs_pass2(c, xstar, M, st);
+    n += tc ? tc_pass1(c, xstar, M, st) : gs_pass1(c, xstar, M, st);
+    n += tc ? tc_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st) : gs_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st);
+    n += tc ? tc_pass2(c, xstar, M, st) : gs_pass2(c, xstar, M, st);
     n += gs_finish_predict(c, xstar, M, mean, var, dmean, dvar, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
@@ -738,4 +779,28 @@ extern "C" int bagel_profile_get(bagel_ctx* c, int kernel, double* total_ms, lon
     *total_ms = c->prof_ms[kernel];
     *launches = c->prof_n[kernel];
   });
+}
+
+extern "C" int bagel_tc_selftest(bagel_ctx* c, const void* A, const void* B, int N, int K, float* D) {
+  return guarded(c, [&] {
+    REQUIRE(A && B && D && N >= 16 && N <= 256 && N % 16 == 0 && K >= 16 && K % 16 == 0 &&
+                (size_t)(128 + N) * K * 2 <= 200 * 1024,
+            BAGEL_E_ARG, "bagel_tc_selftest: bad shape N=%d K=%d", N, K);
+    tc_selftest_launch(A, B, N, K, D, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+extern "C" int bagel_set_gp_kernel(bagel_ctx* c, int version) {
+  return guarded(c, [&] {
+    REQUIRE(version == 0 || version == 1, BAGEL_E_ARG, "bagel_set_gp_kernel: version must be 0 or 1 (got %d)", version);
+    c->gp_kernel = version;
+  });
+}
+
+extern "C" int bagel_get_gp_kernel(const bagel_ctx* c, int* version) {
+  if (!c || !version) return BAGEL_E_ARG;
+  *version = (c->gp_kernel == 1 && c->k > 0 && tc_supported(c)) ? 1 : (c->gp_kernel == 1 && c->k == 0 ? 1 : 0);
+  return BAGEL_OK;
 }

@@ -44,9 +44,26 @@ struct GpDesc {
   float s[BAGEL_MAX_P];
 };
 
+// Tensor-core (tcgen05) path state: packed operand tiles (cache-build time) and
+// its per-step buffers (see gp_step_tc.cu for layouts).
+struct TcState {
+  uint8_t* tiles1 = nullptr;  // p x t1_stride bytes
+  uint8_t* tiles2 = nullptr;  // p x t2_stride bytes
+  size_t t1_stride = 0, t2_stride = 0;
+  float* colscale = nullptr;      // p x k  (2^e_j)
+  float* colscale_inv = nullptr;  // p x k  (2^-e_j)
+  float* qscale = nullptr;        // p x MAX_D
+  float* P1z = nullptr;           // S1 x p x nct x NZ x B
+  float* P1h = nullptr;           // S1 x p x B x (1 + d)
+  uint8_t* Zp = nullptr;          // packed pass-2 A operand
+  float* zrow_inv = nullptr;      // p x B
+};
+
 struct Workspace {
   int B = 0, T = 0;         // capacity
-  int S1 = 0, S2 = 0;       // N-splits of pass 1 / pass 2
+  int S1 = 0, S2 = 0;       // N-splits of pass 1 / pass 2 (v0 FFMA path)
+  int S1tc = 0, S2tc = 0, tps1 = 0, tps2 = 0;  // tcgen05 path splits / tiles per split
+  int S2eff = 0;            // number of pass-2 partial slices the epilogue sums
   float* xstar = nullptr;   // B x d
   float* P1 = nullptr;      // S1 x p x B x Cld partial [mu | k a X | z]
   float* Z = nullptr;       // p x B x k
@@ -91,6 +108,8 @@ struct bagel_ctx {
   PolicyDesc pol{};
   RewardDesc rw{};
   Workspace ws;
+  TcState tcs;
+  int gp_kernel = 1;  // 1: tcgen05 path (default), 0: v0 FFMA path (reference / A-B tests)
   int last_launches = 0;
   int num_sms = 148;
   // per-kernel-class event timing (bagel_profile)
@@ -155,3 +174,16 @@ int ro_philox_raw(const uint32_t* ctr, uint32_t k0, uint32_t k1, int n, uint32_t
 int ro_philox_normals(uint64_t seed, long long traj_offset, int B, int T, int p, float* out,
                       cudaStream_t st);
 int ro_reverse_block_rows();
+
+// gp_step_tc.cu
+bool tc_supported(const bagel_ctx* c);
+size_t tc_tiles1_bytes(const bagel_ctx* c);
+size_t tc_tiles2_bytes(const bagel_ctx* c);
+int tc_pack(bagel_ctx* c, int m, cudaStream_t st);
+void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2);
+size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1);
+size_t tc_zp_bytes(const bagel_ctx* c, int B);
+int tc_njt(const bagel_ctx* c);
+int tc_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);
+int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st);
+int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);

@@ -354,6 +354,6 @@ int gs_finish_predict(const bagel_ctx* c, const float* xstar, int B, float* mean
                       float* dmean, float* dvar, cudaStream_t st) {
   (void)dmean;  // written by gs_reduce1
   DISPATCH_D(c->gp.d, (k_finish_predict<D><<<cdiv(B * c->gp.p, 128), 128, 0, st>>>(
-                          c->gp, xstar, B, c->ws.S2, c->ws.P2, c->ws.mu, c->ws.var, mean, var, dvar)));
+                          c->gp, xstar, B, c->ws.S2eff, c->ws.P2, c->ws.mu, c->ws.var, mean, var, dvar)));
   return 1;
 }

@@ -1,0 +1,798 @@
+// gp_step_tc.cu -- the GP step of the rollout on the 5th-generation tensor cores
+// (north star item (2): "a fused sm_100a kernel that generates k(x*,X) tiles on the
+// fly in shared memory ... and contracts them against [alpha | R^T] staged by TMA on
+// tensor cores ... it also emits the input Jacobians").
+//
+// Per output m and a batch of query rows x* (Eq.2-3 with LOVE):
+//   pass 1 (k_p1_tc)  z = R k(x*, X) on tcgen05 (3-pass fp16 hi/lo split, fp32 TMEM
+//                     accumulation); the 1 + d mean columns [mu | sum k a X_c] are
+//                     accumulated in fp32 on the CUDA cores by the same warps that
+//                     generate ktilde = exp2(-||x_hat - X_hat||^2) (never stored in HBM).
+//   reduce 1          sums the N-split partials; v = s - ||z||^2, sigma, J^mu; packs
+//                     z as the fp16 hi/lo A operand of pass 2.
+//   pass 2 (k_p2_tc)  W = Z R (w_n = sum_j z_j R_jn) on tcgen05, then on the CUDA cores
+//                     sum_n w_n k_n [1 | X_n] for J^v (ktilde regenerated).
+// Operands are packed once at cache-build time in the canonical no-swizzle K-major
+// layout (tc.cuh) so every pipeline stage is ONE contiguous 1-D bulk copy (TMA engine).
+// Split precision: a = hi + lo with hi = fp16(a), lo = fp16(a - hi); the product
+// a.b ~ hi.hi + hi.lo + lo.hi (fp32 accumulate) -- fp32-class accuracy (SURVEY §7
+// hard part 1), verified in tests/test_gpu_tc.py.  B operands carry power-of-two
+// scales (per z column in pass 1, per training point in pass 2; per row for Z),
+// undone exactly in the epilogues.
+#include <cuda_fp16.h>
+
+#include "bagel_internal.h"
+#include "tc.cuh"
+
+namespace tcg {
+
+constexpr int KT1 = 32;      // training points per pass-1 stage
+constexpr int ST1 = 4;       // pass-1 pipeline stages
+constexpr int AUXW = 20;     // floats of per-n side data per stage row
+constexpr int NT2 = 32;      // training points per pass-2 stage
+constexpr int ST2 = 2;       // pass-2 pipeline stages
+constexpr int GEN_WARPS = 8; // generator / epilogue warps (2 per TMEM lane quarter)
+constexpr int THREADS = 64 + 32 * GEN_WARPS;
+constexpr int P2_LD = 1 + BAGEL_MAX_D;
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+__host__ __device__ inline int cdiv_dev(int a, int b) { return (a + b - 1) / b; }
+
+struct Geo {
+  int N, d, p, k;
+  int nct, NZ;        // pass-1 z-column tiles and their width (<= 256, multiple of 16)
+  int njt, KJ;        // pass-2 j tiles (<= 256, multiple of 16)
+  int nt1, nt2;       // number of n-tiles of pass 1 / pass 2
+  size_t t1_bytes;    // bytes of one pass-1 stage tile [B hi | B lo | aux]
+  size_t t2_bytes;    // bytes of one pass-2 stage tile
+};
+
+__host__ __device__ inline size_t t1_bytes(int NZ) { return (size_t)4 * NZ * KT1 + (size_t)KT1 * AUXW * 4; }
+__host__ __device__ inline size_t t2_bytes(int KJ) { return (size_t)4 * NT2 * KJ + (size_t)NT2 * AUXW * 4; }
+
+inline Geo make_geo(int N, int d, int p, int k) {
+  Geo g{};
+  g.N = N; g.d = d; g.p = p; g.k = k;
+  g.nct = cdiv(k, 256);
+  g.NZ = cdiv(cdiv(k, g.nct), 16) * 16;
+  g.njt = cdiv(k, 256);
+  g.KJ = cdiv(cdiv(k, g.njt), 16) * 16;
+  g.nt1 = cdiv(N, KT1);
+  g.nt2 = cdiv(N, NT2);
+  g.t1_bytes = t1_bytes(g.NZ);
+  g.t2_bytes = t2_bytes(g.KJ);
+  return g;
+}
+
+__device__ __forceinline__ void split_f16(float v, __half& hi, __half& lo) {
+  hi = __float2half_rn(v);
+  lo = __float2half_rn(v - __half2float(hi));
+}
+
+// power-of-two scale bringing max|v| into [0.5, 1): returns 2^-e (and the inverse 2^e)
+__device__ __forceinline__ float pow2_scale_for(float amax, float* inv) {
+  if (!(amax > 0.0f)) {
+    *inv = 1.0f;
+    return 1.0f;
+  }
+  int e;
+  frexpf(amax, &e);  // amax = f 2^e, f in [0.5, 1)
+  *inv = ldexpf(1.0f, e);
+  return ldexpf(1.0f, -e);
+}
+
+// ====================================================================== packing
+// Pass-1 tiles of output m: [ct][t] -> [B hi: NZ x KT1 | B lo | aux: KT1 x AUXW]
+// B(j, n) = s R_jn * colscale_j^-1 (j = ct*NZ + row), aux(n) = [X_hat(d) | s alpha | s alpha X(d)].
+__global__ void k_pack1(Geo g, const float* __restrict__ X, const double* __restrict__ alpha,
+                        const double* __restrict__ R, double s, const float* __restrict__ qscale,
+                        const float* __restrict__ colscale_inv, uint8_t* __restrict__ out) {
+  const int t = blockIdx.x, ct = blockIdx.y;
+  uint8_t* tile = out + ((size_t)ct * g.nt1 + t) * g.t1_bytes;
+  __half* bhi = reinterpret_cast<__half*>(tile);
+  __half* blo = bhi + (size_t)g.NZ * KT1;
+  float* aux = reinterpret_cast<float*>(blo + (size_t)g.NZ * KT1);
+  for (int idx = threadIdx.x; idx < g.NZ * KT1; idx += blockDim.x) {
+    const int jr = idx / KT1, nn = idx % KT1;
+    const int j = ct * g.NZ + jr, n = t * KT1 + nn;
+    float v = 0.0f;
+    if (j < g.k && n < g.N) v = (float)(s * R[(size_t)j * g.N + n]) * colscale_inv[j];
+    __half hi, lo;
+    split_f16(v, hi, lo);
+    const int ci = tc::canon_idx(jr, nn, KT1);
+    bhi[ci] = hi;
+    blo[ci] = lo;
+  }
+  for (int idx = threadIdx.x; idx < KT1 * AUXW; idx += blockDim.x) {
+    const int nn = idx / AUXW, f = idx % AUXW;
+    const int n = t * KT1 + nn;
+    float v = 0.0f;
+    if (n < g.N) {
+      if (f < g.d) v = X[(size_t)n * g.d + f] * qscale[f];
+      else if (f == g.d) v = (float)(s * alpha[n]);
+      else if (f < 2 * g.d + 1) v = (float)(s * alpha[n] * (double)X[(size_t)n * g.d + f - g.d - 1]);
+    } else if (f < g.d) {
+      v = 1e18f;  // padded training point: infinitely far, ktilde = 0
+    }
+    aux[idx] = v;
+  }
+}
+
+// Per-column (j) power-of-two scales of s R_j (max over n): colscale_inv = 2^-e_j, colscale = 2^e_j.
+__global__ void k_colscale(const double* __restrict__ R, int N, int k, double s, float* __restrict__ cs_inv,
+                           float* __restrict__ cs) {
+  const int j = blockIdx.x;
+  __shared__ float red[256];
+  float a = 0.0f;
+  for (int n = threadIdx.x; n < N; n += 256) a = fmaxf(a, fabsf((float)(s * R[(size_t)j * N + n])));
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    float inv;
+    const float sc = pow2_scale_for(red[0], &inv);
+    cs_inv[j] = sc;
+    cs[j] = inv;
+  }
+}
+
+// Pass-2 tiles of output m: [jt][t] -> [B hi: NT2 x KJ | B lo | aux: NT2 x AUXW]
+// B(n, j) = s R_jn * 2^-f_n (f_n from max over the tile's j range), aux(n) = [X_hat(d) | X(d) | 2^f_n].
+__global__ void k_pack2(Geo g, const float* __restrict__ X, const double* __restrict__ R, double s,
+                        const float* __restrict__ qscale, uint8_t* __restrict__ out) {
+  const int t = blockIdx.x, jt = blockIdx.y;
+  uint8_t* tile = out + ((size_t)jt * g.nt2 + t) * g.t2_bytes;
+  __half* bhi = reinterpret_cast<__half*>(tile);
+  __half* blo = bhi + (size_t)NT2 * g.KJ;
+  float* aux = reinterpret_cast<float*>(blo + (size_t)NT2 * g.KJ);
+  __shared__ float rsc[NT2], rinv[NT2];
+  // per-n scale: one warp per n row
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int nn = warp; nn < NT2; nn += blockDim.x / 32) {
+    const int n = t * NT2 + nn;
+    float a = 0.0f;
+    if (n < g.N)
+      for (int jr = lane; jr < g.KJ; jr += 32) {
+        const int j = jt * g.KJ + jr;
+        if (j < g.k) a = fmaxf(a, fabsf((float)(s * R[(size_t)j * g.N + n])));
+      }
+    for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane == 0) {
+      float inv;
+      rsc[nn] = pow2_scale_for(a, &inv);
+      rinv[nn] = inv;
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < NT2 * g.KJ; idx += blockDim.x) {
+    const int nn = idx / g.KJ, jr = idx % g.KJ;
+    const int n = t * NT2 + nn, j = jt * g.KJ + jr;
+    float v = 0.0f;
+    if (n < g.N && j < g.k) v = (float)(s * R[(size_t)j * g.N + n]) * rsc[nn];
+    __half hi, lo;
+    split_f16(v, hi, lo);
+    const int ci = tc::canon_idx(nn, jr, g.KJ);
+    bhi[ci] = hi;
+    blo[ci] = lo;
+  }
+  for (int idx = threadIdx.x; idx < NT2 * AUXW; idx += blockDim.x) {
+    const int nn = idx / AUXW, f = idx % AUXW;
+    const int n = t * NT2 + nn;
+    float v = 0.0f;
+    if (n < g.N) {
+      if (f < g.d) v = X[(size_t)n * g.d + f] * qscale[f];
+      else if (f < 2 * g.d) v = X[(size_t)n * g.d + f - g.d];
+      else if (f == 2 * g.d) v = rinv[nn];
+    } else if (f < g.d) {
+      v = 1e18f;
+    }
+    aux[idx] = v;
+  }
+}
+
+// ====================================================================== pass 1
+struct P1Args {
+  Geo g;
+  int m_count;               // p
+  const float* xstar;        // B x d
+  int B;
+  const uint8_t* tiles;      // [m][ct][t] pass-1 tiles
+  size_t m_stride;           // bytes per output m of tiles
+  int tiles_per_split;
+  float* P1z;                // [split][m][ct][NZ][B]
+  float* P1h;                // [split][m][B][1 + d]
+  float qscale[BAGEL_MAX_P][BAGEL_MAX_D];
+};
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const Geo& g = a.g;
+  const int NZ = g.NZ;
+  const size_t a_bytes = (size_t)128 * KT1 * 2;     // one fp16 A tile (hi or lo)
+  const size_t stage_bytes = 2 * a_bytes + g.t1_bytes;
+  __shared__ __align__(8) uint64_t full_b[ST1], full_a[ST1], empty[ST1], done;
+  __shared__ uint32_t tmem_base;
+  __shared__ float hsum[128][1 + D];
+
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int row0 = blockIdx.x * 128;
+  const int m = blockIdx.y / g.nct, ct = blockIdx.y % g.nct;
+  const int split = blockIdx.z;
+  const int t_begin = split * a.tiles_per_split;
+  const int t_end = min(g.nt1, t_begin + a.tiles_per_split);
+  const int ntile = max(0, t_end - t_begin);
+  const uint8_t* tiles = a.tiles + (size_t)m * a.m_stride + ((size_t)ct * g.nt1) * g.t1_bytes;
+
+  uint32_t ncols = 32;
+  while ((int)ncols < NZ) ncols <<= 1;
+  if (tid == 0) {
+    for (int s = 0; s < ST1; ++s) {
+      tc::mbar_init(&full_b[s], 1);
+      tc::mbar_init(&full_a[s], 32 * GEN_WARPS);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&done, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(&tmem_base, ncols);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  auto stage_ptr = [&](int s) { return sm + (size_t)s * stage_bytes; };
+
+  if (warp == 0) {
+    // ------------------------------------------------ producer (one elected lane)
+    if (lane == 0) {
+      for (int i = 0; i < ntile; ++i) {
+        const int s = i % ST1;
+        const uint32_t ph = (uint32_t)(i / ST1) & 1u;
+        tc::mbar_wait(&empty[s], ph ^ 1u);
+        tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)g.t1_bytes);
+        tc::bulk_g2s(stage_ptr(s) + 2 * a_bytes, tiles + (size_t)(t_begin + i) * g.t1_bytes, (uint32_t)g.t1_bytes,
+                     &full_b[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_f16(128, NZ);
+      for (int i = 0; i < ntile; ++i) {
+        const int s = i % ST1;
+        const uint32_t ph = (uint32_t)(i / ST1) & 1u;
+        tc::mbar_wait(&full_b[s], ph);
+        tc::mbar_wait(&full_a[s], ph);
+        tc::tc_fence_after();
+        const uint32_t base = tc::smem_u32(stage_ptr(s));
+        const uint32_t ahi = base, alo = base + (uint32_t)a_bytes;
+        const uint32_t bhi = base + 2u * (uint32_t)a_bytes, blo = bhi + (uint32_t)NZ * KT1 * 2u;
+        constexpr uint32_t SBO = (KT1 / 8) * 128;
+#pragma unroll
+        for (int ks = 0; ks < KT1 / 16; ++ks) {
+          const uint32_t o = ks * 256u;
+          const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
+          tc::mma_f16(tmem, tc::umma_desc(ahi + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, acc0);
+          tc::mma_f16(tmem, tc::umma_desc(ahi + o, 128, SBO), tc::umma_desc(blo + o, 128, SBO), idesc, 1u);
+          tc::mma_f16(tmem, tc::umma_desc(alo + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, 1u);
+        }
+        tc::umma_commit(&empty[s]);
+      }
+      tc::umma_commit(&done);
+    }
+  } else {
+    // ------------------------------------------------ ktilde generators (2 threads per row)
+    const int gt = tid - 64;           // 0..255
+    const int r = gt % 128, half = gt / 128;
+    const int row = row0 + r;
+    float xq[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] * a.qscale[m][c] : 0.0f;
+    float hacc[1 + D];
+#pragma unroll
+    for (int c = 0; c <= D; ++c) hacc[c] = 0.0f;
+    for (int i = 0; i < ntile; ++i) {
+      const int s = i % ST1;
+      const uint32_t ph = (uint32_t)(i / ST1) & 1u;
+      tc::mbar_wait(&empty[s], ph ^ 1u);  // MMA done reading A[s] from the previous round
+      tc::mbar_wait(&full_b[s], ph);      // aux (X_hat, s alpha, ...) of this tile landed
+      uint8_t* st = stage_ptr(s);
+      __half* ahi = reinterpret_cast<__half*>(st);
+      __half* alo = ahi + 128 * KT1;
+      const float* aux = reinterpret_cast<const float*>(st + 2 * a_bytes + (size_t)4 * NZ * KT1);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {  // two 8-wide chunks per thread
+        const int kk = half * 2 + cc;
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          float kv[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float* an = aux + (kk * 8 + e + u) * AUXW;
+            float q = 0.0f;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              const float df = xq[c] - an[c];
+              q = fmaf(df, df, q);
+            }
+            const float kt = exp2f(-q);
+            kv[u] = kt;
+            hacc[0] = fmaf(kt, an[D], hacc[0]);
+#pragma unroll
+            for (int c = 0; c < D; ++c) hacc[1 + c] = fmaf(kt, an[D + 1 + c], hacc[1 + c]);
+          }
+          const __half2 h2 = __floats2half2_rn(kv[0], kv[1]);
+          const float2 hf = __half22float2(h2);
+          const __half2 l2 = __floats2half2_rn(kv[0] - hf.x, kv[1] - hf.y);
+          hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+          lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+        }
+        const int ci = tc::canon_idx(r, kk * 8, KT1);
+        *reinterpret_cast<uint4*>(ahi + ci) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(alo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&full_a[s]);
+    }
+    // ---- mean columns: combine the two halves of each row
+    if (half == 1)
+      for (int c = 0; c <= D; ++c) hsum[r][c] = hacc[c];
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS));
+    if (half == 0 && row < a.B && ct == 0) {
+      float* o = a.P1h + ((size_t)(split * a.m_count + m) * a.B + row) * (1 + D);
+      for (int c = 0; c <= D; ++c) o[c] = hacc[c] + hsum[r][c];
+    }
+    // ---- z columns: TMEM -> registers -> global (column-major over rows, coalesced)
+    tc::mbar_wait(&done, 0);
+    __syncwarp();
+    tc::tc_fence_after();
+    const int quarter = warp % 4;  // TMEM lane quarter accessible to this warp
+    const int wrow = quarter * 32 + lane;
+    const int cols_half = NZ / 2;  // NZ multiple of 16 -> halves multiple of 8
+    const int c_begin = half * cols_half;
+    float* zout = a.P1z + ((size_t)((split * a.m_count + m) * g.nct + ct) * NZ) * a.B;
+    for (int c0 = 0; c0 < cols_half; c0 += 16) {
+      float v[16];
+      // columns beyond this half are loaded (x16 granularity) but not stored
+      tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c_begin + c0), v);
+      tc::tmem_ld_wait();
+      const int grow = row0 + wrow;
+      if (grow < a.B) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int c = c0 + u;
+          if (c < cols_half) zout[(size_t)(c_begin + c) * a.B + grow] = ntile > 0 ? v[u] : 0.0f;
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, ncols);
+}
+
+// ====================================================================== reduce 1
+struct R1Args {
+  Geo g;
+  const float* xstar;
+  int B, S1;
+  const float* P1z;
+  const float* P1h;
+  const float* colscale;   // [m][k] 2^e_j
+  float s[BAGEL_MAX_P];
+  float ell2inv[BAGEL_MAX_P][BAGEL_MAX_D];
+  float* Z;                // [m][B][k] fp32 (unscaled z)
+  uint8_t* Zp;             // packed pass-2 A operand [m][rowtile][jt][hi | lo]
+  float* zrow_inv;         // [m][B] 2^e_r (undo of the per-row Z scale)
+  float* mu;               // [m][B]
+  float* var;              // [m][B]
+  float* jmu;              // [B][p][d] (nullable)
+  float* sig;              // [B][p] (nullable)
+};
+
+// One CTA per (32 rows, output m); 256 threads: row r = tid % 32, j group = tid / 32.
+template <int D>
+__global__ void __launch_bounds__(256) k_r1_tc(R1Args a) {
+  const Geo& g = a.g;
+  const int m = blockIdx.y;
+  const int r = threadIdx.x % 32, jg = threadIdx.x / 32;
+  const int row = blockIdx.x * 32 + r;
+  const bool ok = row < a.B;
+  __shared__ double zz_s[8][32];
+  __shared__ float zmax_s[8][32];
+  __shared__ float scale_s[32];
+  const int per = cdiv_dev(cdiv_dev(g.k, 8), 8) * 8;  // j range per thread, multiple of 8
+  const int j0 = jg * per, j1 = min(g.k, j0 + per);
+  double zz = 0.0;
+  float zmax = 0.0f;
+  for (int j = j0; j < j1; ++j) {
+    const int ct = j / g.NZ, jr = j % g.NZ;
+    float v = 0.0f;
+    if (ok)
+      for (int s = 0; s < a.S1; ++s)
+        v += a.P1z[((size_t)((s * g.p + m) * g.nct + ct) * g.NZ + jr) * a.B + row];
+    v *= a.colscale[(size_t)m * g.k + j];
+    if (ok) a.Z[((size_t)m * a.B + row) * g.k + j] = v;
+    zz += (double)v * (double)v;
+    zmax = fmaxf(zmax, fabsf(v));
+  }
+  zz_s[jg][r] = zz;
+  zmax_s[jg][r] = zmax;
+  __syncthreads();
+  if (jg == 0) {
+    double t = 0.0;
+    float mx = 0.0f;
+    for (int i = 0; i < 8; ++i) {  // fixed order
+      t += zz_s[i][r];
+      mx = fmaxf(mx, zmax_s[i][r]);
+    }
+    float inv;
+    const float sc = pow2_scale_for(mx, &inv);
+    scale_s[r] = sc;
+    if (ok) {
+      a.zrow_inv[(size_t)m * a.B + row] = inv;
+      float h[1 + D];
+#pragma unroll
+      for (int c = 0; c <= D; ++c) h[c] = 0.0f;
+      for (int s = 0; s < a.S1; ++s) {
+        const float* src = a.P1h + ((size_t)(s * g.p + m) * a.B + row) * (1 + D);
+#pragma unroll
+        for (int c = 0; c <= D; ++c) h[c] += src[c];
+      }
+      const float v = (float)((double)a.s[m] - t);
+      const float sg = sqrtf(fmaxf(v, BAGEL_VAR_FLOOR));
+      a.mu[(size_t)m * a.B + row] = h[0];
+      a.var[(size_t)m * a.B + row] = v;
+      if (a.sig) a.sig[(size_t)row * g.p + m] = v > BAGEL_VAR_FLOOR ? sg : -sg;
+      if (a.jmu)
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+          a.jmu[((size_t)row * g.p + m) * D + c] = (h[1 + c] - a.xstar[(size_t)row * D + c] * h[0]) * a.ell2inv[m][c];
+    }
+  }
+  __syncthreads();
+  // pack scaled z as fp16 hi/lo (pass-2 A operand): rows of 128, K = KJ per j tile
+  const float sc = scale_s[r];
+  const int rt = row / 128, rr = row % 128;
+  const size_t tile_halfs = (size_t)128 * g.KJ;
+  for (int j8 = j0; j8 < j1; j8 += 8) {
+    const int jt = j8 / g.KJ, jr = j8 % g.KJ;
+    uint8_t* base = a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * tile_halfs * 2 * 2;
+    __half* zhi = reinterpret_cast<__half*>(base);
+    __half* zlo = zhi + tile_halfs;
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      float v0 = 0.0f, v1 = 0.0f;
+      if (ok) {
+        if (j8 + e < g.k) v0 = a.Z[((size_t)m * a.B + row) * g.k + j8 + e] * sc;
+        if (j8 + e + 1 < g.k) v1 = a.Z[((size_t)m * a.B + row) * g.k + j8 + e + 1] * sc;
+      }
+      const __half2 h2 = __floats2half2_rn(v0, v1);
+      const float2 hf = __half22float2(h2);
+      const __half2 l2 = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+      hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+      lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+    }
+    const int ci = tc::canon_idx(rr, jr, g.KJ);
+    *reinterpret_cast<uint4*>(zhi + ci) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(zlo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+  }
+}
+
+// ====================================================================== pass 2
+struct P2Args {
+  Geo g;
+  int m_count;
+  const float* xstar;
+  int B;
+  const uint8_t* tiles;     // [m][jt][t] pass-2 tiles
+  size_t m_stride;
+  const uint8_t* Zp;        // packed Z
+  const float* zrow_inv;    // [m][B]
+  int tiles_per_split;
+  float* P2;                // [split * njt + jt][m][B][P2_LD]
+  float qscale[BAGEL_MAX_P][BAGEL_MAX_D];
+};
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const Geo& g = a.g;
+  const int KJ = g.KJ;
+  const size_t zt_bytes = (size_t)128 * KJ * 2;  // one fp16 Z tile (hi or lo)
+  __shared__ __align__(8) uint64_t zfull, full_b[ST2], empty[ST2], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float asum[128][1 + D];
+
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int row0 = blockIdx.x * 128;
+  const int m = blockIdx.y / g.njt, jt = blockIdx.y % g.njt;
+  const int split = blockIdx.z;
+  const int t_begin = split * a.tiles_per_split;
+  const int t_end = min(g.nt2, t_begin + a.tiles_per_split);
+  const int ntile = max(0, t_end - t_begin);
+  const uint8_t* tiles = a.tiles + (size_t)m * a.m_stride + ((size_t)jt * g.nt2) * g.t2_bytes;
+  uint8_t* zsm = sm;                       // Z hi | Z lo
+  uint8_t* bsm = sm + 2 * zt_bytes;        // stages
+  constexpr uint32_t NCOLS = 2 * NT2 < 32 ? 32 : 2 * NT2;
+
+  if (tid == 0) {
+    tc::mbar_init(&zfull, 1);
+    for (int s = 0; s < ST2; ++s) {
+      tc::mbar_init(&full_b[s], 1);
+      tc::mbar_init(&empty[s], 1 + 32 * GEN_WARPS);  // MMA commit + every epilogue thread (aux reads)
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 32 * GEN_WARPS);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(&tmem_base, NCOLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int rt = blockIdx.x;
+      const uint8_t* zsrc = a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * zt_bytes * 2;
+      tc::mbar_arrive_expect_tx(&zfull, (uint32_t)(2 * zt_bytes));
+      tc::bulk_g2s(zsm, zsrc, (uint32_t)(2 * zt_bytes), &zfull);
+      for (int i = 0; i < ntile; ++i) {
+        const int s = i % ST2;
+        const uint32_t ph = (uint32_t)(i / ST2) & 1u;
+        tc::mbar_wait(&empty[s], ph ^ 1u);
+        tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)g.t2_bytes);
+        tc::bulk_g2s(bsm + (size_t)s * g.t2_bytes, tiles + (size_t)(t_begin + i) * g.t2_bytes, (uint32_t)g.t2_bytes,
+                     &full_b[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_f16(128, NT2);
+      const uint32_t SBO = (uint32_t)(KJ / 8) * 128u;
+      const uint32_t zhi = tc::smem_u32(zsm), zlo = zhi + (uint32_t)zt_bytes;
+      tc::mbar_wait(&zfull, 0);
+      for (int i = 0; i < ntile; ++i) {
+        const int s = i % ST2, b = i & 1;
+        const uint32_t ph = (uint32_t)(i / ST2) & 1u;
+        const uint32_t tph = (uint32_t)(i / 2) & 1u;
+        tc::mbar_wait(&tempty[b], tph ^ 1u);  // epilogue drained TMEM buffer b
+        tc::mbar_wait(&full_b[s], ph);
+        tc::tc_fence_after();
+        const uint32_t bhi = tc::smem_u32(bsm + (size_t)s * g.t2_bytes);
+        const uint32_t blo = bhi + (uint32_t)(NT2 * KJ * 2);
+        const uint32_t d = tmem + (uint32_t)(b * NT2);
+        for (int ks = 0; ks < KJ / 16; ++ks) {
+          const uint32_t o = ks * 256u;
+          tc::mma_f16(d, tc::umma_desc(zhi + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, ks > 0 ? 1u : 0u);
+          tc::mma_f16(d, tc::umma_desc(zhi + o, 128, SBO), tc::umma_desc(blo + o, 128, SBO), idesc, 1u);
+          tc::mma_f16(d, tc::umma_desc(zlo + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, 1u);
+        }
+        tc::umma_commit(&empty[s]);
+        tc::umma_commit(&tfull[b]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue: sum_n (s w_n) ktilde_n [1 | X_n]
+    const int gt = tid - 64;
+    const int quarter = warp % 4, half = gt / 128;  // column half of the NT2 columns
+    const int r = quarter * 32 + lane;
+    const int row = row0 + r;
+    float xq[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] * a.qscale[m][c] : 0.0f;
+    const float zinv = row < a.B ? a.zrow_inv[(size_t)m * a.B + row] : 0.0f;
+    float acc[1 + D];
+#pragma unroll
+    for (int c = 0; c <= D; ++c) acc[c] = 0.0f;
+    for (int i = 0; i < ntile; ++i) {
+      const int s = i % ST2, b = i & 1;
+      const uint32_t tph = (uint32_t)(i / 2) & 1u;
+      tc::mbar_wait(&tfull[b], tph);
+      __syncwarp();
+      tc::tc_fence_after();
+      float w[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * NT2 + half * 16), w);
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[b]);
+      // stage s (its aux rows) stays resident until every epilogue thread has arrived on empty[s]
+      const float* aux = reinterpret_cast<const float*>(bsm + (size_t)s * g.t2_bytes + (size_t)4 * NT2 * KJ);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float* an = aux + (half * 16 + u) * AUXW;
+        float q = 0.0f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const float df = xq[c] - an[c];
+          q = fmaf(df, df, q);
+        }
+        const float t = w[u] * an[2 * D] * exp2f(-q);
+        acc[0] += t;
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc[1 + c] = fmaf(t, an[D + c], acc[1 + c]);
+      }
+      tc::mbar_arrive(&empty[s]);
+    }
+    // combine the two column halves of each row, undo the Z row scale
+    if (half == 1)
+      for (int c = 0; c <= D; ++c) asum[r][c] = acc[c];
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS));
+    if (half == 0 && row < a.B) {
+      float* o = a.P2 + (((size_t)(split * g.njt + jt) * a.m_count + m) * a.B + row) * P2_LD;
+      for (int c = 0; c <= D; ++c) o[c] = (acc[c] + asum[r][c]) * zinv;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, NCOLS);
+}
+
+}  // namespace tcg
+
+// ====================================================================== host side
+using namespace tcg;
+
+namespace {
+
+#define DISPATCH_D(dv, ...)                              \
+  switch (dv) {                                          \
+    case 2: { constexpr int D = 2; __VA_ARGS__; break; } \
+    case 3: { constexpr int D = 3; __VA_ARGS__; break; } \
+    case 4: { constexpr int D = 4; __VA_ARGS__; break; } \
+    case 5: { constexpr int D = 5; __VA_ARGS__; break; } \
+    case 6: { constexpr int D = 6; __VA_ARGS__; break; } \
+    case 7: { constexpr int D = 7; __VA_ARGS__; break; } \
+    case 8: { constexpr int D = 8; __VA_ARGS__; break; } \
+    default: break;                                      \
+  }
+
+Geo geo_of(const bagel_ctx* c) { return make_geo(c->N, c->d, c->p, c->k); }
+
+size_t p1_smem(const Geo& g) { return (size_t)ST1 * (2 * (size_t)128 * KT1 * 2 + g.t1_bytes); }
+size_t p2_smem(const Geo& g) { return 2 * (size_t)128 * g.KJ * 2 + (size_t)ST2 * g.t2_bytes; }
+
+}  // namespace
+
+size_t tc_tiles1_bytes(const bagel_ctx* c) {
+  const Geo g = geo_of(c);
+  return (size_t)g.nct * g.nt1 * g.t1_bytes;  // per output
+}
+size_t tc_tiles2_bytes(const bagel_ctx* c) {
+  const Geo g = geo_of(c);
+  return (size_t)g.njt * g.nt2 * g.t2_bytes;
+}
+bool tc_supported(const bagel_ctx* c) {
+  const Geo g = geo_of(c);
+  return p1_smem(g) <= 220 * 1024 && p2_smem(g) <= 220 * 1024;
+}
+
+// Pack output m of the cache into the tensor-core operand tiles (cache-build time).
+int tc_pack(bagel_ctx* c, int m, cudaStream_t st) {
+  const Geo g = geo_of(c);
+  TcState& T = c->tcs;
+  const double s = (double)c->s[m];
+  float* qs_dev = T.qscale + (size_t)m * BAGEL_MAX_D;
+  cudaMemcpyAsync(qs_dev, c->gp.qscale[m], sizeof(float) * BAGEL_MAX_D, cudaMemcpyHostToDevice, st);
+  const double* R = c->R64 + (size_t)m * c->k * c->N;
+  k_colscale<<<c->k, 256, 0, st>>>(R, c->N, c->k, s, T.colscale_inv + (size_t)m * c->k, T.colscale + (size_t)m * c->k);
+  k_pack1<<<dim3(g.nt1, g.nct), 256, 0, st>>>(g, c->X, c->alpha64 + (size_t)m * c->N, R, s, qs_dev,
+                                              T.colscale_inv + (size_t)m * c->k, T.tiles1 + (size_t)m * T.t1_stride);
+  k_pack2<<<dim3(g.nt2, g.njt), 256, 0, st>>>(g, c->X, R, s, qs_dev, T.tiles2 + (size_t)m * T.t2_stride);
+  return 3;
+}
+
+void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2) {
+  const Geo g = geo_of(c);
+  const int rt = cdiv(B, 128);
+  const int target = c->num_sms;  // one CTA per SM (smem-bound), one wave
+  int s1 = cdiv(target, rt * g.p * g.nct);
+  s1 = s1 < 1 ? 1 : (s1 > g.nt1 ? g.nt1 : s1);
+  *tps1 = cdiv(g.nt1, s1);
+  *S1 = cdiv(g.nt1, *tps1);
+  int s2 = cdiv(target, rt * g.p * g.njt);
+  s2 = s2 < 1 ? 1 : (s2 > g.nt2 ? g.nt2 : s2);
+  *tps2 = cdiv(g.nt2, s2);
+  *S2 = cdiv(g.nt2, *tps2);
+}
+
+size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1) {
+  const Geo g = geo_of(c);
+  return (size_t)S1 * g.p * g.nct * g.NZ * B;
+}
+size_t tc_zp_bytes(const bagel_ctx* c, int B) {
+  const Geo g = geo_of(c);
+  return (size_t)g.p * cdiv(B, 128) * g.njt * 128 * g.KJ * 2 * 2;
+}
+int tc_njt(const bagel_ctx* c) { return geo_of(c).njt; }
+
+static void set_attrs() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  for (int dv = 2; dv <= 8; ++dv) {
+    DISPATCH_D(dv, ({
+      cudaFuncSetAttribute(k_p1_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_p2_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    }));
+  }
+}
+
+int tc_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
+  set_attrs();
+  const Geo g = geo_of(c);
+  const TcState& T = c->tcs;
+  P1Args a{};
+  a.g = g;
+  a.m_count = c->p;
+  a.xstar = xstar;
+  a.B = B;
+  a.tiles = T.tiles1;
+  a.m_stride = T.t1_stride;
+  a.tiles_per_split = c->ws.tps1;
+  a.P1z = T.P1z;
+  a.P1h = T.P1h;
+  for (int m = 0; m < c->p; ++m)
+    for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
+  dim3 grid(cdiv(B, 128), c->p * g.nct, c->ws.S1tc);
+  DISPATCH_D(c->d, (k_p1_tc<D><<<grid, THREADS, p1_smem(g), st>>>(a)));
+  return 1;
+}
+
+int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st) {
+  const Geo g = geo_of(c);
+  const TcState& T = c->tcs;
+  R1Args a{};
+  a.g = g;
+  a.xstar = xstar;
+  a.B = B;
+  a.S1 = c->ws.S1tc;
+  a.P1z = T.P1z;
+  a.P1h = T.P1h;
+  a.colscale = T.colscale;
+  for (int m = 0; m < c->p; ++m) {
+    a.s[m] = c->gp.s[m];
+    for (int j = 0; j < BAGEL_MAX_D; ++j) a.ell2inv[m][j] = c->gp.ell2inv[m][j];
+  }
+  a.Z = c->ws.Z;
+  a.Zp = T.Zp;
+  a.zrow_inv = T.zrow_inv;
+  a.mu = c->ws.mu;
+  a.var = c->ws.var;
+  a.jmu = jmu_out;
+  a.sig = sig_out;
+  dim3 grid(cdiv(B, 32), c->p);
+  DISPATCH_D(c->d, (k_r1_tc<D><<<grid, 256, 0, st>>>(a)));
+  return 1;
+}
+
+int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
+  set_attrs();
+  const Geo g = geo_of(c);
+  const TcState& T = c->tcs;
+  P2Args a{};
+  a.g = g;
+  a.m_count = c->p;
+  a.xstar = xstar;
+  a.B = B;
+  a.tiles = T.tiles2;
+  a.m_stride = T.t2_stride;
+  a.Zp = T.Zp;
+  a.zrow_inv = T.zrow_inv;
+  a.tiles_per_split = c->ws.tps2;
+  a.P2 = c->ws.P2;
+  for (int m = 0; m < c->p; ++m)
+    for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
+  dim3 grid(cdiv(B, 128), c->p * g.njt, c->ws.S2tc);
+  DISPATCH_D(c->d, (k_p2_tc<D><<<grid, THREADS, p2_smem(g), st>>>(a)));
+  return 1;
+}

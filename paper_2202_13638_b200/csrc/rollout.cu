@@ -382,7 +382,7 @@ int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals,
   const int p = c->gp.p, d = c->gp.d;
   const Workspace& w = c->ws;
   DISPATCH_D(d, (k_epilogue<D><<<cdiv(B, EPI_ROWS), EPI_THREADS, epi_smem(c->pol), st>>>(
-                    c->pol, c->rw, c->gp, theta, goals, B, t, w.S2, w.P2, w.mu, w.var,
+                    c->pol, c->rw, c->gp, theta, goals, B, t, w.S2eff, w.P2, w.mu, w.var,
                     w.tape_x + (size_t)t * B * p, w.tape_sig + (size_t)t * B * p,
                     w.tape_jv + (size_t)t * B * p * d, w.tape_x + (size_t)(t + 1) * B * p, w.G, w.xstar,
                     seed, traj_offset, policy_next ? 1 : 0, w.err_flag, trace_mu, trace_var)));

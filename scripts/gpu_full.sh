@@ -1,0 +1,14 @@
+# full GPU round: parity tests, smoke, bench, then (only if the plain bench exited 0) ncu
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -rA --timeout=600 2>&1 | tail -${TAIL:-70} > gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python bench.py --steps ${STEPS:-10} --warmup 3 > gpurun_out/bench.log 2>&1
+if [ -n "$NCU" ]; then
+  timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b_plain.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 12000 --csv --log-file gpurun_out/launches.csv \
+      python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$NCU" -s 10 -c 2 -o gpurun_out/prof \
+      python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+fi
+echo done
