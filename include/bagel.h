@@ -197,12 +197,19 @@ int bagel_set_gp_kernel(bagel_ctx* ctx, int version);
 int bagel_get_gp_kernel(const bagel_ctx* ctx, int* version);
 
 /* Tensor-core probe: one CTA computes D[128 x N] = A[128 x K] . B[N x K]^T with
- * fp16 operands (tcgen05.mma kind::f16, fp32 accumulate in TMEM).  A and B are
- * [dev] fp16 arrays in the canonical no-swizzle K-major packing of
- * csrc/tc.cuh (element (r, k) at ((r/8)(K/8) + k/8) 64 + (r%8) 8 + k%8);
+ * fp16 operands (tcgen05.mma kind::f16, fp32 accumulate in TMEM).  B is a [dev]
+ * fp16 array in the canonical no-swizzle K-major packing of csrc/tc.cuh
+ * (element (r, k) at ((r/8)(K/8) + k/8) 64 + (r%8) 8 + k%8).  mode 0: A [dev]
+ * in the same packing, read from shared memory; mode 1: A [dev] row-major
+ * 128 x K, placed in TMEM and read by the TS form of tcgen05.mma.
  * D [dev] row-major 128 x N float32.  N in {16, 32, ..., 256}, K in {16, 32, ...},
  * (128 + N) K 2 bytes <= 200 KB.  Errors: E_ARG, E_CUDA. */
-int bagel_tc_selftest(bagel_ctx* ctx, const void* A, const void* B, int N, int K, float* D);
+int bagel_tc_selftest(bagel_ctx* ctx, const void* A, const void* B, int N, int K, int mode, float* D);
+
+/* Tensor-core issue-rate microbenchmark: `ctas` CTAs (one per SM) each issue `iters`
+ * back-to-back tcgen05.mma (M = 128, N, K = 16; mode 0: A from shared memory, 1: A from
+ * TMEM) and write the elapsed SM cycles to cycles [dev] (ctas int64).  Errors: E_ARG. */
+int bagel_tc_bench(bagel_ctx* ctx, int N, int iters, int mode, int ctas, long long* cycles);
 
 #ifdef __cplusplus
 }

@@ -59,8 +59,9 @@ def lib() -> C.CDLL:
             L.bagel_cache_set.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
             L.bagel_profile.argtypes = [_vp, C.c_int]
             L.bagel_profile_get.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
-            L.bagel_tc_selftest.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, _vp]
+            L.bagel_tc_selftest.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]
             L.bagel_set_gp_kernel.argtypes = [_vp, C.c_int]
+            L.bagel_tc_bench.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp]
             L.bagel_get_gp_kernel.argtypes = [_vp, C.POINTER(C.c_int)]
             _lib = L
     return _lib
@@ -70,7 +71,7 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "policy_configure", "reward_configure", "rollout_cost_and_grad", "bagel_last_launch_count",
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
-           "bagel_set_gp_kernel", "bagel_get_gp_kernel"]
+           "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench"]
 
 PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce"]
 
@@ -229,10 +230,15 @@ class Context:
         self._check(self.L.bagel_get_gp_kernel(self.h, C.byref(v)))
         return v.value
 
-    def tc_selftest(self, A_packed: torch.Tensor, B_packed: torch.Tensor, N: int, K: int) -> torch.Tensor:
+    def tc_selftest(self, A: torch.Tensor, B_packed: torch.Tensor, N: int, K: int, mode: int = 0) -> torch.Tensor:
         D = torch.empty(128, N, dtype=torch.float32, device=self.dev)
-        self._check(self.L.bagel_tc_selftest(self.h, _ptr(A_packed), _ptr(B_packed), int(N), int(K), _ptr(D)))
+        self._check(self.L.bagel_tc_selftest(self.h, _ptr(A), _ptr(B_packed), int(N), int(K), int(mode), _ptr(D)))
         return D
+
+    def tc_bench(self, N: int, iters: int, mode: int = 0, ctas: int = 1) -> np.ndarray:
+        cyc = torch.zeros(ctas, dtype=torch.int64, device=self.dev)
+        self._check(self.L.bagel_tc_bench(self.h, int(N), int(iters), int(mode), int(ctas), _ptr(cyc)))
+        return cyc.cpu().numpy()
 
     def cache_rank(self) -> int:
         k = C.c_int(0)

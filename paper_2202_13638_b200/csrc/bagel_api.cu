@@ -19,7 +19,9 @@
 size_t gs_pass2_smem(int k, int d);
 size_t ro_reverse_smem(const PolicyDesc& P);
 size_t ro_epilogue_smem(const PolicyDesc& P);
-int tc_selftest_launch(const void* A, const void* B, int N, int K, float* D, cudaStream_t st);
+size_t ro_policy_smem(const PolicyDesc& P);
+int tc_selftest_launch(const void* A, const void* B, int N, int K, float* D, int mode, cudaStream_t st);
+int tc_bench_launch(int N, int iters, int mode, int ctas, long long* cycles, cudaStream_t st);
 
 namespace {
 
@@ -145,8 +147,9 @@ void free_workspace(bagel_ctx* c) {
   Workspace& w = c->ws;
   dev_free(w.xstar); dev_free(w.P1); dev_free(w.Z); dev_free(w.P2); dev_free(w.mu); dev_free(w.var);
   dev_free(w.tape_x); dev_free(w.tape_sig); dev_free(w.tape_jmu); dev_free(w.tape_jv); dev_free(w.G);
-  dev_free(w.theta_part); dev_free(w.grad_tmp); dev_free(w.cost_dev); dev_free(w.err_flag);
+  dev_free(w.theta_part); dev_free(w.grad_tmp); dev_free(w.thetaT); dev_free(w.cost_dev); dev_free(w.err_flag);
   dev_free(c->tcs.P1z); dev_free(c->tcs.P1h); dev_free(c->tcs.Zp); dev_free(c->tcs.zrow_inv);
+  dev_free(c->tcs.zz_part); dev_free(c->tcs.zmax_part);
   w.B = w.T = 0;
   w.S1 = w.S2 = 0;
   w.theta_part_cap = 0;
@@ -199,6 +202,8 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
       dev_alloc(c, c->tcs.Zp, tc_zp_bytes(c, B));
       CK(cudaMemsetAsync(c->tcs.Zp, 0, tc_zp_bytes(c, B), c->stream));  // padding rows / j stay zero
       dev_alloc(c, c->tcs.zrow_inv, (size_t)p * Bs);
+      dev_alloc(c, c->tcs.zz_part, tc_zpart_count(c, B));
+      dev_alloc(c, c->tcs.zmax_part, tc_zpart_count(c, B));
     }
     dev_alloc(c, w.mu, (size_t)p * Bs);
     dev_alloc(c, w.var, (size_t)p * Bs);
@@ -225,6 +230,7 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
       w.theta_part_cap = need;
     }
     if (!w.grad_tmp) dev_alloc(c, w.grad_tmp, (size_t)c->pol.n_params + 64);
+    if (!w.thetaT) dev_alloc(c, w.thetaT, (size_t)c->pol.n_params + 64);
   }
 }
 
@@ -599,7 +605,7 @@ extern "C" int policy_configure(bagel_ctx* c, const int* sizes, int n_sizes) {
     P.max_width = mw;
     P.act_total = at;
     P.phi_mode = sizes[0] == 3 * c->p ? 1 : 0;
-    REQUIRE(ro_reverse_smem(P) <= 200 * 1024, BAGEL_E_ARG,
+    REQUIRE(ro_reverse_smem(P) <= 200 * 1024 && ro_policy_smem(P) <= 200 * 1024, BAGEL_E_ARG,
             "policy_configure: policy with %d parameters exceeds the v0 reverse kernel's shared-memory budget",
             P.n_params);
     c->pol = P;
@@ -607,6 +613,7 @@ extern "C" int policy_configure(bagel_ctx* c, const int* sizes, int n_sizes) {
     c->ws.theta_part_cap = 0;
     dev_free(c->ws.theta_part);
     dev_free(c->ws.grad_tmp);
+    dev_free(c->ws.thetaT);
   });
 }
 
@@ -781,12 +788,12 @@ extern "C" int bagel_profile_get(bagel_ctx* c, int kernel, double* total_ms, lon
   });
 }
 
-extern "C" int bagel_tc_selftest(bagel_ctx* c, const void* A, const void* B, int N, int K, float* D) {
+extern "C" int bagel_tc_selftest(bagel_ctx* c, const void* A, const void* B, int N, int K, int mode, float* D) {
   return guarded(c, [&] {
     REQUIRE(A && B && D && N >= 16 && N <= 256 && N % 16 == 0 && K >= 16 && K % 16 == 0 &&
-                (size_t)(128 + N) * K * 2 <= 200 * 1024,
-            BAGEL_E_ARG, "bagel_tc_selftest: bad shape N=%d K=%d", N, K);
-    tc_selftest_launch(A, B, N, K, D, c->stream);
+                (size_t)(128 + N) * K * 2 <= 200 * 1024 && (mode == 0 || (mode == 1 && N + K / 2 <= 512)),
+            BAGEL_E_ARG, "bagel_tc_selftest: bad shape N=%d K=%d mode=%d", N, K, mode);
+    tc_selftest_launch(A, B, N, K, D, mode, c->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
   });
@@ -803,4 +810,14 @@ extern "C" int bagel_get_gp_kernel(const bagel_ctx* c, int* version) {
   if (!c || !version) return BAGEL_E_ARG;
   *version = (c->gp_kernel == 1 && c->k > 0 && tc_supported(c)) ? 1 : (c->gp_kernel == 1 && c->k == 0 ? 1 : 0);
   return BAGEL_OK;
+}
+
+extern "C" int bagel_tc_bench(bagel_ctx* c, int N, int iters, int mode, int ctas, long long* cycles) {
+  return guarded(c, [&] {
+    REQUIRE(cycles && N >= 16 && N <= 256 && N % 16 == 0 && iters >= 1 && ctas >= 1 && mode >= 0 && mode < 32,
+            BAGEL_E_ARG, "bagel_tc_bench: bad arguments");
+    tc_bench_launch(N, iters, mode, ctas, cycles, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+  });
 }

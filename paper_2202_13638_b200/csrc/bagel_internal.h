@@ -57,6 +57,8 @@ struct TcState {
   float* P1h = nullptr;           // S1 x p x B x (1 + d)
   uint8_t* Zp = nullptr;          // packed pass-2 A operand
   float* zrow_inv = nullptr;      // p x B
+  double* zz_part = nullptr;      // p x (k/32) x B partial ||z||^2
+  float* zmax_part = nullptr;     // p x (k/32) x B partial max|z|
 };
 
 struct Workspace {
@@ -79,6 +81,7 @@ struct Workspace {
   float* theta_part = nullptr;  // nblk x n_params reverse partials
   int theta_part_cap = 0;
   float* grad_tmp = nullptr;    // n_params (host-grad staging)
+  float* thetaT = nullptr;      // n_params: per-layer transposed weights (coalesced policy forward)
   double* cost_dev = nullptr;   // 1
   int* err_flag = nullptr;      // first (t * B + b) + 1 with a non-finite state, else 0
   // host staging of [dev|host] inputs
@@ -123,6 +126,24 @@ struct bagel_ctx {
   double prof_ms[8] = {};
   long long prof_n[8] = {};
 };
+
+// Opt a kernel into the largest dynamic shared memory the device allows next to its
+// static shared memory (capped at `want`); never leaves a pending CUDA error behind.
+template <class K>
+inline void bagel_set_smem_attr(K kernel, size_t want) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  size_t cap = optin > (int)fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+  if (want > cap) want = cap;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
+  cudaGetLastError();
+}
 
 // ----------------------------------------------------------------- launchers
 // Every launcher returns the number of kernels it enqueued (for gpu_launches).
@@ -184,6 +205,7 @@ void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, in
 size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1);
 size_t tc_zp_bytes(const bagel_ctx* c, int B);
 int tc_njt(const bagel_ctx* c);
+size_t tc_zpart_count(const bagel_ctx* c, int B);
 int tc_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);
 int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st);
 int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);

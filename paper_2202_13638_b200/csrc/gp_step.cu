@@ -342,7 +342,7 @@ int gs_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
   DISPATCH_D(c->gp.d, ({
     static bool attr_set = false;  // per-process: the attribute is a function property
     if (!attr_set) {
-      cudaFuncSetAttribute(k_pass2<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      bagel_set_smem_attr(k_pass2<D>, 200 * 1024);
       attr_set = true;
     }
     k_pass2<D><<<grid, P2_THREADS, smem, st>>>(c->gp, xstar, B, c->X, c->Xs, c->V, c->ws.Z, nps, c->ws.P2);

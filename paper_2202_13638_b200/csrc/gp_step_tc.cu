@@ -27,12 +27,16 @@
 namespace tcg {
 
 constexpr int KT1 = 32;      // training points per pass-1 stage
-constexpr int ST1 = 4;       // pass-1 pipeline stages
+constexpr int ST1 = 4;       // pass-1 A (ktilde) and B (R tile) ring stages
 constexpr int AUXW = 20;     // floats of per-n side data per stage row
-constexpr int NT2 = 32;      // training points per pass-2 stage
-constexpr int ST2 = 2;       // pass-2 pipeline stages
-constexpr int GEN_WARPS = 8; // generator / epilogue warps (2 per TMEM lane quarter)
-constexpr int THREADS = 64 + 32 * GEN_WARPS;
+constexpr int NT2 = 128;     // training points per pass-2 tile (the MMA N dimension)
+constexpr int KS2 = 64;      // j per pass-2 K slab (one pipeline stage)
+constexpr int ST2 = 6;       // pass-2 slab ring stages (Z lives in TMEM)
+constexpr int STX2 = 2;      // pass-2 aux ring stages (one per tile)
+constexpr int STA = 8;       // pass-1 aux (per-n side data) ring stages
+constexpr int CTRL_WARPS = 3; // B producer, MMA issuer, aux producer
+constexpr int GEN_WARPS = 16; // generator / epilogue warps (4 per TMEM lane quarter)
+constexpr int THREADS = 32 * CTRL_WARPS + 32 * GEN_WARPS;
 constexpr int P2_LD = 1 + BAGEL_MAX_D;
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
@@ -41,7 +45,7 @@ __host__ __device__ inline int cdiv_dev(int a, int b) { return (a + b - 1) / b; 
 struct Geo {
   int N, d, p, k;
   int nct, NZ;        // pass-1 z-column tiles and their width (<= 256, multiple of 16)
-  int njt, KJ;        // pass-2 j tiles (<= 256, multiple of 16)
+  int njt, KJ;        // pass-2 j tiles (<= 256, multiple of KS2)
   int nt1, nt2;       // number of n-tiles of pass 1 / pass 2
   size_t t1_bytes;    // bytes of one pass-1 stage tile [B hi | B lo | aux]
   size_t t2_bytes;    // bytes of one pass-2 stage tile
@@ -56,7 +60,7 @@ inline Geo make_geo(int N, int d, int p, int k) {
   g.nct = cdiv(k, 256);
   g.NZ = cdiv(cdiv(k, g.nct), 16) * 16;
   g.njt = cdiv(k, 256);
-  g.KJ = cdiv(cdiv(k, g.njt), 16) * 16;
+  g.KJ = cdiv(cdiv(k, g.njt), KS2) * KS2;
   g.nt1 = cdiv(N, KT1);
   g.nt2 = cdiv(N, NT2);
   g.t1_bytes = t1_bytes(g.NZ);
@@ -139,17 +143,16 @@ __global__ void k_colscale(const double* __restrict__ R, int N, int k, double s,
   }
 }
 
-// Pass-2 tiles of output m: [jt][t] -> [B hi: NT2 x KJ | B lo | aux: NT2 x AUXW]
+// Pass-2 tiles of output m: [jt][t] -> KJ/KS2 slabs [B hi: NT2 x KS2 | B lo: NT2 x KS2] (canonical
+// K-major, rows = training points, K = j), then aux: NT2 x AUXW.
 // B(n, j) = s R_jn * 2^-f_n (f_n from max over the tile's j range), aux(n) = [X_hat(d) | X(d) | 2^f_n].
 __global__ void k_pack2(Geo g, const float* __restrict__ X, const double* __restrict__ R, double s,
                         const float* __restrict__ qscale, uint8_t* __restrict__ out) {
   const int t = blockIdx.x, jt = blockIdx.y;
   uint8_t* tile = out + ((size_t)jt * g.nt2 + t) * g.t2_bytes;
-  __half* bhi = reinterpret_cast<__half*>(tile);
-  __half* blo = bhi + (size_t)NT2 * g.KJ;
-  float* aux = reinterpret_cast<float*>(blo + (size_t)NT2 * g.KJ);
+  __half* slabs = reinterpret_cast<__half*>(tile);
+  float* aux = reinterpret_cast<float*>(tile + (size_t)4 * NT2 * g.KJ);
   __shared__ float rsc[NT2], rinv[NT2];
-  // per-n scale: one warp per n row
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   for (int nn = warp; nn < NT2; nn += blockDim.x / 32) {
     const int n = t * NT2 + nn;
@@ -168,15 +171,17 @@ __global__ void k_pack2(Geo g, const float* __restrict__ X, const double* __rest
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < NT2 * g.KJ; idx += blockDim.x) {
-    const int nn = idx / g.KJ, jr = idx % g.KJ;
+    const int jr = idx / NT2, nn = idx % NT2;  // coalesced reads of R rows
     const int n = t * NT2 + nn, j = jt * g.KJ + jr;
     float v = 0.0f;
     if (n < g.N && j < g.k) v = (float)(s * R[(size_t)j * g.N + n]) * rsc[nn];
     __half hi, lo;
     split_f16(v, hi, lo);
-    const int ci = tc::canon_idx(nn, jr, g.KJ);
-    bhi[ci] = hi;
-    blo[ci] = lo;
+    const int sl = jr / KS2, jj = jr % KS2;
+    __half* sb = slabs + (size_t)sl * 2 * NT2 * KS2;
+    const int ci = tc::canon_idx(nn, jj, KS2);
+    sb[ci] = hi;
+    sb[NT2 * KS2 + ci] = lo;
   }
   for (int idx = threadIdx.x; idx < NT2 * AUXW; idx += blockDim.x) {
     const int nn = idx / AUXW, f = idx % AUXW;
@@ -207,16 +212,50 @@ struct P1Args {
   float qscale[BAGEL_MAX_P][BAGEL_MAX_D];
 };
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// aux row of one training point as registers (float4 loads; rows are 16-byte aligned)
+template <int NV>
+__device__ __forceinline__ void load_aux(const float* row, float* out) {
+#pragma unroll
+  for (int v = 0; v < (NV + 3) / 4; ++v) {
+    const float4 f = *reinterpret_cast<const float4*>(row + 4 * v);
+    out[4 * v] = f.x;
+    if (4 * v + 1 < NV) out[4 * v + 1] = f.y;
+    if (4 * v + 2 < NV) out[4 * v + 2] = f.z;
+    if (4 * v + 3 < NV) out[4 * v + 3] = f.w;
+  }
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 template <int D>
 __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const Geo& g = a.g;
   const int NZ = g.NZ;
-  const size_t a_bytes = (size_t)128 * KT1 * 2;     // one fp16 A tile (hi or lo)
-  const size_t stage_bytes = 2 * a_bytes + g.t1_bytes;
-  __shared__ __align__(8) uint64_t full_b[ST1], full_a[ST1], empty[ST1], done;
+  constexpr int NAUX = 2 * D + 1;
+  const size_t a_bytes = (size_t)128 * KT1 * 2;  // one fp16 A tile (hi or lo)
+  const size_t b_bytes = (size_t)4 * NZ * KT1;   // B hi + lo of one tile
+  const size_t x_bytes = (size_t)KT1 * AUXW * 4; // aux rows of one tile
+  uint8_t* asm_ = sm;                            // ST1 x (A hi | A lo)
+  uint8_t* bsm = asm_ + ST1 * 2 * a_bytes;       // ST1 x (B hi | B lo)
+  uint8_t* xsm = bsm + ST1 * b_bytes;            // STA x aux
+  __shared__ __align__(8) uint64_t full_a[ST1], empty_a[ST1], full_b[ST1], empty_b[ST1], full_x[STA], empty_x[STA],
+      done;
   __shared__ uint32_t tmem_base;
-  __shared__ float hsum[128][1 + D];
+  __shared__ float hsum[3][128][1 + D];
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row0 = blockIdx.x * 128;
@@ -231,9 +270,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   while ((int)ncols < NZ) ncols <<= 1;
   if (tid == 0) {
     for (int s = 0; s < ST1; ++s) {
-      tc::mbar_init(&full_b[s], 1);
       tc::mbar_init(&full_a[s], 32 * GEN_WARPS);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty_a[s], 1);
+      tc::mbar_init(&full_b[s], 1);
+      tc::mbar_init(&empty_b[s], 1);
+    }
+    for (int s = 0; s < STA; ++s) {
+      tc::mbar_init(&full_x[s], 1);
+      tc::mbar_init(&empty_x[s], 32 * GEN_WARPS);
     }
     tc::mbar_init(&done, 1);
     tc::fence_mbar_init();
@@ -244,50 +288,62 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base;
 
-  auto stage_ptr = [&](int s) { return sm + (size_t)s * stage_bytes; };
-
   if (warp == 0) {
-    // ------------------------------------------------ producer (one elected lane)
+    // ------------------------------------------------ B-tile producer (one elected lane)
     if (lane == 0) {
       for (int i = 0; i < ntile; ++i) {
         const int s = i % ST1;
-        const uint32_t ph = (uint32_t)(i / ST1) & 1u;
-        tc::mbar_wait(&empty[s], ph ^ 1u);
-        tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)g.t1_bytes);
-        tc::bulk_g2s(stage_ptr(s) + 2 * a_bytes, tiles + (size_t)(t_begin + i) * g.t1_bytes, (uint32_t)g.t1_bytes,
+        tc::mbar_wait(&empty_b[s], ((uint32_t)(i / ST1) & 1u) ^ 1u);
+        tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)b_bytes);
+        tc::bulk_g2s(bsm + (size_t)s * b_bytes, tiles + (size_t)(t_begin + i) * g.t1_bytes, (uint32_t)b_bytes,
                      &full_b[s]);
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ aux producer (runs up to STA tiles ahead)
+    if (lane == 0) {
+      for (int i = 0; i < ntile; ++i) {
+        const int x = i % STA;
+        tc::mbar_wait(&empty_x[x], ((uint32_t)(i / STA) & 1u) ^ 1u);
+        tc::mbar_arrive_expect_tx(&full_x[x], (uint32_t)x_bytes);
+        tc::bulk_g2s(xsm + (size_t)x * x_bytes, tiles + (size_t)(t_begin + i) * g.t1_bytes + b_bytes,
+                     (uint32_t)x_bytes, &full_x[x]);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_f16(128, NZ);
+      constexpr uint32_t SBO = (KT1 / 8) * 128;
       for (int i = 0; i < ntile; ++i) {
         const int s = i % ST1;
         const uint32_t ph = (uint32_t)(i / ST1) & 1u;
         tc::mbar_wait(&full_b[s], ph);
         tc::mbar_wait(&full_a[s], ph);
         tc::tc_fence_after();
-        const uint32_t base = tc::smem_u32(stage_ptr(s));
-        const uint32_t ahi = base, alo = base + (uint32_t)a_bytes;
-        const uint32_t bhi = base + 2u * (uint32_t)a_bytes, blo = bhi + (uint32_t)NZ * KT1 * 2u;
-        constexpr uint32_t SBO = (KT1 / 8) * 128;
+        const uint32_t abase = tc::smem_u32(asm_ + (size_t)s * 2 * a_bytes);
+        const uint32_t bbase = tc::smem_u32(bsm + (size_t)s * b_bytes);
+        const uint64_t dahi = tc::umma_desc(abase, 128, SBO);
+        const uint64_t dalo = tc::umma_desc(abase + (uint32_t)a_bytes, 128, SBO);
+        const uint64_t dbhi = tc::umma_desc(bbase, 128, SBO);
+        const uint64_t dblo = tc::umma_desc(bbase + (uint32_t)NZ * KT1 * 2u, 128, SBO);
 #pragma unroll
         for (int ks = 0; ks < KT1 / 16; ++ks) {
-          const uint32_t o = ks * 256u;
+          const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
           const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
-          tc::mma_f16(tmem, tc::umma_desc(ahi + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, acc0);
-          tc::mma_f16(tmem, tc::umma_desc(ahi + o, 128, SBO), tc::umma_desc(blo + o, 128, SBO), idesc, 1u);
-          tc::mma_f16(tmem, tc::umma_desc(alo + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, 1u);
+          tc::mma_f16(tmem, dahi + o, dbhi + o, idesc, acc0);
+          tc::mma_f16(tmem, dahi + o, dblo + o, idesc, 1u);
+          tc::mma_f16(tmem, dalo + o, dbhi + o, idesc, 1u);
         }
-        tc::umma_commit(&empty[s]);
+        tc::umma_commit(&empty_a[s]);
+        tc::umma_commit(&empty_b[s]);
       }
       tc::umma_commit(&done);
     }
   } else {
-    // ------------------------------------------------ ktilde generators (2 threads per row)
-    const int gt = tid - 64;           // 0..255
-    const int r = gt % 128, half = gt / 128;
+    // ------------------------------------------------ ktilde generators (4 threads per row, 8 n each)
+    const int gt = tid - 32 * CTRL_WARPS;  // 0..511
+    const int r = gt % 128, qd = gt / 128;
     const int row = row0 + r;
     float xq[D];
 #pragma unroll
@@ -296,78 +352,71 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
 #pragma unroll
     for (int c = 0; c <= D; ++c) hacc[c] = 0.0f;
     for (int i = 0; i < ntile; ++i) {
-      const int s = i % ST1;
-      const uint32_t ph = (uint32_t)(i / ST1) & 1u;
-      tc::mbar_wait(&empty[s], ph ^ 1u);  // MMA done reading A[s] from the previous round
-      tc::mbar_wait(&full_b[s], ph);      // aux (X_hat, s alpha, ...) of this tile landed
-      uint8_t* st = stage_ptr(s);
-      __half* ahi = reinterpret_cast<__half*>(st);
+      const int s = i % ST1, x = i % STA;
+      tc::mbar_wait(&full_x[x], (uint32_t)(i / STA) & 1u);             // aux rows of tile i landed
+      tc::mbar_wait(&empty_a[s], ((uint32_t)(i / ST1) & 1u) ^ 1u);     // MMA done reading A[s]
+      __half* ahi = reinterpret_cast<__half*>(asm_ + (size_t)s * 2 * a_bytes);
       __half* alo = ahi + 128 * KT1;
-      const float* aux = reinterpret_cast<const float*>(st + 2 * a_bytes + (size_t)4 * NZ * KT1);
+      const float* aux = reinterpret_cast<const float*>(xsm + (size_t)x * x_bytes);
+      uint32_t hw[4], lw[4];
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {  // two 8-wide chunks per thread
-        const int kk = half * 2 + cc;
-        uint32_t hw[4], lw[4];
+      for (int e = 0; e < 8; e += 2) {
+        float kv[2];
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          float kv[2];
+        for (int u = 0; u < 2; ++u) {
+          float an[NAUX];
+          load_aux<NAUX>(aux + (qd * 8 + e + u) * AUXW, an);
+          float q = 0.0f;
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const float* an = aux + (kk * 8 + e + u) * AUXW;
-            float q = 0.0f;
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              const float df = xq[c] - an[c];
-              q = fmaf(df, df, q);
-            }
-            const float kt = exp2f(-q);
-            kv[u] = kt;
-            hacc[0] = fmaf(kt, an[D], hacc[0]);
-#pragma unroll
-            for (int c = 0; c < D; ++c) hacc[1 + c] = fmaf(kt, an[D + 1 + c], hacc[1 + c]);
+          for (int c = 0; c < D; ++c) {
+            const float df = xq[c] - an[c];
+            q = fmaf(df, df, q);
           }
-          const __half2 h2 = __floats2half2_rn(kv[0], kv[1]);
-          const float2 hf = __half22float2(h2);
-          const __half2 l2 = __floats2half2_rn(kv[0] - hf.x, kv[1] - hf.y);
-          hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-          lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+          const float kt = ex2_approx(-q);
+          kv[u] = kt;
+          hacc[0] = fmaf(kt, an[D], hacc[0]);
+#pragma unroll
+          for (int c = 0; c < D; ++c) hacc[1 + c] = fmaf(kt, an[D + 1 + c], hacc[1 + c]);
         }
-        const int ci = tc::canon_idx(r, kk * 8, KT1);
-        *reinterpret_cast<uint4*>(ahi + ci) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(alo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        const __half2 h2 = __floats2half2_rn(kv[0], kv[1]);
+        const float2 hf = __half22float2(h2);
+        const __half2 l2 = __floats2half2_rn(kv[0] - hf.x, kv[1] - hf.y);
+        hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+        lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
       }
+      tc::mbar_arrive(&empty_x[x]);
+      const int ci = tc::canon_idx(r, qd * 8, KT1);
+      *reinterpret_cast<uint4*>(ahi + ci) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(alo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       tc::fence_proxy_async();
       tc::mbar_arrive(&full_a[s]);
     }
-    // ---- mean columns: combine the two halves of each row
-    if (half == 1)
-      for (int c = 0; c <= D; ++c) hsum[r][c] = hacc[c];
+    // ---- mean columns: combine the four quarters of each row (fixed order)
+    if (qd > 0)
+      for (int c = 0; c <= D; ++c) hsum[qd - 1][r][c] = hacc[c];
     asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS));
-    if (half == 0 && row < a.B && ct == 0) {
+    if (qd == 0 && row < a.B && ct == 0) {
       float* o = a.P1h + ((size_t)(split * a.m_count + m) * a.B + row) * (1 + D);
-      for (int c = 0; c <= D; ++c) o[c] = hacc[c] + hsum[r][c];
+      for (int c = 0; c <= D; ++c) o[c] = ((hacc[c] + hsum[0][r][c]) + hsum[1][r][c]) + hsum[2][r][c];
     }
     // ---- z columns: TMEM -> registers -> global (column-major over rows, coalesced)
     tc::mbar_wait(&done, 0);
     __syncwarp();
     tc::tc_fence_after();
     const int quarter = warp % 4;  // TMEM lane quarter accessible to this warp
+    const int cg = (warp - CTRL_WARPS) / 4;  // column group 0..3
     const int wrow = quarter * 32 + lane;
-    const int cols_half = NZ / 2;  // NZ multiple of 16 -> halves multiple of 8
-    const int c_begin = half * cols_half;
+    const int gw = cdiv_dev(NZ, 32) * 8;  // columns per group (multiple of 8)
+    const int c_begin = cg * gw, c_end = min(NZ, c_begin + gw);
     float* zout = a.P1z + ((size_t)((split * a.m_count + m) * g.nct + ct) * NZ) * a.B;
-    for (int c0 = 0; c0 < cols_half; c0 += 16) {
-      float v[16];
-      // columns beyond this half are loaded (x16 granularity) but not stored
-      tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c_begin + c0), v);
+    const int grow = row0 + wrow;
+    for (int c0 = c_begin; c0 < c_end; c0 += 8) {
+      float v[8];
+      tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
       tc::tmem_ld_wait();
-      const int grow = row0 + wrow;
       if (grow < a.B) {
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int c = c0 + u;
-          if (c < cols_half) zout[(size_t)(c_begin + c) * a.B + grow] = ntile > 0 ? v[u] : 0.0f;
-        }
+        for (int u = 0; u < 8; ++u) zout[(size_t)(c0 + u) * a.B + grow] = ntile > 0 ? v[u] : 0.0f;
       }
     }
   }
@@ -386,7 +435,7 @@ struct R1Args {
   const float* colscale;   // [m][k] 2^e_j
   float s[BAGEL_MAX_P];
   float ell2inv[BAGEL_MAX_P][BAGEL_MAX_D];
-  float* Z;                // [m][B][k] fp32 (unscaled z)
+  float* Z;                // [m][k][B] fp32 z (after the column scales are undone)
   uint8_t* Zp;             // packed pass-2 A operand [m][rowtile][jt][hi | lo]
   float* zrow_inv;         // [m][B] 2^e_r (undo of the per-row Z scale)
   float* mu;               // [m][B]
@@ -395,55 +444,127 @@ struct R1Args {
   float* sig;              // [B][p] (nullable)
 };
 
-// One CTA per (32 rows, output m); 256 threads: row r = tid % 32, j group = tid / 32.
-template <int D>
-__global__ void __launch_bounds__(256) k_r1_tc(R1Args a) {
+// Reduce 1 in two launches with ample parallelism (the split partials are L2-resident):
+//  r1a  grid (row groups of 32, m, j groups of 32): lane = row, warp = 4 j's; sums the S1
+//       partials in split order, writes z (Z[m][j][row], coalesced) and per-(j group, row)
+//       partial ||z||^2 (fp64) and max|z|.
+//  r1b  grid (row groups of 32, m): per-row totals in j-group order -> v, sigma, J^mu,
+//       row scale; packs z as the fp16 hi/lo pass-2 A operand (row-major, the TMEM image).
+constexpr int R1_JG = 32;
+__global__ void __launch_bounds__(256) k_r1a_tc(R1Args a, double* __restrict__ zz_part, float* __restrict__ zmax_part) {
   const Geo& g = a.g;
-  const int m = blockIdx.y;
-  const int r = threadIdx.x % 32, jg = threadIdx.x / 32;
-  const int row = blockIdx.x * 32 + r;
+  const int m = blockIdx.y, jg = blockIdx.z;
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const int row = blockIdx.x * 32 + lane;
   const bool ok = row < a.B;
   __shared__ double zz_s[8][32];
-  __shared__ float zmax_s[8][32];
-  __shared__ float scale_s[32];
-  const int per = cdiv_dev(cdiv_dev(g.k, 8), 8) * 8;  // j range per thread, multiple of 8
-  const int j0 = jg * per, j1 = min(g.k, j0 + per);
-  double zz = 0.0;
-  float zmax = 0.0f;
-  for (int j = j0; j < j1; ++j) {
-    const int ct = j / g.NZ, jr = j % g.NZ;
-    float v = 0.0f;
-    if (ok)
-      for (int s = 0; s < a.S1; ++s)
-        v += a.P1z[((size_t)((s * g.p + m) * g.nct + ct) * g.NZ + jr) * a.B + row];
-    v *= a.colscale[(size_t)m * g.k + j];
-    if (ok) a.Z[((size_t)m * a.B + row) * g.k + j] = v;
-    zz += (double)v * (double)v;
-    zmax = fmaxf(zmax, fabsf(v));
+  __shared__ float zm_s[8][32];
+  float z[4] = {0.f, 0.f, 0.f, 0.f};
+  const int j0 = jg * R1_JG + w * 4;
+  if (ok) {
+    const float* src[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = min(j0 + u, g.k - 1);
+      const int ct = j / g.NZ, jr = j % g.NZ;
+      src[u] = a.P1z + ((size_t)(m * g.nct + ct) * g.NZ + jr) * a.B + row;
+    }
+    const size_t sstride = (size_t)g.p * g.nct * g.NZ * a.B;
+    // 8 splits x 4 columns of independent loads in flight, then summed in split order
+    for (int s0 = 0; s0 < a.S1; s0 += 8) {
+      float v[8][4];
+#pragma unroll
+      for (int ss = 0; ss < 8; ++ss)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[ss][u] = (s0 + ss < a.S1) ? __ldg(src[u] + (size_t)(s0 + ss) * sstride) : 0.0f;
+#pragma unroll
+      for (int ss = 0; ss < 8; ++ss)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) z[u] += v[ss][u];
+    }
   }
-  zz_s[jg][r] = zz;
-  zmax_s[jg][r] = zmax;
+  double zz = 0.0;
+  float zm = 0.0f;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = j0 + u;
+    if (j < g.k && ok) {
+      const float v = z[u] * a.colscale[(size_t)m * g.k + j];
+      a.Z[((size_t)m * g.k + j) * a.B + row] = v;
+      zz += (double)v * (double)v;
+      zm = fmaxf(zm, fabsf(v));
+    }
+  }
+  zz_s[w][lane] = zz;
+  zm_s[w][lane] = zm;
   __syncthreads();
-  if (jg == 0) {
+  if (w == 0 && ok) {
     double t = 0.0;
     float mx = 0.0f;
-    for (int i = 0; i < 8; ++i) {  // fixed order
-      t += zz_s[i][r];
-      mx = fmaxf(mx, zmax_s[i][r]);
+    for (int i = 0; i < 8; ++i) {
+      t += zz_s[i][lane];
+      mx = fmaxf(mx, zm_s[i][lane]);
     }
-    float inv;
-    const float sc = pow2_scale_for(mx, &inv);
-    scale_s[r] = sc;
-    if (ok) {
-      a.zrow_inv[(size_t)m * a.B + row] = inv;
-      float h[1 + D];
+    const int njg = cdiv_dev(g.k, R1_JG);
+    zz_part[((size_t)m * njg + jg) * a.B + row] = t;
+    zmax_part[((size_t)m * njg + jg) * a.B + row] = mx;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_r1b_tc(R1Args a, const double* __restrict__ zz_part,
+                                                const float* __restrict__ zmax_part) {
+  const Geo& g = a.g;
+  const int m = blockIdx.y;
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const int row = blockIdx.x * 32 + lane;
+  const bool ok = row < a.B;
+  __shared__ float scale_s[32];
+  __shared__ double t_s[8][32];
+  __shared__ float mx_s[8][32];
+  __shared__ float h_s[8][32][1 + D];
+  {
+    // warp w: j groups w, w+8, ... and splits w, w+8, ... (partials combined below in fixed order)
+    const int njg = cdiv_dev(g.k, R1_JG);
+    double t = 0.0;
+    float mx = 0.0f;
+    float h[1 + D];
 #pragma unroll
-      for (int c = 0; c <= D; ++c) h[c] = 0.0f;
-      for (int s = 0; s < a.S1; ++s) {
+    for (int c = 0; c <= D; ++c) h[c] = 0.0f;
+    if (ok) {
+      for (int i = w; i < njg; i += 8) {
+        t += zz_part[((size_t)m * njg + i) * a.B + row];
+        mx = fmaxf(mx, zmax_part[((size_t)m * njg + i) * a.B + row]);
+      }
+      for (int s = w; s < a.S1; s += 8) {
         const float* src = a.P1h + ((size_t)(s * g.p + m) * a.B + row) * (1 + D);
 #pragma unroll
         for (int c = 0; c <= D; ++c) h[c] += src[c];
       }
+    }
+    t_s[w][lane] = t;
+    mx_s[w][lane] = mx;
+#pragma unroll
+    for (int c = 0; c <= D; ++c) h_s[w][lane][c] = h[c];
+  }
+  __syncthreads();
+  if (w == 0) {
+    float sc = 1.0f;
+    if (ok) {
+      double t = 0.0;
+      float mx = 0.0f;
+      float h[1 + D];
+#pragma unroll
+      for (int c = 0; c <= D; ++c) h[c] = 0.0f;
+      for (int i = 0; i < 8; ++i) {  // fixed order
+        t += t_s[i][lane];
+        mx = fmaxf(mx, mx_s[i][lane]);
+#pragma unroll
+        for (int c = 0; c <= D; ++c) h[c] += h_s[i][lane][c];
+      }
+      float inv;
+      sc = pow2_scale_for(mx, &inv);
+      a.zrow_inv[(size_t)m * a.B + row] = inv;
       const float v = (float)((double)a.s[m] - t);
       const float sg = sqrtf(fmaxf(v, BAGEL_VAR_FLOOR));
       a.mu[(size_t)m * a.B + row] = h[0];
@@ -454,34 +575,33 @@ __global__ void __launch_bounds__(256) k_r1_tc(R1Args a) {
         for (int c = 0; c < D; ++c)
           a.jmu[((size_t)row * g.p + m) * D + c] = (h[1 + c] - a.xstar[(size_t)row * D + c] * h[0]) * a.ell2inv[m][c];
     }
+    scale_s[lane] = sc;
   }
   __syncthreads();
-  // pack scaled z as fp16 hi/lo (pass-2 A operand): rows of 128, K = KJ per j tile
-  const float sc = scale_s[r];
+  if (!ok) return;
+  const float sc = scale_s[lane];
   const int rt = row / 128, rr = row % 128;
   const size_t tile_halfs = (size_t)128 * g.KJ;
-  for (int j8 = j0; j8 < j1; j8 += 8) {
+  for (int c8 = w; c8 * 8 < g.k; c8 += 8) {
+    const int j8 = c8 * 8;
     const int jt = j8 / g.KJ, jr = j8 % g.KJ;
+    // row-major per row: [hi: KJ fp16 | lo: KJ fp16] (the TMEM image of the pass-2 A operand)
     uint8_t* base = a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * tile_halfs * 2 * 2;
-    __half* zhi = reinterpret_cast<__half*>(base);
-    __half* zlo = zhi + tile_halfs;
+    __half* zhi = reinterpret_cast<__half*>(base) + (size_t)rr * 2 * g.KJ;
+    __half* zlo = zhi + g.KJ;
     uint32_t hw[4], lw[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      float v0 = 0.0f, v1 = 0.0f;
-      if (ok) {
-        if (j8 + e < g.k) v0 = a.Z[((size_t)m * a.B + row) * g.k + j8 + e] * sc;
-        if (j8 + e + 1 < g.k) v1 = a.Z[((size_t)m * a.B + row) * g.k + j8 + e + 1] * sc;
-      }
+      const float v0 = j8 + e < g.k ? a.Z[((size_t)m * g.k + j8 + e) * a.B + row] * sc : 0.0f;
+      const float v1 = j8 + e + 1 < g.k ? a.Z[((size_t)m * g.k + j8 + e + 1) * a.B + row] * sc : 0.0f;
       const __half2 h2 = __floats2half2_rn(v0, v1);
       const float2 hf = __half22float2(h2);
       const __half2 l2 = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
       hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
       lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
     }
-    const int ci = tc::canon_idx(rr, jr, g.KJ);
-    *reinterpret_cast<uint4*>(zhi + ci) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    *reinterpret_cast<uint4*>(zlo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    *reinterpret_cast<uint4*>(zhi + jr) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(zlo + jr) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
 }
 
@@ -505,10 +625,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const Geo& g = a.g;
   const int KJ = g.KJ;
-  const size_t zt_bytes = (size_t)128 * KJ * 2;  // one fp16 Z tile (hi or lo)
-  __shared__ __align__(8) uint64_t zfull, full_b[ST2], empty[ST2], tfull[2], tempty[2];
+  const int nsl = KJ / KS2;                            // slabs per tile
+  constexpr int NAUX = 2 * D + 1;
+  constexpr size_t slab_bytes = (size_t)4 * NT2 * KS2;  // hi + lo of one slab
+  constexpr size_t x_bytes = (size_t)NT2 * AUXW * 4;    // aux rows of one tile
+  __shared__ __align__(8) uint64_t zready, full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2],
+      tempty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ float asum[128][1 + D];
+  __shared__ float asum[3][128][1 + D];
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row0 = blockIdx.x * 128;
@@ -518,15 +642,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   const int t_end = min(g.nt2, t_begin + a.tiles_per_split);
   const int ntile = max(0, t_end - t_begin);
   const uint8_t* tiles = a.tiles + (size_t)m * a.m_stride + ((size_t)jt * g.nt2) * g.t2_bytes;
-  uint8_t* zsm = sm;                       // Z hi | Z lo
-  uint8_t* bsm = sm + 2 * zt_bytes;        // stages
-  constexpr uint32_t NCOLS = 2 * NT2 < 32 ? 32 : 2 * NT2;
+  uint8_t* ssm = sm;                              // ST2 slab stages
+  uint8_t* xsm = ssm + ST2 * slab_bytes;          // STX2 aux stages
+  // TMEM columns: [0, 2*NT2) two accumulators, then Z hi (KJ/2 cols) and Z lo (KJ/2 cols)
+  constexpr uint32_t ZC = 2 * NT2;
+  constexpr uint32_t NCOLS = 512;
 
   if (tid == 0) {
-    tc::mbar_init(&zfull, 1);
+    tc::mbar_init(&zready, 32 * GEN_WARPS);
     for (int s = 0; s < ST2; ++s) {
-      tc::mbar_init(&full_b[s], 1);
-      tc::mbar_init(&empty[s], 1 + 32 * GEN_WARPS);  // MMA commit + every epilogue thread (aux reads)
+      tc::mbar_init(&full_s[s], 1);
+      tc::mbar_init(&empty_s[s], 1);
+    }
+    for (int s = 0; s < STX2; ++s) {
+      tc::mbar_init(&full_x[s], 1);
+      tc::mbar_init(&empty_x[s], 32 * GEN_WARPS);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
@@ -542,51 +672,81 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
 
   if (warp == 0) {
     if (lane == 0) {
-      const int rt = blockIdx.x;
-      const uint8_t* zsrc = a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * zt_bytes * 2;
-      tc::mbar_arrive_expect_tx(&zfull, (uint32_t)(2 * zt_bytes));
-      tc::bulk_g2s(zsm, zsrc, (uint32_t)(2 * zt_bytes), &zfull);
+      int q = 0;
       for (int i = 0; i < ntile; ++i) {
-        const int s = i % ST2;
-        const uint32_t ph = (uint32_t)(i / ST2) & 1u;
-        tc::mbar_wait(&empty[s], ph ^ 1u);
-        tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)g.t2_bytes);
-        tc::bulk_g2s(bsm + (size_t)s * g.t2_bytes, tiles + (size_t)(t_begin + i) * g.t2_bytes, (uint32_t)g.t2_bytes,
-                     &full_b[s]);
+        const uint8_t* src = tiles + (size_t)(t_begin + i) * g.t2_bytes;
+        for (int sl = 0; sl < nsl; ++sl, ++q) {
+          const int s = q % ST2;
+          tc::mbar_wait(&empty_s[s], ((uint32_t)(q / ST2) & 1u) ^ 1u);
+          tc::mbar_arrive_expect_tx(&full_s[s], (uint32_t)slab_bytes);
+          tc::bulk_g2s(ssm + (size_t)s * slab_bytes, src + (size_t)sl * slab_bytes, (uint32_t)slab_bytes, &full_s[s]);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      for (int i = 0; i < ntile; ++i) {
+        const int x = i % STX2;
+        tc::mbar_wait(&empty_x[x], ((uint32_t)(i / STX2) & 1u) ^ 1u);
+        tc::mbar_arrive_expect_tx(&full_x[x], (uint32_t)x_bytes);
+        tc::bulk_g2s(xsm + (size_t)x * x_bytes, tiles + (size_t)(t_begin + i) * g.t2_bytes + (size_t)4 * NT2 * KJ,
+                     (uint32_t)x_bytes, &full_x[x]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_f16(128, NT2);
-      const uint32_t SBO = (uint32_t)(KJ / 8) * 128u;
-      const uint32_t zhi = tc::smem_u32(zsm), zlo = zhi + (uint32_t)zt_bytes;
-      tc::mbar_wait(&zfull, 0);
+      constexpr uint32_t SBO = (KS2 / 8) * 128u;
+      const uint32_t zhi = tmem + ZC, zlo = tmem + ZC + (uint32_t)(KJ / 2);
+      tc::mbar_wait(&zready, 0);
+      tc::tc_fence_after();
+      int q = 0;
       for (int i = 0; i < ntile; ++i) {
-        const int s = i % ST2, b = i & 1;
-        const uint32_t ph = (uint32_t)(i / ST2) & 1u;
-        const uint32_t tph = (uint32_t)(i / 2) & 1u;
-        tc::mbar_wait(&tempty[b], tph ^ 1u);  // epilogue drained TMEM buffer b
-        tc::mbar_wait(&full_b[s], ph);
+        const int b = i & 1;
+        tc::mbar_wait(&tempty[b], ((uint32_t)(i / 2) & 1u) ^ 1u);  // epilogue drained accumulator b
         tc::tc_fence_after();
-        const uint32_t bhi = tc::smem_u32(bsm + (size_t)s * g.t2_bytes);
-        const uint32_t blo = bhi + (uint32_t)(NT2 * KJ * 2);
         const uint32_t d = tmem + (uint32_t)(b * NT2);
-        for (int ks = 0; ks < KJ / 16; ++ks) {
-          const uint32_t o = ks * 256u;
-          tc::mma_f16(d, tc::umma_desc(zhi + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, ks > 0 ? 1u : 0u);
-          tc::mma_f16(d, tc::umma_desc(zhi + o, 128, SBO), tc::umma_desc(blo + o, 128, SBO), idesc, 1u);
-          tc::mma_f16(d, tc::umma_desc(zlo + o, 128, SBO), tc::umma_desc(bhi + o, 128, SBO), idesc, 1u);
+        for (int sl = 0; sl < nsl; ++sl, ++q) {
+          const int s = q % ST2;
+          tc::mbar_wait(&full_s[s], (uint32_t)(q / ST2) & 1u);
+          tc::tc_fence_after();
+          const uint32_t sb = tc::smem_u32(ssm + (size_t)s * slab_bytes);
+          const uint64_t dbhi = tc::umma_desc(sb, 128, SBO);
+          const uint64_t dblo = tc::umma_desc(sb + (uint32_t)(NT2 * KS2 * 2), 128, SBO);
+#pragma unroll
+          for (int ks = 0; ks < KS2 / 16; ++ks) {
+            const uint64_t o = (uint64_t)(ks * 16);
+            const uint32_t ac = (uint32_t)(sl * (KS2 / 2) + ks * 8);
+            tc::mma_f16_ts(d, zhi + ac, dbhi + o, idesc, (sl > 0 || ks > 0) ? 1u : 0u);
+            tc::mma_f16_ts(d, zhi + ac, dblo + o, idesc, 1u);
+            tc::mma_f16_ts(d, zlo + ac, dbhi + o, idesc, 1u);
+          }
+          tc::umma_commit(&empty_s[s]);
         }
-        tc::umma_commit(&empty[s]);
         tc::umma_commit(&tfull[b]);
       }
     }
   } else {
-    // ------------------------------------------------ epilogue: sum_n (s w_n) ktilde_n [1 | X_n]
-    const int gt = tid - 64;
-    const int quarter = warp % 4, half = gt / 128;  // column half of the NT2 columns
+    const int quarter = warp % 4, cg = (warp - CTRL_WARPS) / 4;  // lane quarter, 32-column group
     const int r = quarter * 32 + lane;
     const int row = row0 + r;
+    // ---- Z hi/lo of this CTA's rows -> TMEM (8-word chunks dealt round-robin to the column groups)
+    {
+      const int rt = blockIdx.x;
+      const uint32_t* zrow = reinterpret_cast<const uint32_t*>(
+          a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * (size_t)128 * KJ * 2 * 2 +
+          (size_t)r * KJ * 2 * 2);  // KJ words: [hi KJ/2 words | lo KJ/2 words]
+      for (int w0 = cg * 8; w0 < KJ; w0 += 32) {
+        const uint4 q0 = *reinterpret_cast<const uint4*>(zrow + w0);
+        const uint4 q1 = *reinterpret_cast<const uint4*>(zrow + w0 + 4);
+        const uint32_t v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        tc::tmem_st8(tmem + ((uint32_t)(quarter * 32) << 16) + ZC + (uint32_t)w0, v);
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&zready);
+    }
+    // ------------------------------------------------ epilogue: sum_n (s w_n) ktilde_n [1 | X_n]
     float xq[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] * a.qscale[m][c] : 0.0f;
@@ -595,41 +755,45 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
 #pragma unroll
     for (int c = 0; c <= D; ++c) acc[c] = 0.0f;
     for (int i = 0; i < ntile; ++i) {
-      const int s = i % ST2, b = i & 1;
-      const uint32_t tph = (uint32_t)(i / 2) & 1u;
-      tc::mbar_wait(&tfull[b], tph);
+      const int b = i & 1, x = i % STX2;
+      tc::mbar_wait(&tfull[b], (uint32_t)(i / 2) & 1u);
       __syncwarp();
       tc::tc_fence_after();
-      float w[16];
-      tc::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * NT2 + half * 16), w);
+      float w[32];
+      const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * NT2 + cg * 32);
+      tmem_ld8(ta, w);
+      tmem_ld8(ta + 8, w + 8);
+      tmem_ld8(ta + 16, w + 16);
+      tmem_ld8(ta + 24, w + 24);
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[b]);
-      // stage s (its aux rows) stays resident until every epilogue thread has arrived on empty[s]
-      const float* aux = reinterpret_cast<const float*>(bsm + (size_t)s * g.t2_bytes + (size_t)4 * NT2 * KJ);
+      tc::mbar_wait(&full_x[x], (uint32_t)(i / STX2) & 1u);
+      const float* aux = reinterpret_cast<const float*>(xsm + (size_t)x * x_bytes);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const float* an = aux + (half * 16 + u) * AUXW;
+      for (int u = 0; u < 32; ++u) {
+        float an[NAUX];
+        load_aux<NAUX>(aux + (cg * 32 + u) * AUXW, an);
         float q = 0.0f;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
           const float df = xq[c] - an[c];
           q = fmaf(df, df, q);
         }
-        const float t = w[u] * an[2 * D] * exp2f(-q);
+        const float t = w[u] * an[2 * D] * ex2_approx(-q);
         acc[0] += t;
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[1 + c] = fmaf(t, an[D + c], acc[1 + c]);
       }
-      tc::mbar_arrive(&empty[s]);
+      tc::mbar_arrive(&empty_x[x]);
     }
-    // combine the two column halves of each row, undo the Z row scale
-    if (half == 1)
-      for (int c = 0; c <= D; ++c) asum[r][c] = acc[c];
+    // combine the four column groups of each row (fixed order), undo the Z row scale
+    if (cg > 0)
+      for (int c = 0; c <= D; ++c) asum[cg - 1][r][c] = acc[c];
     asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS));
-    if (half == 0 && row < a.B) {
+    if (cg == 0 && row < a.B) {
       float* o = a.P2 + (((size_t)(split * g.njt + jt) * a.m_count + m) * a.B + row) * P2_LD;
-      for (int c = 0; c <= D; ++c) o[c] = (acc[c] + asum[r][c]) * zinv;
+      for (int c = 0; c <= D; ++c) o[c] = (((acc[c] + asum[0][r][c]) + asum[1][r][c]) + asum[2][r][c]) * zinv;
     }
   }
   tc::tc_fence_before();
@@ -658,8 +822,13 @@ namespace {
 
 Geo geo_of(const bagel_ctx* c) { return make_geo(c->N, c->d, c->p, c->k); }
 
-size_t p1_smem(const Geo& g) { return (size_t)ST1 * (2 * (size_t)128 * KT1 * 2 + g.t1_bytes); }
-size_t p2_smem(const Geo& g) { return 2 * (size_t)128 * g.KJ * 2 + (size_t)ST2 * g.t2_bytes; }
+size_t p1_smem(const Geo& g) {
+  return (size_t)ST1 * (2 * (size_t)128 * KT1 * 2 + (size_t)4 * g.NZ * KT1) + (size_t)STA * KT1 * AUXW * 4;
+}
+size_t p2_smem(const Geo& g) {
+  (void)g;
+  return (size_t)ST2 * 4 * NT2 * KS2 + (size_t)STX2 * NT2 * AUXW * 4;
+}
 
 }  // namespace
 
@@ -695,11 +864,11 @@ void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, in
   const Geo g = geo_of(c);
   const int rt = cdiv(B, 128);
   const int target = c->num_sms;  // one CTA per SM (smem-bound), one wave
-  int s1 = cdiv(target, rt * g.p * g.nct);
+  int s1 = target / (rt * g.p * g.nct);  // floor: never more CTAs than SMs (one wave)
   s1 = s1 < 1 ? 1 : (s1 > g.nt1 ? g.nt1 : s1);
   *tps1 = cdiv(g.nt1, s1);
   *S1 = cdiv(g.nt1, *tps1);
-  int s2 = cdiv(target, rt * g.p * g.njt);
+  int s2 = target / (rt * g.p * g.njt);
   s2 = s2 < 1 ? 1 : (s2 > g.nt2 ? g.nt2 : s2);
   *tps2 = cdiv(g.nt2, s2);
   *S2 = cdiv(g.nt2, *tps2);
@@ -714,6 +883,7 @@ size_t tc_zp_bytes(const bagel_ctx* c, int B) {
   return (size_t)g.p * cdiv(B, 128) * g.njt * 128 * g.KJ * 2 * 2;
 }
 int tc_njt(const bagel_ctx* c) { return geo_of(c).njt; }
+size_t tc_zpart_count(const bagel_ctx* c, int B) { return (size_t)c->p * cdiv(c->k, R1_JG) * B; }
 
 static void set_attrs() {
   static bool done = false;
@@ -721,8 +891,8 @@ static void set_attrs() {
   done = true;
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
-      cudaFuncSetAttribute(k_p1_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      cudaFuncSetAttribute(k_p2_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      bagel_set_smem_attr(k_p1_tc<D>, 220 * 1024);
+      bagel_set_smem_attr(k_p2_tc<D>, 220 * 1024);
     }));
   }
 }
@@ -770,9 +940,9 @@ int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, fl
   a.var = c->ws.var;
   a.jmu = jmu_out;
   a.sig = sig_out;
-  dim3 grid(cdiv(B, 32), c->p);
-  DISPATCH_D(c->d, (k_r1_tc<D><<<grid, 256, 0, st>>>(a)));
-  return 1;
+  k_r1a_tc<<<dim3(cdiv(B, 32), c->p, cdiv(c->k, R1_JG)), 256, 0, st>>>(a, T.zz_part, T.zmax_part);
+  DISPATCH_D(c->d, (k_r1b_tc<D><<<dim3(cdiv(B, 32), c->p), 256, 0, st>>>(a, T.zz_part, T.zmax_part)));
+  return 2;
 }
 
 int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {

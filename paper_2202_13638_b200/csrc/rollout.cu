@@ -14,7 +14,7 @@
 
 namespace {
 
-constexpr int EPI_ROWS = 32, EPI_THREADS = 256;
+constexpr int EPI_ROWS = 8;
 constexpr int REV_ROWS = 8, REV_THREADS = 256;
 constexpr int P2_LD = 1 + BAGEL_MAX_D;
 
@@ -52,25 +52,48 @@ __device__ void phi_rows(const PolicyDesc& P, int p, const float* x, const float
 }
 
 // h_{l+1} = tanh(W_l h_l + b_l) for every layer (block-cooperative; act in smem).
-__device__ void mlp_forward_rows(const PolicyDesc& P, const float* __restrict__ theta, int nrows, float* act) {
+// thetaT holds every W_l transposed (Wt[i][o], same offsets as theta) so that the
+// threads of a warp (consecutive o) read consecutive weights: coalesced, L1-resident.
+__device__ void mlp_forward_rows(const PolicyDesc& P, const float* __restrict__ thetaT, int nrows, float* act) {
   int off_in = 0;
   for (int l = 0; l < P.n_layers; ++l) {
     const int in = P.sizes[l], out = P.sizes[l + 1];
     const int off_out = off_in + in;
-    const float* W = theta + P.w_off[l];
-    const float* bb = theta + P.b_off[l];
+    const float* Wt = thetaT + P.w_off[l];
+    const float* bb = thetaT + P.b_off[l];
     __syncthreads();
     for (int idx = threadIdx.x; idx < nrows * out; idx += blockDim.x) {
       const int r = idx / out, o = idx % out;
       const float* h = act + r * P.act_total + off_in;
-      const float* w = W + (size_t)o * in;
-      float a = __ldg(bb + o);
-      for (int i = 0; i < in; ++i) a = fmaf(__ldg(w + i), h[i], a);
-      act[r * P.act_total + off_out + o] = tanhf(a);
+      float a0 = bb[o], a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;  // 4 independent chains (ILP)
+      int i = 0;
+      for (; i + 4 <= in; i += 4) {
+        a0 = fmaf(Wt[(size_t)i * out + o], h[i], a0);
+        a1 = fmaf(Wt[(size_t)(i + 1) * out + o], h[i + 1], a1);
+        a2 = fmaf(Wt[(size_t)(i + 2) * out + o], h[i + 2], a2);
+        a3 = fmaf(Wt[(size_t)(i + 3) * out + o], h[i + 3], a3);
+      }
+      for (; i < in; ++i) a0 = fmaf(Wt[(size_t)i * out + o], h[i], a0);
+      act[r * P.act_total + off_out + o] = tanhf((a0 + a1) + (a2 + a3));
     }
     off_in = off_out;
   }
   __syncthreads();
+}
+
+// thetaT: per layer W_l^T (in x out), biases copied.
+__global__ void k_transpose_theta(PolicyDesc P, const float* __restrict__ theta, float* __restrict__ thetaT) {
+  for (int l = 0; l < P.n_layers; ++l) {
+    const int in = P.sizes[l], out = P.sizes[l + 1];
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < in * out + out; idx += gridDim.x * blockDim.x) {
+      if (idx < in * out) {
+        const int i = idx / out, o = idx % out;
+        thetaT[P.w_off[l] + idx] = theta[P.w_off[l] + o * in + i];
+      } else {
+        thetaT[P.b_off[l] + idx - in * out] = theta[P.b_off[l] + idx - in * out];
+      }
+    }
+  }
 }
 
 template <int D>
@@ -84,89 +107,208 @@ __device__ void write_xstar(const PolicyDesc& P, int p, const float* act, int nr
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(EPI_THREADS) k_init(PolicyDesc P, RewardDesc rw, int p,
-                                                      const float* __restrict__ theta,
-                                                      const float* __restrict__ x0,
-                                                      const float* __restrict__ goals, int B,
-                                                      float* __restrict__ tape_x0, double* __restrict__ G,
-                                                      float* __restrict__ xstar) {
-  extern __shared__ float act[];
-  const int row0 = blockIdx.x * EPI_ROWS;
-  const int valid = min(EPI_ROWS, B - row0);
-  for (int r = threadIdx.x; r < valid; r += blockDim.x) {
-    const int b = row0 + r;
-    G[b] = (double)reward_fn(rw, x0 + (size_t)b * p, goals + (size_t)b * p, p);
-    for (int c = 0; c < p; ++c) tape_x0[(size_t)b * p + c] = x0[(size_t)b * p + c];
+// ---------------------------------------------------------------- warp-per-rows policy forward
+// The block stages thetaT (every W_l transposed, Wt[i][o], plus biases) in shared memory once;
+// each warp then evaluates u = pi(x, g) for RPW rows at a time: lanes own output units
+// o = lane + 32 k, activations live in a per-warp shared buffer.  No block-wide barrier after
+// the staging.
+constexpr int WARP_ROWS_BLOCK = 4;  // warps per block
+constexpr int RPW = 2;              // rows per warp
+constexpr int ROWS_BLOCK = WARP_ROWS_BLOCK * RPW;
+
+__device__ void stage_theta(const PolicyDesc& P, const float* __restrict__ thetaT, float* th_s) {
+  const int n4 = P.n_params / 4;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x)
+    reinterpret_cast<float4*>(th_s)[i] = __ldg(reinterpret_cast<const float4*>(thetaT) + i);
+  for (int i = 4 * n4 + threadIdx.x; i < P.n_params; i += blockDim.x) th_s[i] = __ldg(thetaT + i);
+  __syncthreads();
+}
+
+// rows r < nr of this warp: x[r], g[r] (p each); u_out[r] (q each).  buf: RPW x 2 x BAGEL_MAX_WIDTH
+__device__ void warp_policy(const PolicyDesc& P, int p, const float* th_s, const float* x, const float* g, int nr,
+                            float* buf, float* u_out) {
+  const int lane = threadIdx.x % 32;
+  constexpr int W2 = 2 * BAGEL_MAX_WIDTH;
+  for (int r = 0; r < RPW; ++r)
+    for (int i = lane; i < P.sizes[0]; i += 32) {
+      float v = 0.0f;
+      if (r < nr) {
+        const float* xr = x + r * p;
+        const float* gr = g + r * p;
+        if (i < p) v = xr[i];
+        else if (i < 2 * p) v = gr[i - p];
+        else v = gr[i - 2 * p] - xr[i - 2 * p];
+      }
+      buf[r * W2 + i] = v;
+    }
+  __syncwarp();
+  int cur = 0;
+  for (int l = 0; l < P.n_layers; ++l) {
+    const int in = P.sizes[l], out = P.sizes[l + 1];
+    const float* Wt = th_s + P.w_off[l];
+    const float* bb = th_s + P.b_off[l];
+    const int nxt = BAGEL_MAX_WIDTH - cur;
+    if (out >= 16) {
+      // lanes over output units; 2 interleaved chains per row
+      for (int o = lane; o < out; o += 32) {
+        float acc[RPW][2];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          acc[r][0] = bb[o];
+          acc[r][1] = 0.0f;
+        }
+        int i = 0;
+        for (; i + 2 <= in; i += 2) {
+          const float w0 = Wt[i * out + o], w1 = Wt[(i + 1) * out + o];
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) {
+            acc[r][0] = fmaf(w0, buf[r * W2 + cur + i], acc[r][0]);
+            acc[r][1] = fmaf(w1, buf[r * W2 + cur + i + 1], acc[r][1]);
+          }
+        }
+        if (i < in) {
+          const float w0 = Wt[i * out + o];
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) acc[r][0] = fmaf(w0, buf[r * W2 + cur + i], acc[r][0]);
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) buf[r * W2 + nxt + o] = tanhf(acc[r][0] + acc[r][1]);
+      }
+    } else {
+      // narrow layer (e.g. the action head): lanes over inputs, butterfly reduction
+      for (int o = 0; o < out; ++o) {
+        float acc[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) acc[r] = 0.0f;
+        for (int i = lane; i < in; i += 32) {
+          const float wv = Wt[i * out + o];
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) acc[r] = fmaf(wv, buf[r * W2 + cur + i], acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+          for (int sh = 16; sh > 0; sh >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], sh);
+          if (lane == 0) buf[r * W2 + nxt + o] = tanhf(acc[r] + bb[o]);
+        }
+      }
+    }
+    __syncwarp();
+    cur = nxt;
   }
-  phi_rows(P, p, x0 + (size_t)row0 * p, goals + (size_t)row0 * p, EPI_ROWS, valid, act);
-  mlp_forward_rows(P, theta, EPI_ROWS, act);
-  write_xstar<D>(P, p, act, EPI_ROWS, row0, B, xstar, x0 + (size_t)row0 * p);
+  const int q = P.sizes[P.n_layers];
+  for (int r = 0; r < nr; ++r)
+    for (int o = lane; o < q; o += 32) u_out[r * BAGEL_MAX_D + o] = buf[r * W2 + cur + o];
+  __syncwarp();
+}
+
+size_t policy_smem(const PolicyDesc& P) {
+  return sizeof(float) * (((P.n_params + 3) & ~3) + (size_t)WARP_ROWS_BLOCK * RPW * 2 * BAGEL_MAX_WIDTH);
 }
 
 template <int D>
-__global__ void __launch_bounds__(EPI_THREADS) k_epilogue(
-    PolicyDesc P, RewardDesc rw, GpDesc g, const float* __restrict__ theta, const float* __restrict__ goals,
+__global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_init(PolicyDesc P, RewardDesc rw, int p,
+                                                              const float* __restrict__ thetaT,
+                                                              const float* __restrict__ x0,
+                                                              const float* __restrict__ goals, int B,
+                                                              float* __restrict__ tape_x0, double* __restrict__ G,
+                                                              float* __restrict__ xstar) {
+  extern __shared__ __align__(16) float sm[];
+  float* th_s = sm;
+  float* bufs = sm + ((P.n_params + 3) & ~3);
+  __shared__ float us[WARP_ROWS_BLOCK][RPW][BAGEL_MAX_D];
+  stage_theta(P, thetaT, th_s);
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
+  if (b0 >= B) return;  // warp-uniform
+  const int nr = min(RPW, B - b0);
+  const float* x = x0 + (size_t)b0 * p;
+  const float* g = goals + (size_t)b0 * p;
+  if (lane < nr) G[b0 + lane] = (double)reward_fn(rw, x + lane * p, g + lane * p, p);
+  for (int i = lane; i < nr * p; i += 32) tape_x0[(size_t)b0 * p + i] = x[i];
+  warp_policy(P, p, th_s, x, g, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0]);
+  for (int i = lane; i < nr * D; i += 32) {
+    const int r = i / D, c = i % D;
+    xstar[(size_t)(b0 + r) * D + c] = c < p ? x[r * p + c] : us[w][r][c - p];
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(
+    PolicyDesc P, RewardDesc rw, GpDesc g, const float* __restrict__ thetaT, const float* __restrict__ goals,
     int B, int t, int S2, const float* __restrict__ P2, const float* __restrict__ mu,
     const float* __restrict__ var, const float* __restrict__ tape_x_t, const float* __restrict__ sig_t,
     float* __restrict__ jv_t, float* __restrict__ tape_x_next, double* __restrict__ G,
     float* __restrict__ xstar, uint64_t seed, long long traj_offset, int policy_next,
     int* __restrict__ err_flag, float* __restrict__ trace_mu, float* __restrict__ trace_var) {
-  extern __shared__ float act[];
-  __shared__ float xn_s[EPI_ROWS * BAGEL_MAX_P];
+  extern __shared__ __align__(16) float sm[];
+  float* th_s = sm;
+  float* bufs = sm + ((P.n_params + 3) & ~3);
+  __shared__ float us[WARP_ROWS_BLOCK][RPW][BAGEL_MAX_D];
+  __shared__ float xn_s[WARP_ROWS_BLOCK][RPW * BAGEL_MAX_P];
+  if (policy_next) stage_theta(P, thetaT, th_s);
   const int p = g.p;
-  const int row0 = blockIdx.x * EPI_ROWS;
-  const int valid = min(EPI_ROWS, B - row0);
-  for (int r = threadIdx.x; r < valid; r += blockDim.x) {
-    const int b = row0 + r;
-    const float4 e4 = bagel_rollout_eps4(seed, (uint32_t)(traj_offset + b), (uint32_t)t);
-    float xn[BAGEL_MAX_P];
-    bool finite = true;
-    for (int m = 0; m < p; ++m) {
-      float sums[1 + D];
-#pragma unroll
-      for (int c = 0; c <= D; ++c) sums[c] = 0.0f;
-      for (int s = 0; s < S2; ++s) {
-        const float* src = P2 + ((size_t)(s * p + m) * B + b) * P2_LD;
-#pragma unroll
-        for (int c = 0; c <= D; ++c) sums[c] += src[c];
-      }
-      const float* xs = xstar + (size_t)b * D;
-#pragma unroll
-      for (int c = 0; c < D; ++c)
-        jv_t[((size_t)b * p + m) * D + c] = 2.0f * g.ell2inv[m][c] * (xs[c] * sums[0] - sums[1 + c]);
-      const float sg = fabsf(sig_t[(size_t)b * p + m]);
-      const float mum = mu[(size_t)m * B + b];
-      xn[m] = tape_x_t[(size_t)b * p + m] + mum + sg * bagel_f4get(e4, m & 3);
-      finite = finite && isfinite(xn[m]);
-      if (trace_mu) trace_mu[(size_t)b * p + m] = mum;
-      if (trace_var) trace_var[(size_t)b * p + m] = var[(size_t)m * B + b];
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
+  if (b0 >= B) return;  // warp-uniform
+  const int nr = min(RPW, B - b0);
+  // lane = r * p * (D + 1) + m * (D + 1) + c: pass-2 partial of (row r, output m, column c)
+  const int per_row = p * (D + 1);
+  const int nl = nr * per_row;  // <= 2 * 4 * 9 = 72 > 32 possible: loop
+  for (int base = 0; base < RPW * per_row; base += 32) {
+    const int li = base + lane;
+    const bool act = li < nl;
+    const int r = act ? li / per_row : 0, m = act ? (li % per_row) / (D + 1) : 0, c = act ? li % (D + 1) : 0;
+    const int b = b0 + r;
+    float part = 0.0f;
+    if (act)
+      for (int s = 0; s < S2; ++s) part += P2[((size_t)(s * p + m) * B + b) * P2_LD + c];
+    // the c = 0 partial (sum w k) of the same (r, m) sits at lane li - c (same 32-lane window
+    // only when aligned; fetch it from global instead to keep lanes independent)
+    float s0 = part;
+    if (act && c > 0) {
+      s0 = 0.0f;
+      for (int s = 0; s < S2; ++s) s0 += P2[((size_t)(s * p + m) * B + b) * P2_LD];
+      jv_t[((size_t)b * p + m) * D + c - 1] = 2.0f * g.ell2inv[m][c - 1] * (xstar[(size_t)b * D + c - 1] * s0 - part);
     }
-    if (!finite) atomicMin(err_flag, t * B + b);
-    for (int m = 0; m < p; ++m) {
-      tape_x_next[(size_t)b * p + m] = xn[m];
-      xn_s[r * p + m] = xn[m];
-    }
-    G[b] += (double)reward_fn(rw, xn, goals + (size_t)b * p, p);
   }
-  if (!policy_next) return;  // uniform
-  __syncthreads();
-  phi_rows(P, p, xn_s, goals + (size_t)row0 * p, EPI_ROWS, valid, act);
-  mlp_forward_rows(P, theta, EPI_ROWS, act);
-  write_xstar<D>(P, p, act, EPI_ROWS, row0, B, xstar, xn_s);
+  if (lane < nr * p) {
+    const int r = lane / p, m = lane % p, b = b0 + r;
+    const float4 e4 = bagel_rollout_eps4(seed, (uint32_t)(traj_offset + b), (uint32_t)t);
+    const float sg = fabsf(sig_t[(size_t)b * p + m]);
+    const float mum = mu[(size_t)m * B + b];
+    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * bagel_f4get(e4, m & 3);
+    if (!isfinite(xn)) atomicMin(err_flag, t * B + b);
+    tape_x_next[(size_t)b * p + m] = xn;
+    xn_s[w][r * p + m] = xn;
+    if (trace_mu) trace_mu[(size_t)b * p + m] = mum;
+    if (trace_var) trace_var[(size_t)b * p + m] = var[(size_t)m * B + b];
+  }
+  __syncwarp();
+  const float* gb = goals + (size_t)b0 * p;
+  if (lane < nr) G[b0 + lane] += (double)reward_fn(rw, &xn_s[w][lane * p], gb + lane * p, p);
+  if (!policy_next) return;
+  warp_policy(P, p, th_s, xn_s[w], gb, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0]);
+  for (int i = lane; i < nr * D; i += 32) {
+    const int r = i / D, c = i % D;
+    xstar[(size_t)(b0 + r) * D + c] = c < p ? xn_s[w][r * p + c] : us[w][r][c - p];
+  }
 }
 
 // ------------------------------------------------------------------ reverse
 // smem: gacc[n_params] | act[REV_ROWS x act_total] | dl[2][REV_ROWS x max_width] | xbar | xsbar
 template <int D>
 __global__ void __launch_bounds__(REV_THREADS) k_reverse(
-    PolicyDesc P, RewardDesc rw, int p, const float* __restrict__ theta, const float* __restrict__ goals,
-    int B, int T, const float* __restrict__ tape_x, const float* __restrict__ tape_sig,
+    PolicyDesc P, RewardDesc rw, int p, const float* __restrict__ theta, const float* __restrict__ thetaT,
+    const float* __restrict__ goals, int B, int T, const float* __restrict__ tape_x, const float* __restrict__ tape_sig,
     const float* __restrict__ tape_jmu, const float* __restrict__ tape_jv, uint64_t seed,
     long long traj_offset, float invB, float* __restrict__ theta_part) {
-  extern __shared__ float sm[];
-  float* gacc = sm;
-  float* act = gacc + ((P.n_params + 3) & ~3);
+  extern __shared__ __align__(16) float sm[];
+  const int np4 = (P.n_params + 3) & ~3;
+  float* th_s = sm;                 // theta (W_l row-major) for h-bar = W^T delta
+  float* thT_s = th_s + np4;        // theta^T for the forward recompute
+  float* gacc = thT_s + np4;
+  float* act = gacc + np4;
   float* dl0 = act + REV_ROWS * P.act_total;
   float* dl1 = dl0 + REV_ROWS * P.max_width;
   float* xbar = dl1 + REV_ROWS * P.max_width;  // REV_ROWS x p
@@ -177,7 +319,11 @@ __global__ void __launch_bounds__(REV_THREADS) k_reverse(
   const int row0 = blockIdx.x * REV_ROWS;
   const int valid = min(REV_ROWS, B - row0);
   const float inv_sr2 = 2.0f * rw.inv_two_sr2;
-  for (int i = tid; i < P.n_params; i += blockDim.x) gacc[i] = 0.0f;
+  for (int i = tid; i < P.n_params; i += blockDim.x) {
+    gacc[i] = 0.0f;
+    th_s[i] = __ldg(theta + i);
+    thT_s[i] = __ldg(thetaT + i);
+  }
   for (int i = tid; i < REV_ROWS * p; i += blockDim.x) {
     const int r = i / p, c = i % p;
     gs[i] = r < valid ? goals[(size_t)(row0 + r) * p + c] : 0.0f;
@@ -217,7 +363,7 @@ __global__ void __launch_bounds__(REV_THREADS) k_reverse(
       }
     }
     phi_rows(P, p, xt, gs, REV_ROWS, valid, act);
-    mlp_forward_rows(P, theta, REV_ROWS, act);  // ends with __syncthreads
+    mlp_forward_rows(P, thT_s, REV_ROWS, act);  // ends with __syncthreads
     // delta_L = ubar (1 - u^2)
     {
       const int q = P.sizes[L];
@@ -234,7 +380,7 @@ __global__ void __launch_bounds__(REV_THREADS) k_reverse(
       __syncthreads();
       const int in = P.sizes[l], out = P.sizes[l + 1];
       off_in -= in;
-      const float* W = theta + P.w_off[l];
+      const float* W = th_s + P.w_off[l];
       // theta-bar: W_l[o][i] += sum_r delta[r][o] h_l[r][i];  b_l[o] += sum_r delta[r][o]
       for (int idx = tid; idx < out * in + out; idx += blockDim.x) {
         float a = 0.0f;
@@ -253,8 +399,16 @@ __global__ void __launch_bounds__(REV_THREADS) k_reverse(
       // h-bar_l = W_l^T delta; delta_{l-1} = h-bar (1 - h^2) for hidden layers
       for (int idx = tid; idx < REV_ROWS * in; idx += blockDim.x) {
         const int r = idx / in, i = idx % in;
-        float a = 0.0f;
-        for (int o = 0; o < out; ++o) a = fmaf(__ldg(W + (size_t)o * in + i), dcur[r * P.max_width + o], a);
+        float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+        int o = 0;
+        for (; o + 4 <= out; o += 4) {
+          a0 = fmaf(W[(size_t)o * in + i], dcur[r * P.max_width + o], a0);
+          a1 = fmaf(W[(size_t)(o + 1) * in + i], dcur[r * P.max_width + o + 1], a1);
+          a2 = fmaf(W[(size_t)(o + 2) * in + i], dcur[r * P.max_width + o + 2], a2);
+          a3 = fmaf(W[(size_t)(o + 3) * in + i], dcur[r * P.max_width + o + 3], a3);
+        }
+        for (; o < out; ++o) a0 = fmaf(W[(size_t)o * in + i], dcur[r * P.max_width + o], a0);
+        float a = (a0 + a1) + (a2 + a3);
         if (l > 0) {
           const float h = act[r * P.act_total + off_in + i];
           a *= (1.0f - h * h);
@@ -348,9 +502,10 @@ size_t epi_smem(const PolicyDesc& P) { return sizeof(float) * EPI_ROWS * P.act_t
 }  // namespace
 
 size_t ro_reverse_smem(const PolicyDesc& P) {
-  return sizeof(float) * (((P.n_params + 3) & ~3) + REV_ROWS * P.act_total + 2 * REV_ROWS * P.max_width +
+  return sizeof(float) * (3 * ((P.n_params + 3) & ~3) + REV_ROWS * P.act_total + 2 * REV_ROWS * P.max_width +
                           REV_ROWS * BAGEL_MAX_P + REV_ROWS * BAGEL_MAX_D);
 }
+size_t ro_policy_smem(const PolicyDesc& P) { return policy_smem(P); }
 size_t ro_epilogue_smem(const PolicyDesc& P) { return epi_smem(P); }
 int ro_reverse_block_rows() { return REV_ROWS; }
 
@@ -360,9 +515,10 @@ void ro_set_attributes() {
   done = true;
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
-      cudaFuncSetAttribute(k_reverse<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_epilogue<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(k_init<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      bagel_set_smem_attr(k_reverse<D>, 200 * 1024);
+      bagel_set_smem_attr(k_epilogue<D>, 200 * 1024);
+      bagel_set_smem_attr(k_init<D>, 200 * 1024);
+
     }));
   }
 }
@@ -370,9 +526,10 @@ void ro_set_attributes() {
 int ro_init(const bagel_ctx* c, const float* theta, const float* x0, const float* goals, int B,
             cudaStream_t st) {
   ro_set_attributes();
-  DISPATCH_D(c->gp.d, (k_init<D><<<cdiv(B, EPI_ROWS), EPI_THREADS, epi_smem(c->pol), st>>>(
-                          c->pol, c->rw, c->gp.p, theta, x0, goals, B, c->ws.tape_x, c->ws.G, c->ws.xstar)));
-  return 1;
+  k_transpose_theta<<<cdiv(c->pol.n_params, 256), 256, 0, st>>>(c->pol, theta, c->ws.thetaT);
+  DISPATCH_D(c->gp.d, (k_init<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
+                          c->pol, c->rw, c->gp.p, c->ws.thetaT, x0, goals, B, c->ws.tape_x, c->ws.G, c->ws.xstar)));
+  return 2;
 }
 
 int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, int T,
@@ -381,8 +538,8 @@ int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals,
   (void)T;
   const int p = c->gp.p, d = c->gp.d;
   const Workspace& w = c->ws;
-  DISPATCH_D(d, (k_epilogue<D><<<cdiv(B, EPI_ROWS), EPI_THREADS, epi_smem(c->pol), st>>>(
-                    c->pol, c->rw, c->gp, theta, goals, B, t, w.S2eff, w.P2, w.mu, w.var,
+  DISPATCH_D(d, (k_epilogue<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
+                    c->pol, c->rw, c->gp, w.thetaT, goals, B, t, w.S2eff, w.P2, w.mu, w.var,
                     w.tape_x + (size_t)t * B * p, w.tape_sig + (size_t)t * B * p,
                     w.tape_jv + (size_t)t * B * p * d, w.tape_x + (size_t)(t + 1) * B * p, w.G, w.xstar,
                     seed, traj_offset, policy_next ? 1 : 0, w.err_flag, trace_mu, trace_var)));
@@ -396,7 +553,7 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
   *nblk_out = nblk;
   const Workspace& w = c->ws;
   DISPATCH_D(c->gp.d, (k_reverse<D><<<nblk, REV_THREADS, ro_reverse_smem(c->pol), st>>>(
-                          c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_sig, w.tape_jmu,
+                          c->pol, c->rw, c->gp.p, theta, w.thetaT, goals, B, T, w.tape_x, w.tape_sig, w.tape_jmu,
                           w.tape_jv, seed, traj_offset, (float)(1.0 / (double)B_global), w.theta_part)));
   return 1;
 }

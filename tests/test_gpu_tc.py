@@ -27,19 +27,24 @@ def ctx():
     return bagel.Context(0)
 
 
-def _run(ctx, A16, B16):
+def _run(ctx, A16, B16, mode=0):
     N, K = B16.shape
-    a = torch.from_numpy(pack(A16).view(np.int16)).cuda()
+    a16 = pack(A16) if mode == 0 else np.ascontiguousarray(A16)
+    a = torch.from_numpy(a16.view(np.int16).reshape(-1)).cuda()
     b = torch.from_numpy(pack(B16).view(np.int16)).cuda()
-    return ctx.tc_selftest(a, b, N, K).cpu().numpy().astype(np.float64)
+    return ctx.tc_selftest(a, b, N, K, mode).cpu().numpy().astype(np.float64)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("N,K", [(256, 64), (16, 16), (128, 128), (32, 512), (272 - 16, 32)])
-def test_single_mma_matches_exact_products(ctx, N, K):
+def test_single_mma_matches_exact_products(ctx, N, K, mode):
+    """mode 0: A and B from shared memory; mode 1: A from TMEM (TS form)."""
+    if mode == 1 and N + K // 2 > 512:
+        pytest.skip("TMEM columns")
     rng = np.random.default_rng(N * 1000 + K)
     A = rng.uniform(-1, 1, (128, K)).astype(np.float16)
     B = rng.uniform(-1, 1, (N, K)).astype(np.float16)
-    D = _run(ctx, A, B)
+    D = _run(ctx, A, B, mode)
     ref = A.astype(np.float64) @ B.astype(np.float64).T
     scale = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64)).T
     assert np.all(np.abs(D - ref) <= 4 * K * 2.0 ** -24 * scale + 1e-30)
