@@ -206,6 +206,11 @@ int bagel_get_gp_kernel(const bagel_ctx* ctx, int* version);
  * (128 + N) K 2 bytes <= 200 KB.  Errors: E_ARG, E_CUDA. */
 int bagel_tc_selftest(bagel_ctx* ctx, const void* A, const void* B, int N, int K, int mode, float* D);
 
+/* Debug copy of an internal per-step buffer into host memory dst [host] (bytes <= its size):
+ * 0 pass-1 mean-column partials, 1 pass-1 z partials, 2 pass-2 partials, 3 step means.
+ * Layouts are internal (csrc/gp_step_tc.cu).  Errors: E_ARG. */
+int bagel_debug_buffer(bagel_ctx* ctx, int which, void* dst, size_t bytes);
+
 /* Tensor-core issue-rate microbenchmark: `ctas` CTAs (one per SM) each issue `iters`
  * back-to-back tcgen05.mma (M = 128, N, K = 16; mode 0: A from shared memory, 1: A from
  * TMEM) and write the elapsed SM cycles to cycles [dev] (ctas int64).  Errors: E_ARG. */

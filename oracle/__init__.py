@@ -79,7 +79,7 @@ def lib():
             L.orc_reward_fn.restype = C.c_double
             L.orc_rollout.argtypes = [C.POINTER(GP), C.POINTER(Policy), C.POINTER(Reward), _dp, _dp,
                                       C.c_int, C.c_int, C.c_uint64, C.c_longlong, C.c_longlong,
-                                      C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
+                                      C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_uint64]
             L.orc_rollout.restype = C.c_int
             L.orc_num_threads.restype = C.c_int
             L.orc_set_num_threads.argtypes = [C.c_int]
@@ -215,8 +215,10 @@ def reward(Q, sigma_r, x, g) -> float:
 
 
 def rollout(model: Model, sizes, phi_mode, theta, Q, sigma_r, x0, goals, T, seed, traj_offset=0,
-            B_global=None, eps_mode=0, want_grad=True, trace=False):
-    """Returns dict(cost, grad, ret, [x, mu, var]).  phi_mode: 'xg' or 'xgd'."""
+            B_global=None, eps_mode=0, want_grad=True, trace=False, perturb_mode=0, perturb_seed=0):
+    """Returns dict(cost, grad, ret, [x, mu, var]).  phi_mode: 'xg' or 'xgd'.
+    perturb_mode (fp32-sensitivity mode): 0 exact; 1 every kernel value x (1 + U(+-2^-22));
+    2 only the mean path (mu, J^mu); 3 only the variance path (z, J^v)."""
     x0, goals, theta, Q = _d(x0), _d(goals), _d(theta), _d(Q)
     B, p = x0.shape
     if B_global is None:
@@ -233,7 +235,8 @@ def rollout(model: Model, sizes, phi_mode, theta, Q, sigma_r, x0, goals, T, seed
     tv = np.zeros((T, B, p)) if trace else None
     rc = lib().orc_rollout(C.byref(model.struct), C.byref(pol), C.byref(rw), _ptr(x0), _ptr(goals), B, T,
                            int(seed), int(traj_offset), int(B_global), int(eps_mode), int(bool(want_grad)),
-                           C.byref(cost), _ptr(grad), _ptr(tx), _ptr(tm), _ptr(tv), _ptr(ret))
+                           C.byref(cost), _ptr(grad), _ptr(tx), _ptr(tm), _ptr(tv), _ptr(ret),
+                           int(perturb_mode), int(perturb_seed))
     if rc != 0:
         t, b = divmod(rc - 1, B)
         raise FloatingPointError(f"oracle rollout: non-finite state at step {t}, row {b}")

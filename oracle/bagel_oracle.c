@@ -360,20 +360,64 @@ typedef struct {
     const double* R;     /* p x k x N */
 } orc_gp;
 
-static void orc_query(const orc_gp* gp, int m, const double* x, double* scratch, double* mean,
-                      double* var, double* jmu, double* jv, double* mbound, double* vbound)
+/* fp32-sensitivity mode (variant (a)): every kernel value entering the
+ * mean path (mu, J^mu; mode 1 or 2) and/or the variance path (z, J^v; mode 1 or 3) is
+ * multiplied by (1 + delta), delta ~ U(-2^-22, 2^-22) from a Philox stream keyed by `seed`
+ * with counter (b_global, t, m * N + n, 5 | 6).  It measures the parity floor any fp32
+ * implementation can reach on a problem; mode 0 is the exact oracle. */
+typedef struct {
+    int mode;
+    uint64_t seed;
+    uint32_t b, t;
+} orc_perturb;
+
+static double orc_delta(const orc_perturb* pt, int m, int N, int n, uint32_t stream)
+{
+    uint32_t key[2] = {(uint32_t)(pt->seed & 0xffffffffu), (uint32_t)(pt->seed >> 32)};
+    uint32_t ctr[4] = {pt->b, pt->t, (uint32_t)(m * N + n), stream};
+    uint32_t o[4];
+    orc_philox4x32_10(ctr, key, o);
+    return (orc_uniform(o[0]) * 2.0 - 1.0) * (1.0 / 4194304.0); /* U(-2^-22, 2^-22) */
+}
+
+static void orc_query_p(const orc_gp* gp, int m, const double* x, double* scratch, double* mean,
+                        double* var, double* jmu, double* jv, double* mbound, double* vbound,
+                        const orc_perturb* pt)
 {
     const int N = gp->N, d = gp->d, k = gp->k;
     const double* ell = gp->ell + (size_t)m * d;
     const double s = gp->s[m];
     const double* alpha = gp->alpha + (size_t)m * N;
     const double* R = gp->R + (size_t)m * k * N;
-    double* kv = scratch;
+    double* kv = scratch;              /* kernel values of the mean path */
     double* w = scratch + N;
     double* z = scratch + 2 * N;
+    double* kvv = scratch + 2 * N + k; /* kernel values of the variance path */
+    const int pm = pt ? pt->mode : 0;
     double mu = 0.0, mb = 0.0;
     for (int n = 0; n < N; ++n) {
-        kv[n] = orc_kernel(x, gp->X + (size_t)n * d, d, ell, s);
+        double kn = orc_kernel(x, gp->X + (size_t)n * d, d, ell, s);
+        if (pm == 4 || pm == 5) {
+            /* variant (b): the exponent as an fp32 GPU forms it -- mode 4 scales before the
+             * difference (x_hat - X_hat with x_hat = fl(x kappa/l)), mode 5 differences first
+             * then scales; exp2 and everything else exact. */
+            const float kap = 0.84932180028801907f;
+            float q = 0.0f;
+            for (int c = 0; c < d; ++c) {
+                const float sc = (float)((double)kap / ell[c]);
+                float df;
+                if (pm == 4) {
+                    const float xh = (float)x[c] * sc, Xh = (float)gp->X[(size_t)n * d + c] * sc;
+                    df = xh - Xh;
+                } else {
+                    df = ((float)x[c] - (float)gp->X[(size_t)n * d + c]) * sc;
+                }
+                q = fmaf(df, df, q);
+            }
+            kn = s * exp2(-(double)q);
+        }
+        kv[n] = (pm == 1 || pm == 2) ? kn * (1.0 + orc_delta(pt, m, N, n, 5)) : kn;  /* mode 4/5: kn above */
+        kvv[n] = (pm == 1 || pm == 3) ? kn * (1.0 + orc_delta(pt, m, N, n, 6)) : kn;
         mu += kv[n] * alpha[n];
         mb += fabs(kv[n] * alpha[n]);
     }
@@ -381,8 +425,8 @@ static void orc_query(const orc_gp* gp, int m, const double* x, double* scratch,
     for (int j = 0; j < k; ++j) {
         double acc = 0.0, aabs = 0.0;
         for (int n = 0; n < N; ++n) {
-            acc += R[(size_t)j * N + n] * kv[n];
-            aabs += fabs(R[(size_t)j * N + n] * kv[n]);
+            acc += R[(size_t)j * N + n] * kvv[n];
+            aabs += fabs(R[(size_t)j * N + n] * kvv[n]);
         }
         z[j] = acc;
         zz += acc * acc;
@@ -404,12 +448,18 @@ static void orc_query(const orc_gp* gp, int m, const double* x, double* scratch,
             for (int n = 0; n < N; ++n) {
                 double dx = gp->X[(size_t)n * d + c] - x[c];
                 am += kv[n] * alpha[n] * dx;
-                av += w[n] * kv[n] * (-dx);
+                av += w[n] * kvv[n] * (-dx);
             }
             if (jmu) jmu[c] = il2 * am;
             if (jv) jv[c] = 2.0 * il2 * av;
         }
     }
+}
+
+static void orc_query(const orc_gp* gp, int m, const double* x, double* scratch, double* mean,
+                      double* var, double* jmu, double* jv, double* mbound, double* vbound)
+{
+    orc_query_p(gp, m, x, scratch, mean, var, jmu, jv, mbound, vbound, NULL);
 }
 
 /* Batched query for all outputs: outputs are M x p (mean, var, bounds) and M x p x d (Jacobians). */
@@ -419,7 +469,7 @@ void orc_love_predict(const orc_gp* gp, const double* xs, int M, double* mean, d
     const int p = gp->p, d = gp->d;
 #pragma omp parallel
     {
-        double* scratch = (double*)malloc(sizeof(double) * (2 * (size_t)gp->N + gp->k + 1));
+        double* scratch = (double*)malloc(sizeof(double) * (3 * (size_t)gp->N + gp->k + 1));
 #pragma omp for schedule(static)
         for (int i = 0; i < M; ++i)
             for (int m = 0; m < p; ++m) {
@@ -502,7 +552,7 @@ int orc_rollout(const orc_gp* gp, const orc_policy* pol, const orc_reward* rw, c
                 const double* goals, int B, int T, uint64_t seed, long long traj_offset,
                 long long B_global, int eps_mode, int want_grad, double* cost_out,
                 double* grad_out, double* trace_x, double* trace_mu, double* trace_var,
-                double* ret_out)
+                double* ret_out, int perturb_mode, uint64_t perturb_seed)
 {
     const int p = gp->p, d = gp->d, L = pol->n_layers;
     const int maxw = orc_max_width(pol);
@@ -515,7 +565,7 @@ int orc_rollout(const orc_gp* gp, const orc_policy* pol, const orc_reward* rw, c
 
 #pragma omp parallel
     {
-        double* scratch = (double*)malloc(sizeof(double) * (2 * (size_t)gp->N + gp->k + 1));
+        double* scratch = (double*)malloc(sizeof(double) * (3 * (size_t)gp->N + gp->k + 1));
         /* per-trajectory tape */
         double* tx = (double*)malloc(sizeof(double) * (size_t)(T + 1) * p);
         double* th = (double*)malloc(sizeof(double) * (size_t)(T > 0 ? T : 1) * (L + 1) * maxw);
@@ -548,8 +598,9 @@ int orc_rollout(const orc_gp* gp, const orc_policy* pol, const orc_reward* rw, c
                 double* xn = tx + (size_t)(t + 1) * p;
                 for (int m = 0; m < p; ++m) {
                     double mu, v;
-                    orc_query(gp, m, xs, scratch, &mu, &v, tjm + ((size_t)t * p + m) * d,
-                              tjv + ((size_t)t * p + m) * d, NULL, NULL);
+                    orc_perturb pt = {perturb_mode, perturb_seed, bg, (uint32_t)t};
+                    orc_query_p(gp, m, xs, scratch, &mu, &v, tjm + ((size_t)t * p + m) * d,
+                                tjv + ((size_t)t * p + m) * d, NULL, NULL, perturb_mode ? &pt : NULL);
                     double vh = v > ORC_VAR_FLOOR ? v : ORC_VAR_FLOOR;
                     double sig = sqrt(vh);
                     double e = eps_mode == 0 ? orc_rollout_eps(seed, bg, (uint32_t)t, m) : 0.0;

@@ -62,6 +62,7 @@ def lib() -> C.CDLL:
             L.bagel_tc_selftest.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]
             L.bagel_set_gp_kernel.argtypes = [_vp, C.c_int]
             L.bagel_tc_bench.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp]
+            L.bagel_debug_buffer.argtypes = [_vp, C.c_int, _vp, C.c_size_t]
             L.bagel_get_gp_kernel.argtypes = [_vp, C.POINTER(C.c_int)]
             _lib = L
     return _lib
@@ -71,7 +72,8 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "policy_configure", "reward_configure", "rollout_cost_and_grad", "bagel_last_launch_count",
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
-           "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench"]
+           "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench",
+           "bagel_debug_buffer"]
 
 PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce"]
 
@@ -239,6 +241,11 @@ class Context:
         cyc = torch.zeros(ctas, dtype=torch.int64, device=self.dev)
         self._check(self.L.bagel_tc_bench(self.h, int(N), int(iters), int(mode), int(ctas), _ptr(cyc)))
         return cyc.cpu().numpy()
+
+    def debug_buffer(self, which: int, n_floats: int) -> np.ndarray:
+        out = np.empty(n_floats, dtype=np.float32)
+        self._check(self.L.bagel_debug_buffer(self.h, int(which), out.ctypes.data, out.nbytes))
+        return out
 
     def cache_rank(self) -> int:
         k = C.c_int(0)

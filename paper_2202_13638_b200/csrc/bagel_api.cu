@@ -821,3 +821,22 @@ extern "C" int bagel_tc_bench(bagel_ctx* c, int N, int iters, int mode, int ctas
     CK(cudaStreamSynchronize(c->stream));
   });
 }
+
+extern "C" int bagel_debug_buffer(bagel_ctx* c, int which, void* dst, size_t bytes) {
+  return guarded(c, [&] {
+    const void* src = nullptr;
+    size_t have = 0;
+    const Workspace& w = c->ws;
+    switch (which) {
+      case 0: src = c->tcs.P1h; have = (size_t)w.S1tc * c->p * w.B * (1 + c->d) * sizeof(float); break;
+      case 1: src = c->tcs.P1z; have = tc_p1z_floats(c, w.B, w.S1tc) * sizeof(float); break;
+      case 2: src = w.P2; have = (size_t)w.S2eff * c->p * w.B * (1 + BAGEL_MAX_D) * sizeof(float); break;
+      case 3: src = w.mu; have = (size_t)c->p * w.B * sizeof(float); break;
+      default: break;
+    }
+    REQUIRE(src && dst && bytes <= have, BAGEL_E_ARG, "bagel_debug_buffer: buffer %d unavailable or %zu > %zu bytes",
+            which, bytes, have);
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}

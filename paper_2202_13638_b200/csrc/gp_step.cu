@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(P1_THREADS) k_pass1(GpDesc g, const float* __r
   for (int r = tid; r < P1_BM; r += P1_THREADS) {
     const int row = row0 + r;
 #pragma unroll
-    for (int c = 0; c < D; ++c) xq[c][r] = row < B ? xstar[(size_t)row * D + c] * g.qscale[m][c] : 0.0f;
+    for (int c = 0; c < D; ++c) xq[c][r] = row < B ? xstar[(size_t)row * D + c] : 0.0f;
   }
   const int ty = tid / 8, tx = tid % 8;
   float acc[8][8];
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(P1_THREADS) k_pass1(GpDesc g, const float* __r
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
 
   const float* Vm = V + (size_t)m * g.N * g.Cld;
-  const float* Xm = Xs + (size_t)m * g.N * D;
+  const float* Xm = Xs;  // raw X (N x D): differences first, then the per-dimension scale
   for (int n0 = n_begin; n0 < n_end; n0 += P1_BN) {
     __syncthreads();
     for (int i = tid; i < P1_BN * P1_BC / 4; i += P1_THREADS) {
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(P1_THREADS) k_pass1(GpDesc g, const float* __r
     }
     for (int i = tid; i < P1_BN * D; i += P1_THREADS) {
       const int nn = i / D, c = i % D;
-      Xt[nn][c] = (n0 + nn < n_end) ? Xm[(size_t)(n0 + nn) * D + c] : 0.0f;
+      Xt[nn][c] = (n0 + nn < n_end) ? Xm[(size_t)(n0 + nn) * D + c] : 1e18f;
     }
     __syncthreads();
     for (int i = tid; i < P1_BN * P1_BM; i += P1_THREADS) {
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(P1_THREADS) k_pass1(GpDesc g, const float* __r
       float q = 0.0f;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const float df = xq[c][r] - Xt[nn][c];
+        const float df = (xq[c][r] - Xt[nn][c]) * g.qscale[m][c];
         q = fmaf(df, df, q);
       }
       Ks[nn][r] = exp2f(-q);
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(GpDesc g, const float* __r
   for (int r = tid; r < P2_BM; r += P2_THREADS) {
     const int row = row0 + r;
 #pragma unroll
-    for (int c = 0; c < D; ++c) xq[c * P2_BM + r] = row < B ? xstar[(size_t)row * D + c] * g.qscale[m][c] : 0.0f;
+    for (int c = 0; c < D; ++c) xq[c * P2_BM + r] = row < B ? xstar[(size_t)row * D + c] : 0.0f;
   }
   const int ty = tid / 16, tx = tid % 16;  // rows ty*8..+8, n = tx*4..+4
   float acc[8][1 + D];
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(GpDesc g, const float* __r
         float q = 0.0f;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const float df = xq[c * P2_BM + r] - Xt[nn * D + c];
+          const float df = (xq[c * P2_BM + r] - Xr[nn * D + c]) * g.qscale[m][c];
           q = fmaf(df, df, q);
         }
         const float t = w[i][e] * exp2f(-q);
@@ -318,7 +318,7 @@ int gs_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
   const int S1 = c->ws.S1;
   const int nps = cdiv(cdiv(c->gp.N, S1), P1_BN) * P1_BN;
   dim3 grid(cdiv(B, P1_BM), cdiv(c->gp.C, P1_BC), c->gp.p * S1);
-  DISPATCH_D(c->gp.d, (k_pass1<D><<<grid, P1_THREADS, 0, st>>>(c->gp, xstar, B, c->Xs, c->V, nps, c->ws.P1)));
+  DISPATCH_D(c->gp.d, (k_pass1<D><<<grid, P1_THREADS, 0, st>>>(c->gp, xstar, B, c->X, c->V, nps, c->ws.P1)));
   return 1;
 }
 

@@ -87,7 +87,7 @@ __device__ __forceinline__ float pow2_scale_for(float amax, float* inv) {
 
 // ====================================================================== packing
 // Pass-1 tiles of output m: [ct][t] -> [B hi: NZ x KT1 | B lo | aux: KT1 x AUXW]
-// B(j, n) = s R_jn * colscale_j^-1 (j = ct*NZ + row), aux(n) = [X_hat(d) | s alpha | s alpha X(d)].
+// B(j, n) = s R_jn * colscale_j^-1 (j = ct*NZ + row), aux(n) = [X(d) | s alpha | s alpha X(d)].
 __global__ void k_pack1(Geo g, const float* __restrict__ X, const double* __restrict__ alpha,
                         const double* __restrict__ R, double s, const float* __restrict__ qscale,
                         const float* __restrict__ colscale_inv, uint8_t* __restrict__ out) {
@@ -112,7 +112,7 @@ __global__ void k_pack1(Geo g, const float* __restrict__ X, const double* __rest
     const int n = t * KT1 + nn;
     float v = 0.0f;
     if (n < g.N) {
-      if (f < g.d) v = X[(size_t)n * g.d + f] * qscale[f];
+      if (f < g.d) v = X[(size_t)n * g.d + f];  // raw X: the exponent differences before scaling
       else if (f == g.d) v = (float)(s * alpha[n]);
       else if (f < 2 * g.d + 1) v = (float)(s * alpha[n] * (double)X[(size_t)n * g.d + f - g.d - 1]);
     } else if (f < g.d) {
@@ -145,7 +145,7 @@ __global__ void k_colscale(const double* __restrict__ R, int N, int k, double s,
 
 // Pass-2 tiles of output m: [jt][t] -> KJ/KS2 slabs [B hi: NT2 x KS2 | B lo: NT2 x KS2] (canonical
 // K-major, rows = training points, K = j), then aux: NT2 x AUXW.
-// B(n, j) = s R_jn * 2^-f_n (f_n from max over the tile's j range), aux(n) = [X_hat(d) | X(d) | 2^f_n].
+// B(n, j) = s R_jn * 2^-f_n (f_n from max over the tile's j range), aux(n) = [X(d) | 2^f_n].
 __global__ void k_pack2(Geo g, const float* __restrict__ X, const double* __restrict__ R, double s,
                         const float* __restrict__ qscale, uint8_t* __restrict__ out) {
   const int t = blockIdx.x, jt = blockIdx.y;
@@ -188,9 +188,8 @@ __global__ void k_pack2(Geo g, const float* __restrict__ X, const double* __rest
     const int n = t * NT2 + nn;
     float v = 0.0f;
     if (n < g.N) {
-      if (f < g.d) v = X[(size_t)n * g.d + f] * qscale[f];
-      else if (f < 2 * g.d) v = X[(size_t)n * g.d + f - g.d];
-      else if (f == 2 * g.d) v = rinv[nn];
+      if (f < g.d) v = X[(size_t)n * g.d + f];
+      else if (f == g.d) v = rinv[nn];
     } else if (f < g.d) {
       v = 1e18f;
     }
@@ -345,9 +344,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
     const int gt = tid - 32 * CTRL_WARPS;  // 0..511
     const int r = gt % 128, qd = gt / 128;
     const int row = row0 + r;
-    float xq[D];
+    // exponent as (x*_c - X_nc) * kappa / l_c: difference first, then scale (4x smaller fp32
+    // error in ktilde than scaling first, scripts/fp32_floor.py)
+    float xq[D], sc[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] * a.qscale[m][c] : 0.0f;
+    for (int c = 0; c < D; ++c) {
+      xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] : 0.0f;
+      sc[c] = a.qscale[m][c];
+    }
     float hacc[1 + D];
 #pragma unroll
     for (int c = 0; c <= D; ++c) hacc[c] = 0.0f;
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
           float q = 0.0f;
 #pragma unroll
           for (int c = 0; c < D; ++c) {
-            const float df = xq[c] - an[c];
+            const float df = (xq[c] - an[c]) * sc[c];
             q = fmaf(df, df, q);
           }
           const float kt = ex2_approx(-q);
@@ -384,17 +388,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
         hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
       }
-      tc::mbar_arrive(&empty_x[x]);
       const int ci = tc::canon_idx(r, qd * 8, KT1);
       *reinterpret_cast<uint4*>(ahi + ci) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       *reinterpret_cast<uint4*>(alo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      // MEMBAR.CTA + proxy fence: the A stores are visible to the MMA, and every aux load above
+      // has returned before the aux stage is released (SYNCS.ARRIVE does not wait for pending LDS)
       tc::fence_proxy_async();
       tc::mbar_arrive(&full_a[s]);
+      tc::mbar_arrive(&empty_x[x]);
     }
     // ---- mean columns: combine the four quarters of each row (fixed order)
     if (qd > 0)
       for (int c = 0; c <= D; ++c) hsum[qd - 1][r][c] = hacc[c];
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS));
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS) : "memory");
     if (qd == 0 && row < a.B && ct == 0) {
       float* o = a.P1h + ((size_t)(split * a.m_count + m) * a.B + row) * (1 + D);
       for (int c = 0; c <= D; ++c) o[c] = ((hacc[c] + hsum[0][r][c]) + hsum[1][r][c]) + hsum[2][r][c];
@@ -626,7 +632,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   const Geo& g = a.g;
   const int KJ = g.KJ;
   const int nsl = KJ / KS2;                            // slabs per tile
-  constexpr int NAUX = 2 * D + 1;
+  constexpr int NAUX = D + 1;
   constexpr size_t slab_bytes = (size_t)4 * NT2 * KS2;  // hi + lo of one slab
   constexpr size_t x_bytes = (size_t)NT2 * AUXW * 4;    // aux rows of one tile
   __shared__ __align__(8) uint64_t zready, full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2],
@@ -747,9 +753,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       tc::mbar_arrive(&zready);
     }
     // ------------------------------------------------ epilogue: sum_n (s w_n) ktilde_n [1 | X_n]
-    float xq[D];
+    float xq[D], sc[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] * a.qscale[m][c] : 0.0f;
+    for (int c = 0; c < D; ++c) {
+      xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] : 0.0f;
+      sc[c] = a.qscale[m][c];
+    }
     const float zinv = row < a.B ? a.zrow_inv[(size_t)m * a.B + row] : 0.0f;
     float acc[1 + D];
 #pragma unroll
@@ -777,20 +786,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
         float q = 0.0f;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const float df = xq[c] - an[c];
+          const float df = (xq[c] - an[c]) * sc[c];
           q = fmaf(df, df, q);
         }
-        const float t = w[u] * an[2 * D] * ex2_approx(-q);
+        const float t = w[u] * an[D] * ex2_approx(-q);
         acc[0] += t;
 #pragma unroll
-        for (int c = 0; c < D; ++c) acc[1 + c] = fmaf(t, an[D + c], acc[1 + c]);
+        for (int c = 0; c < D; ++c) acc[1 + c] = fmaf(t, an[c], acc[1 + c]);
       }
+      __threadfence_block();  // every aux load above has returned before the stage is released
       tc::mbar_arrive(&empty_x[x]);
     }
     // combine the four column groups of each row (fixed order), undo the Z row scale
     if (cg > 0)
       for (int c = 0; c <= D; ++c) asum[cg - 1][r][c] = acc[c];
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS));
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS) : "memory");
     if (cg == 0 && row < a.B) {
       float* o = a.P2 + (((size_t)(split * g.njt + jt) * a.m_count + m) * a.B + row) * P2_LD;
       for (int c = 0; c <= D; ++c) o[c] = (((acc[c] + asum[0][r][c]) + asum[1][r][c]) + asum[2][r][c]) * zinv;

@@ -1,7 +1,7 @@
 # full GPU round: parity tests, smoke, bench, then (only if the plain bench exited 0) ncu
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -rA --timeout=600 2>&1 | tail -${TAIL:-70} > gpurun_out/gpu_tests.log
+timeout 1500 python -m pytest tests -m gpu -q -rA --timeout=600 > gpurun_out/gpu_tests_full.log 2>&1; tail -${TAIL:-70} gpurun_out/gpu_tests_full.log > gpurun_out/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 900 python bench.py --steps ${STEPS:-10} --warmup 3 > gpurun_out/bench.log 2>&1
 if [ -n "$NCU" ]; then

@@ -348,7 +348,32 @@ def test_c2_full_batch_sampled_rows(c2):
     print("shard-sum vs full batch: cost rel", abs(cs - c) / abs(c), "grad rel",
           np.linalg.norm(gs - g) / np.linalg.norm(g))
     assert cs == pytest.approx(c, rel=1e-4)
-    assert np.linalg.norm(gs - g) <= 1e-3 * np.linalg.norm(g)
+    # two fp32 roundings of the same batch differ by about the fp32 floor of C2 (~1e-3, see
+    # test_c2_full_batch_vs_oracle / DESIGN.md R30), so the consistency bound is 3x that
+    assert np.linalg.norm(gs - g) <= 3e-3 * np.linalg.norm(g)
+    # bitwise determinism at the bench launch shape
+    c2, g2 = _rollout_gpu(ctx, wl, wl.goals, seed)
+    assert c2 == c and np.array_equal(g2, g)
+
+
+def test_c2_full_batch_vs_oracle(c2):
+    """Bench workload end to end (B = 1024, T = 100, launch shape of bench.py) against the oracle.
+    The gradient bound is max(1e-3, 3 x floor), floor = the oracle's own change under a 2^-22
+    relative perturbation of every kernel value (fp32-sensitivity mode):
+    a few trajectories of this batch are ill-conditioned (their gradient moves by ~0.4% under
+    2^-22 perturbations), which puts the fp32 floor of the full-batch gradient near 1e-3."""
+    wl, mdl, ctx = c2
+    seed = W.rollout_seed(1)
+    c, g = _rollout_gpu(ctx, wl, wl.goals, seed)
+    ref = _rollout_oracle(mdl, wl, wl.goals, seed)
+    pert = O.rollout(mdl, wl.sizes, "xg", wl.theta, wl.Q, wl.sigma_r, wl.x0, wl.goals, wl.T, seed,
+                     perturb_mode=1, perturb_seed=1)
+    floor = np.linalg.norm(pert["grad"] - ref["grad"]) / np.linalg.norm(ref["grad"])
+    rel_c = abs(c - ref["cost"]) / abs(ref["cost"])
+    rel_g = np.linalg.norm(g - ref["grad"]) / np.linalg.norm(ref["grad"])
+    print(f"C2 full batch: cost rel {rel_c:.2e}, grad rel L2 {rel_g:.2e}, fp32 floor {floor:.2e}")
+    assert rel_c <= 1e-3
+    assert rel_g <= max(1e-3, 3.0 * floor)
 
 
 # ------------------------------------------------------------------ both GP-step implementations
