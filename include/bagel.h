@@ -143,11 +143,12 @@ int bagel_last_launch_count(const bagel_ctx* ctx, int* launches);
  * its duration is accumulated per kernel class:
  *   0 gp_pass1 (a2+a3 contraction), 1 gp_reduce1 (a4), 2 gp_pass2 (a5),
  *   3 step_epilogue (a6-a8 + next a1), 4 init (a1 + a7 at t = 0),
- *   5 reverse (a9), 6 reduce (a10).
+ *   5 reverse (a9: the adjoint recursion), 6 reduce (a10), 7 theta_grad (a9: the
+ *   parameter-gradient contraction over the adjoint tape).
  * bagel_profile(ctx, 1) enables and clears, bagel_profile(ctx, 0) disables.
  * bagel_profile_get: total_ms [host] and launches [host] of class `kernel`
  * since the last enable (synchronises the stream).  Errors: E_ARG. */
-#define BAGEL_PROFILE_CLASSES 7
+#define BAGEL_PROFILE_CLASSES 8
 int bagel_profile(bagel_ctx* ctx, int enable);
 int bagel_profile_get(bagel_ctx* ctx, int kernel, double* total_ms, long long* launches);
 
@@ -210,6 +211,10 @@ int bagel_tc_selftest(bagel_ctx* ctx, const void* A, const void* B, int N, int K
  * 0 pass-1 mean-column partials, 1 pass-1 z partials, 2 pass-2 partials, 3 step means.
  * Layouts are internal (csrc/gp_step_tc.cu).  Errors: E_ARG. */
 int bagel_debug_buffer(bagel_ctx* ctx, int which, void* dst, size_t bytes);
+
+/* Enable (1) / disable (0) per-CTA %globaltimer event stamps of the tensor-core GP kernels
+ * (16 per CTA, up to 4096 CTAs; read with bagel_debug_buffer 4 = pass 1, 5 = pass 2). */
+int bagel_debug_trace(bagel_ctx* ctx, int enable);
 
 /* Tensor-core issue-rate microbenchmark: `ctas` CTAs (one per SM) each issue `iters`
  * back-to-back tcgen05.mma (M = 128, N, K = 16; mode 0: A from shared memory, 1: A from

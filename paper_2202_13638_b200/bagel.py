@@ -63,6 +63,7 @@ def lib() -> C.CDLL:
             L.bagel_set_gp_kernel.argtypes = [_vp, C.c_int]
             L.bagel_tc_bench.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp]
             L.bagel_debug_buffer.argtypes = [_vp, C.c_int, _vp, C.c_size_t]
+            L.bagel_debug_trace.argtypes = [_vp, C.c_int]
             L.bagel_get_gp_kernel.argtypes = [_vp, C.POINTER(C.c_int)]
             _lib = L
     return _lib
@@ -73,9 +74,9 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
            "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench",
-           "bagel_debug_buffer"]
+           "bagel_debug_buffer", "bagel_debug_trace"]
 
-PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce"]
+PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce", "theta_grad"]
 
 
 def _ptr(t):
@@ -246,6 +247,14 @@ class Context:
         out = np.empty(n_floats, dtype=np.float32)
         self._check(self.L.bagel_debug_buffer(self.h, int(which), out.ctypes.data, out.nbytes))
         return out
+
+    def debug_trace(self, enable: bool):
+        self._check(self.L.bagel_debug_trace(self.h, int(bool(enable))))
+
+    def debug_stamps(self, which: int) -> np.ndarray:
+        out = np.empty(16 * 4096, dtype=np.uint64)
+        self._check(self.L.bagel_debug_buffer(self.h, int(which), out.ctypes.data, out.nbytes))
+        return out.reshape(4096, 16)
 
     def cache_rank(self) -> int:
         k = C.c_int(0)

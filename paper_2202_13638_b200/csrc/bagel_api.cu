@@ -17,7 +17,7 @@
 #include "bagel_internal.h"
 
 size_t gs_pass2_smem(int k, int d);
-size_t ro_reverse_smem(const PolicyDesc& P);
+size_t ro_reverse_smem(const PolicyDesc& P, int p, int d);
 size_t ro_epilogue_smem(const PolicyDesc& P);
 size_t ro_policy_smem(const PolicyDesc& P);
 int tc_selftest_launch(const void* A, const void* B, int N, int K, float* D, int mode, cudaStream_t st);
@@ -147,6 +147,8 @@ void free_workspace(bagel_ctx* c) {
   Workspace& w = c->ws;
   dev_free(w.xstar); dev_free(w.P1); dev_free(w.Z); dev_free(w.P2); dev_free(w.mu); dev_free(w.var);
   dev_free(w.tape_x); dev_free(w.tape_sig); dev_free(w.tape_jmu); dev_free(w.tape_jv); dev_free(w.G);
+  dev_free(w.tape_A); dev_free(w.tape_act); dev_free(w.tape_delta);
+  w.tape_pol_cap = 0;
   dev_free(w.theta_part); dev_free(w.grad_tmp); dev_free(w.thetaT); dev_free(w.cost_dev); dev_free(w.err_flag);
   dev_free(c->tcs.P1z); dev_free(c->tcs.P1h); dev_free(c->tcs.Zp); dev_free(c->tcs.zrow_inv);
   dev_free(c->tcs.zz_part); dev_free(c->tcs.zmax_part);
@@ -181,12 +183,12 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
   Workspace& w = c->ws;
   int S1, S2;
   gs_choose_splits(c, B, &S1, &S2);
-  int S1t = 0, S2t = 0, tps1 = 0, tps2 = 0;
+  int S1t = 0, S2t = 0, tps1 = 0, tps2 = 0, fused = 0;
   const bool tc = tc_supported(c);
-  if (tc) tc_choose_splits(c, B, &S1t, &S2t, &tps1, &tps2);
+  if (tc) tc_choose_splits(c, B, &S1t, &S2t, &tps1, &tps2, &fused);
   const bool same = w.B >= B && w.T >= T && w.B > 0 && w.S1 == S1 && w.S2 == S2 && w.B == B && w.S1tc == S1t &&
-                    w.S2tc == S2t;
-  const int nblk = (B + ro_reverse_block_rows() - 1) / ro_reverse_block_rows();
+                    w.S2tc == S2t && w.p1_fused == fused && w.tps1 == tps1;
+  const int nblk = ro_theta_blocks(c, B, T);
   if (!same) {
     free_workspace(c);
     const int p = c->p, d = c->d;
@@ -197,11 +199,14 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
     const size_t s2max = std::max((size_t)S2, (size_t)S2t * (tc ? tc_njt(c) : 1));
     dev_alloc(c, w.P2, s2max * p * Bs * (1 + BAGEL_MAX_D));
     if (tc) {
-      dev_alloc(c, c->tcs.P1z, tc_p1z_floats(c, B, S1t));
+      dev_alloc(c, c->tcs.P1z, tc_p1z_floats(c, (B + 127) / 128 * 128, S1t));  // fused layout pads row tiles
       dev_alloc(c, c->tcs.P1h, (size_t)S1t * p * Bs * (1 + d));
       dev_alloc(c, c->tcs.Zp, tc_zp_bytes(c, B));
       CK(cudaMemsetAsync(c->tcs.Zp, 0, tc_zp_bytes(c, B), c->stream));  // padding rows / j stay zero
       dev_alloc(c, c->tcs.zrow_inv, (size_t)p * Bs);
+      if (!c->tcs.gbar) dev_alloc(c, c->tcs.gbar, tc_gbar_count());
+      // the barrier's counters assume a fixed grid: restart them with every new split layout
+      CK(cudaMemsetAsync(c->tcs.gbar, 0, tc_gbar_count() * sizeof(unsigned long long), c->stream));
       dev_alloc(c, c->tcs.zz_part, tc_zpart_count(c, B));
       dev_alloc(c, c->tcs.zmax_part, tc_zpart_count(c, B));
     }
@@ -211,6 +216,7 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
     dev_alloc(c, w.tape_sig, Ts * Bs * p);
     dev_alloc(c, w.tape_jmu, Ts * Bs * p * d);
     dev_alloc(c, w.tape_jv, Ts * Bs * p * d);
+    dev_alloc(c, w.tape_A, Ts * Bs * p * d);
     dev_alloc(c, w.G, Bs);
     dev_alloc(c, w.cost_dev, 1);
     dev_alloc(c, w.err_flag, 1);
@@ -222,12 +228,19 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
     w.S2tc = S2t;
     w.tps1 = tps1;
     w.tps2 = tps2;
+    w.p1_fused = fused;
   }
   if (c->policy_ok) {
     const int need = nblk * c->pol.n_params;
     if (w.theta_part_cap < need) {
       dev_alloc(c, w.theta_part, (size_t)need);
       w.theta_part_cap = need;
+    }
+    const size_t rows = (size_t)std::max(w.T, 1) * w.B;
+    if (w.tape_pol_cap < rows) {
+      dev_alloc(c, w.tape_act, rows * c->pol.act_ld);
+      dev_alloc(c, w.tape_delta, rows * c->pol.d_ld);
+      w.tape_pol_cap = rows;
     }
     if (!w.grad_tmp) dev_alloc(c, w.grad_tmp, (size_t)c->pol.n_params + 64);
     if (!w.thetaT) dev_alloc(c, w.thetaT, (size_t)c->pol.n_params + 64);
@@ -255,7 +268,7 @@ void check_numeric(bagel_ctx* c, int B) {
   }
 }
 
-enum { PC_PASS1 = 0, PC_REDUCE1, PC_PASS2, PC_EPI, PC_INIT, PC_REVERSE, PC_REDUCE };
+enum { PC_PASS1 = 0, PC_REDUCE1, PC_PASS2, PC_EPI, PC_INIT, PC_REVERSE, PC_REDUCE, PC_THETA };
 
 cudaEvent_t prof_event(bagel_ctx* c) {
   if (!c->prof_pool.empty()) {
@@ -308,12 +321,13 @@ int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goal
   const bool tc = use_tc(c);
   w.S2eff = tc ? w.S2tc * tc_njt(c) : w.S2;
   for (int t = 0; t < T; ++t) {
-    launches += timed(c, PC_PASS1, [&] { return tc ? tc_pass1(c, w.xstar, B, st) : gs_pass1(c, w.xstar, B, st); });
-    launches += timed(c, PC_REDUCE1, [&] {
-      float* jm = w.tape_jmu + (size_t)t * B * p * d;
-      float* sg = w.tape_sig + (size_t)t * B * p;
-      return tc ? tc_reduce1(c, w.xstar, B, jm, sg, st) : gs_reduce1(c, w.xstar, B, jm, sg, st);
-    });
+    float* jm = w.tape_jmu + (size_t)t * B * p * d;
+    float* sg = w.tape_sig + (size_t)t * B * p;
+    launches += timed(c, PC_PASS1, [&] { return tc ? tc_pass1(c, w.xstar, B, jm, sg, st) : gs_pass1(c, w.xstar, B, st); });
+    if (!(tc && w.p1_fused))
+      launches += timed(c, PC_REDUCE1, [&] {
+        return tc ? tc_reduce1(c, w.xstar, B, jm, sg, st) : gs_reduce1(c, w.xstar, B, jm, sg, st);
+      });
     launches += timed(c, PC_PASS2, [&] { return tc ? tc_pass2(c, w.xstar, B, st) : gs_pass2(c, w.xstar, B, st); });
     launches += timed(c, PC_EPI, [&] {
       return ro_step_epilogue(c, theta, goals, B, t, T, seed, traj_offset, t + 1 < T,
@@ -374,6 +388,10 @@ extern "C" int bagel_destroy(bagel_ctx* c) {
     cudaEventDestroy(e.b);
   }
   for (auto e : c->prof_pool) cudaEventDestroy(e);
+  dev_free(c->tcs.dbg1);
+  dev_free(c->tcs.dbg2);
+  dev_free(c->tcs.dbg3);
+  dev_free(c->tcs.gbar);
   dev_free(c->X);
   dev_free(c->Y);
   dev_free(c->ws.stage);
@@ -604,14 +622,30 @@ extern "C" int policy_configure(bagel_ctx* c, const int* sizes, int n_sizes) {
     P.n_params = off;
     P.max_width = mw;
     P.act_total = at;
+    {
+      int ao = 0, dof = 0;
+      for (int l = 0; l <= P.n_layers; ++l) {
+        P.aoff[l] = ao;
+        ao += (P.sizes[l] + 3) & ~3;
+        if (l < P.n_layers) {
+          P.doff[l] = dof;
+          dof += (P.sizes[l + 1] + 3) & ~3;
+        }
+      }
+      P.act_ld = ao;
+      P.d_ld = dof;
+    }
     P.phi_mode = sizes[0] == 3 * c->p ? 1 : 0;
-    REQUIRE(ro_reverse_smem(P) <= 200 * 1024 && ro_policy_smem(P) <= 200 * 1024, BAGEL_E_ARG,
-            "policy_configure: policy with %d parameters exceeds the v0 reverse kernel's shared-memory budget",
-            P.n_params);
+    REQUIRE(ro_reverse_smem(P, c->p, c->d) <= 200 * 1024 && ro_policy_smem(P) <= 200 * 1024 &&
+                ro_theta_grad_smem(P) <= 200 * 1024, BAGEL_E_ARG,
+            "policy_configure: policy with %d parameters exceeds the kernels' shared-memory budget", P.n_params);
     c->pol = P;
     c->policy_ok = true;
     c->ws.theta_part_cap = 0;
     dev_free(c->ws.theta_part);
+    c->ws.tape_pol_cap = 0;
+    dev_free(c->ws.tape_act);
+    dev_free(c->ws.tape_delta);
     dev_free(c->ws.grad_tmp);
     dev_free(c->ws.thetaT);
   });
@@ -651,6 +685,7 @@ extern "C" int rollout_cost_and_grad(bagel_ctx* c, const float* policy_params, c
     float* gout = dev_grad ? grad : c->ws.grad_tmp;
     int nblk = 0;
     launches += timed(c, PC_REVERSE, [&] { return ro_reverse(c, th, gd, B, T, seed, traj_offset, B_global, &nblk, st); });
+    launches += timed(c, PC_THETA, [&] { return ro_theta_grad(c, B, T, nblk, st); });
     launches += timed(c, PC_REDUCE, [&] { return ro_reduce(c, nblk, B, B_global, gout, st); });
     CK(cudaGetLastError());
     double cost = 0.0;
@@ -681,8 +716,9 @@ extern "C" int bagel_gp_predict(bagel_ctx* c, const float* xstar, int M, float* 
     const bool tc = use_tc(c);
     c->ws.S2eff = tc ? c->ws.S2tc * tc_njt(c) : c->ws.S2;
     int n = 0;
-    n += tc ? tc_pass1(c, xstar, M, st) : gs_pass1(c, xstar, M, st);
-    n += tc ? tc_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st) : gs_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st);
+    n += tc ? tc_pass1(c, xstar, M, jmu, c->ws.tape_sig, st) : gs_pass1(c, xstar, M, st);
+    if (!(tc && c->ws.p1_fused))
+      n += tc ? tc_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st) : gs_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st);
     n += tc ? tc_pass2(c, xstar, M, st) : gs_pass2(c, xstar, M, st);
     n += gs_finish_predict(c, xstar, M, mean, var, dmean, dvar, st);
     CK(cudaGetLastError());
@@ -829,14 +865,33 @@ extern "C" int bagel_debug_buffer(bagel_ctx* c, int which, void* dst, size_t byt
     const Workspace& w = c->ws;
     switch (which) {
       case 0: src = c->tcs.P1h; have = (size_t)w.S1tc * c->p * w.B * (1 + c->d) * sizeof(float); break;
-      case 1: src = c->tcs.P1z; have = tc_p1z_floats(c, w.B, w.S1tc) * sizeof(float); break;
+      case 1: src = c->tcs.P1z; have = c->tcs.P1z ? tc_p1z_floats(c, w.B, w.S1tc) * sizeof(float) : 0; break;
       case 2: src = w.P2; have = (size_t)w.S2eff * c->p * w.B * (1 + BAGEL_MAX_D) * sizeof(float); break;
       case 3: src = w.mu; have = (size_t)c->p * w.B * sizeof(float); break;
+      case 4: src = c->tcs.dbg1; have = c->tcs.dbg1 ? 16 * 4096 * sizeof(unsigned long long) : 0; break;
+      case 6: src = c->tcs.dbg3; have = c->tcs.dbg3 ? 16 * 4096 * sizeof(unsigned long long) : 0; break;
+      case 5: src = c->tcs.dbg2; have = c->tcs.dbg2 ? 16 * 4096 * sizeof(unsigned long long) : 0; break;
       default: break;
     }
     REQUIRE(src && dst && bytes <= have, BAGEL_E_ARG, "bagel_debug_buffer: buffer %d unavailable or %zu > %zu bytes",
             which, bytes, have);
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+extern "C" int bagel_debug_trace(bagel_ctx* c, int enable) {
+  return guarded(c, [&] {
+    dev_free(c->tcs.dbg1);
+    dev_free(c->tcs.dbg2);
+    dev_free(c->tcs.dbg3);
+    if (enable) {
+      dev_alloc(c, c->tcs.dbg3, (size_t)16 * 4096);
+      CK(cudaMemsetAsync(c->tcs.dbg3, 0, 16 * 4096 * sizeof(unsigned long long), c->stream));
+      dev_alloc(c, c->tcs.dbg1, (size_t)16 * 4096);
+      dev_alloc(c, c->tcs.dbg2, (size_t)16 * 4096);
+      CK(cudaMemsetAsync(c->tcs.dbg1, 0, 16 * 4096 * sizeof(unsigned long long), c->stream));
+      CK(cudaMemsetAsync(c->tcs.dbg2, 0, 16 * 4096 * sizeof(unsigned long long), c->stream));
+    }
   });
 }

@@ -27,6 +27,11 @@ struct PolicyDesc {
   int n_params;
   int max_width;
   int act_total;                // sum of all layer widths (activations per row)
+  // reverse-pass tapes: every segment padded to a multiple of 4 floats (16-byte aligned rows)
+  int aoff[BAGEL_MAX_LAYERS + 1];  // activation tape: offset of layer l's activations (l = 0: phi)
+  int act_ld;                      // activation tape row length
+  int doff[BAGEL_MAX_LAYERS];      // adjoint tape: offset of delta_l (layer l's outputs)
+  int d_ld;                        // adjoint tape row length
 };
 
 struct RewardDesc {
@@ -57,6 +62,10 @@ struct TcState {
   float* P1h = nullptr;           // S1 x p x B x (1 + d)
   uint8_t* Zp = nullptr;          // packed pass-2 A operand
   float* zrow_inv = nullptr;      // p x B
+  unsigned long long* gbar = nullptr;  // grid-barrier counter of the fused pass 1 (monotonic)
+  unsigned long long* dbg1 = nullptr;  // optional per-CTA event stamps (bagel_debug_trace)
+  unsigned long long* dbg2 = nullptr;
+  unsigned long long* dbg3 = nullptr;  // step epilogue (t = 50 of a rollout)
   double* zz_part = nullptr;      // p x (k/32) x B partial ||z||^2
   float* zmax_part = nullptr;     // p x (k/32) x B partial max|z|
 };
@@ -65,6 +74,7 @@ struct Workspace {
   int B = 0, T = 0;         // capacity
   int S1 = 0, S2 = 0;       // N-splits of pass 1 / pass 2 (v0 FFMA path)
   int S1tc = 0, S2tc = 0, tps1 = 0, tps2 = 0;  // tcgen05 path splits / tiles per split
+  int p1_fused = 0;  // pass 1 launched cooperatively with reduce 1 fused in (k_p1_tc<D, true>)
   int S2eff = 0;            // number of pass-2 partial slices the epilogue sums
   float* xstar = nullptr;   // B x d
   float* P1 = nullptr;      // S1 x p x B x Cld partial [mu | k a X | z]
@@ -77,6 +87,12 @@ struct Workspace {
   float* tape_sig = nullptr;
   float* tape_jmu = nullptr;
   float* tape_jv = nullptr;
+  // reverse-pass tape: A = J^mu + (eps / 2 sigma) J^v  T x B x p x d; every policy activation
+  // T x B x act_total; the adjoints delta_l T x B x (act_total - sizes[0])
+  float* tape_A = nullptr;
+  float* tape_act = nullptr;
+  float* tape_delta = nullptr;
+  size_t tape_pol_cap = 0;      // rows (T x B) the activation / delta tapes hold
   double* G = nullptr;      // B returns
   float* theta_part = nullptr;  // nblk x n_params reverse partials
   int theta_part_cap = 0;
@@ -194,18 +210,21 @@ int ro_philox_raw(const uint32_t* ctr, uint32_t k0, uint32_t k1, int n, uint32_t
                   cudaStream_t st);
 int ro_philox_normals(uint64_t seed, long long traj_offset, int B, int T, int p, float* out,
                       cudaStream_t st);
-int ro_reverse_block_rows();
+int ro_theta_blocks(const bagel_ctx* c, int B, int T);
+int ro_theta_grad(const bagel_ctx* c, int B, int T, int nblk, cudaStream_t st);
+size_t ro_theta_grad_smem(const PolicyDesc& P);
 
 // gp_step_tc.cu
 bool tc_supported(const bagel_ctx* c);
 size_t tc_tiles1_bytes(const bagel_ctx* c);
 size_t tc_tiles2_bytes(const bagel_ctx* c);
 int tc_pack(bagel_ctx* c, int m, cudaStream_t st);
-void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2);
+void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2, int* p1_fused);
 size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1);
 size_t tc_zp_bytes(const bagel_ctx* c, int B);
 int tc_njt(const bagel_ctx* c);
 size_t tc_zpart_count(const bagel_ctx* c, int B);
-int tc_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);
+size_t tc_gbar_count();
+int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st);
 int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st);
 int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st);

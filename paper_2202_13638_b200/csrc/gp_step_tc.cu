@@ -20,6 +20,10 @@
 // scales (per z column in pass 1, per training point in pass 2; per row for Z),
 // undone exactly in the epilogues.
 #include <cuda_fp16.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "bagel_internal.h"
 #include "tc.cuh"
@@ -209,7 +213,63 @@ struct P1Args {
   float* P1z;                // [split][m][ct][NZ][B]
   float* P1h;                // [split][m][B][1 + d]
   float qscale[BAGEL_MAX_P][BAGEL_MAX_D];
+  unsigned long long* dbg;   // nullable: per-CTA %globaltimer event stamps (16 per CTA)
+  // fused reduce 1 (cluster of the S1 splits, nct == 1): the outputs of k_r1a_tc + k_r1b_tc
+  const float* colscale;     // [m][k] 2^e_j
+  float s[BAGEL_MAX_P];
+  float ell2inv[BAGEL_MAX_P][BAGEL_MAX_D];
+  uint8_t* Zp;
+  float* zrow_inv;
+  float* mu;
+  float* var;
+  float* jmu;                // nullable
+  float* sig;                // nullable
+  unsigned long long* gbar;  // grid barrier counter
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp(unsigned long long* dbg, int k) {
+  if (dbg) {
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    dbg[cta * 16 + k] = gtimer();
+  }
+}
+
+// Grid-wide barrier for a cooperative launch (every CTA resident).  Two levels so that at most
+// GB_GROUP atomics serialise on one address (L2 atomics serialise per address): CTA i arrives on
+// group counter i / GB_GROUP; the group's last arriver arrives on the top counter.  Counters only
+// grow (each launch adds one round; they are zeroed when the grid shape changes) and live on
+// separate 256-byte lines.
+constexpr int GB_GROUP = 12;
+constexpr int GB_STRIDE = 32;   // unsigned long longs between counters
+constexpr int GB_MAXGROUPS = 64;
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int G = (int)(gridDim.x * gridDim.y * gridDim.z);
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int grp = cta / GB_GROUP, ngroups = (G + GB_GROUP - 1) / GB_GROUP;
+    const unsigned long long gs = (unsigned long long)min(GB_GROUP, G - grp * GB_GROUP);
+    __threadfence();
+    const unsigned long long old = atomicAdd(ctr + GB_STRIDE * (1 + grp), 1ull);
+    const unsigned long long round = old / gs;
+    if (old % gs == gs - 1) {
+      __threadfence();
+      atomicAdd(ctr, 1ull);
+    }
+    const unsigned long long target = (round + 1) * (unsigned long long)ngroups;
+    unsigned long long cur;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(ctr) : "memory");
+    } while (cur < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -239,7 +299,13 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int D>
+// FUSED (nct == 1, cooperative launch: every CTA is resident): after the MMAs each CTA parks its
+// partial z tile in its idle stage memory, writes it row-major to P1z (coalesced), and after a
+// grid-wide barrier every warp reduces whole rows over the S1 partials in split order and
+// finishes them as reduce 1 does (v, sigma, J^mu, row scale, packed Z): the two reduce launches
+// (and their column-strided passes over the partials) disappear.  (A DSMEM cluster reduction was
+// measured first: cluster residency caps S1 at 6 here and DSMEM moves ~20 B/clk/SM -- slower.)
+template <int D, bool FUSED>
 __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const Geo& g = a.g;
@@ -267,6 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
 
   uint32_t ncols = 32;
   while ((int)ncols < NZ) ncols <<= 1;
+  if (tid == 0) stamp(a.dbg, 0);
   if (tid == 0) {
     for (int s = 0; s < ST1; ++s) {
       tc::mbar_init(&full_a[s], 32 * GEN_WARPS);
@@ -336,8 +403,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
         }
         tc::umma_commit(&empty_a[s]);
         tc::umma_commit(&empty_b[s]);
+        if (i == 0) stamp(a.dbg, 1);
       }
       tc::umma_commit(&done);
+      stamp(a.dbg, 2);
     }
   } else {
     // ------------------------------------------------ ktilde generators (4 threads per row, 8 n each)
@@ -397,6 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
       tc::mbar_arrive(&full_a[s]);
       tc::mbar_arrive(&empty_x[x]);
     }
+    if (gt == 0) stamp(a.dbg, 3);
     // ---- mean columns: combine the four quarters of each row (fixed order)
     if (qd > 0)
       for (int c = 0; c <= D; ++c) hsum[qd - 1][r][c] = hacc[c];
@@ -414,21 +484,152 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
     const int wrow = quarter * 32 + lane;
     const int gw = cdiv_dev(NZ, 32) * 8;  // columns per group (multiple of 8)
     const int c_begin = cg * gw, c_end = min(NZ, c_begin + gw);
-    float* zout = a.P1z + ((size_t)((split * a.m_count + m) * g.nct + ct) * NZ) * a.B;
-    const int grow = row0 + wrow;
-    for (int c0 = c_begin; c0 < c_end; c0 += 8) {
-      float v[8];
-      tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
-      tc::tmem_ld_wait();
-      if (grow < a.B) {
+    if (gt == 0) stamp(a.dbg, 4);
+    if (FUSED) {
+      // partial z tile -> own stage memory [128][NZ + 4] (padded rows: conflict-free v4 stores)
+      float* zs = reinterpret_cast<float*>(sm) + (size_t)wrow * (NZ + 4);
+      for (int c0 = c_begin; c0 < c_end; c0 += 8) {
+        float v[8];
+        tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+        tc::tmem_ld_wait();
+        if (ntile == 0)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) zout[(size_t)(c0 + u) * a.B + grow] = ntile > 0 ? v[u] : 0.0f;
+          for (int u = 0; u < 8; ++u) v[u] = 0.0f;
+        *reinterpret_cast<float4*>(zs + c0) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(zs + c0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      }
+    } else {
+      float* zout = a.P1z + ((size_t)((split * a.m_count + m) * g.nct + ct) * NZ) * a.B;
+      const int grow = row0 + wrow;
+      for (int c0 = c_begin; c0 < c_end; c0 += 8) {
+        float v[8];
+        tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+        tc::tmem_ld_wait();
+        if (grow < a.B) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) zout[(size_t)(c0 + u) * a.B + grow] = ntile > 0 ? v[u] : 0.0f;
+        }
       }
     }
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (tid == 0) stamp(a.dbg, 5);
   if (warp == 1) tc::tmem_dealloc(tmem, ncols);
+  if (FUSED) {
+    const int LDZ = NZ + 4;
+    const int rtn = cdiv_dev(a.B, 128);
+    const int S = (int)gridDim.z;
+    const float* zs = reinterpret_cast<const float*>(sm);
+    // CTA (row tile, m, split) finishes rows rr = split, split + S, ... of its tile; the partials
+    // of all other rows go to P1z row-major [split][m][row tile][128][NZ] (one warp per row:
+    // 512-byte contiguous segments)
+    {
+      float* dst = a.P1z + ((size_t)(split * a.m_count + m) * rtn + blockIdx.x) * 128 * NZ;
+      for (int rr = warp; rr < 128 && row0 + rr < a.B; rr += THREADS / 32)
+        if (rr % S != split)
+          for (int c4 = lane; c4 * 4 < NZ; c4 += 32)
+            *reinterpret_cast<float4*>(dst + (size_t)rr * NZ + c4 * 4) =
+                *reinterpret_cast<const float4*>(zs + rr * LDZ + c4 * 4);
+    }
+    if (tid == 0) stamp(a.dbg, 8);
+    grid_barrier(a.gbar);
+    if (tid == 0) stamp(a.dbg, 6);
+    const bool act = lane * 8 < NZ;
+    const size_t sstride = (size_t)a.m_count * rtn * 128 * NZ;  // floats per split
+    for (int rr = split + S * warp; rr < 128 && row0 + rr < a.B; rr += S * (THREADS / 32)) {
+      const int mm = m, row = row0 + rr;
+      const float* src = a.P1z + ((size_t)mm * rtn * 128 + row) * NZ + lane * 8;
+      const float* hsrc = a.P1h + ((size_t)mm * a.B + row) * (1 + D) + min(lane, D);
+      const size_t hstride = (size_t)a.m_count * a.B * (1 + D);
+      // sum the S partials of columns lane*8 .. lane*8+7 in split order (own one from shared
+      // memory; 6 splits' loads in flight)
+      float z[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) z[e] = 0.0f;
+      float hv = 0.0f;
+      for (int s0 = 0; s0 < S; s0 += 6) {
+        float4 q[6][2];
+        float hq[6];
+#pragma unroll
+        for (int ss = 0; ss < 6; ++ss) {
+          if (s0 + ss < S) {
+            if (act) {
+              const float* p = s0 + ss == split ? zs + rr * LDZ + lane * 8 : src + (s0 + ss) * sstride;
+              if (s0 + ss == split) {
+                q[ss][0] = *reinterpret_cast<const float4*>(p);
+                q[ss][1] = *reinterpret_cast<const float4*>(p + 4);
+              } else {
+                q[ss][0] = __ldcg(reinterpret_cast<const float4*>(p));
+                q[ss][1] = __ldcg(reinterpret_cast<const float4*>(p + 4));
+              }
+            }
+            if (lane <= D) hq[ss] = __ldcg(hsrc + (s0 + ss) * hstride);
+          }
+        }
+#pragma unroll
+        for (int ss = 0; ss < 6; ++ss) {
+          if (s0 + ss < S) {
+            if (act) {
+              z[0] += q[ss][0].x; z[1] += q[ss][0].y; z[2] += q[ss][0].z; z[3] += q[ss][0].w;
+              z[4] += q[ss][1].x; z[5] += q[ss][1].y; z[6] += q[ss][1].z; z[7] += q[ss][1].w;
+            }
+            if (lane <= D) hv += hq[ss];
+          }
+        }
+      }
+      if (tid == 0) stamp(a.dbg, 9);
+      // column scales undone; ||z||^2 (fp64) and max|z| over the row
+      double zz = 0.0;
+      float zm = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = lane * 8 + e;
+        const float v = (act && j < g.k) ? z[e] * a.colscale[(size_t)mm * g.k + j] : 0.0f;
+        z[e] = v;
+        zz += (double)v * (double)v;
+        zm = fmaxf(zm, fabsf(v));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        zz += __shfl_xor_sync(0xffffffffu, zz, o);
+        zm = fmaxf(zm, __shfl_xor_sync(0xffffffffu, zm, o));
+      }
+      float inv;
+      const float sc = pow2_scale_for(zm, &inv);
+      const float h0 = __shfl_sync(0xffffffffu, hv, 0);
+      const float v = (float)((double)a.s[mm] - zz);
+      if (tid == 0) stamp(a.dbg, 10);
+      if (lane == 0) {
+        const float sg = sqrtf(fmaxf(v, BAGEL_VAR_FLOOR));
+        a.zrow_inv[(size_t)mm * a.B + row] = inv;
+        a.mu[(size_t)mm * a.B + row] = h0;
+        a.var[(size_t)mm * a.B + row] = v;
+        if (a.sig) a.sig[(size_t)row * g.p + mm] = v > BAGEL_VAR_FLOOR ? sg : -sg;
+      }
+      if (a.jmu && lane >= 1 && lane <= D)
+        a.jmu[((size_t)row * g.p + mm) * D + lane - 1] =
+            (hv - a.xstar[(size_t)row * D + lane - 1] * h0) * a.ell2inv[mm][lane - 1];
+      if (act) {
+        // packed pass-2 A operand (see k_r1b_tc): hi group `lane`, lo group KJ/8 + lane
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const __half2 h2 = __floats2half2_rn(z[e] * sc, z[e + 1] * sc);
+          const float2 hf = __half22float2(h2);
+          const __half2 l2 = __floats2half2_rn(z[e] * sc - hf.x, z[e + 1] * sc - hf.y);
+          hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+          lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
+        }
+        const int rr = row % 128;
+        uint8_t* base = a.Zp + ((size_t)mm * rtn + row / 128) * (size_t)128 * g.KJ * 2 * 2;
+        *reinterpret_cast<uint4*>(base + ((size_t)lane * 128 + rr) * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(base + ((size_t)(g.KJ / 8 + lane) * 128 + rr) * 16) =
+            make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
+    }
+    if (tid == 0) stamp(a.dbg, 7);
+  }
 }
 
 // ====================================================================== reduce 1
@@ -442,7 +643,7 @@ struct R1Args {
   float s[BAGEL_MAX_P];
   float ell2inv[BAGEL_MAX_P][BAGEL_MAX_D];
   float* Z;                // [m][k][B] fp32 z (after the column scales are undone)
-  uint8_t* Zp;             // packed pass-2 A operand [m][rowtile][jt][hi | lo]
+  uint8_t* Zp;             // packed pass-2 A operand [m][rowtile][jt][16-byte group][row][4 words]
   float* zrow_inv;         // [m][B] 2^e_r (undo of the per-row Z scale)
   float* mu;               // [m][B]
   float* var;              // [m][B]
@@ -591,10 +792,12 @@ __global__ void __launch_bounds__(256) k_r1b_tc(R1Args a, const double* __restri
   for (int c8 = w; c8 * 8 < g.k; c8 += 8) {
     const int j8 = c8 * 8;
     const int jt = j8 / g.KJ, jr = j8 % g.KJ;
-    // row-major per row: [hi: KJ fp16 | lo: KJ fp16] (the TMEM image of the pass-2 A operand)
+    // the TMEM image of the pass-2 A operand: per row KJ words [hi: KJ/2 | lo: KJ/2] (2 fp16 each),
+    // stored as 16-byte groups of 4 words, group-major then row: [group][row 128][4 words], so a
+    // warp's load of one group for 32 consecutive rows is one contiguous 512-byte segment
     uint8_t* base = a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * tile_halfs * 2 * 2;
-    __half* zhi = reinterpret_cast<__half*>(base) + (size_t)rr * 2 * g.KJ;
-    __half* zlo = zhi + g.KJ;
+    uint8_t* zhi = base + ((size_t)(jr / 8) * 128 + rr) * 16;
+    uint8_t* zlo = base + ((size_t)(g.KJ / 8 + jr / 8) * 128 + rr) * 16;
     uint32_t hw[4], lw[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
@@ -606,8 +809,8 @@ __global__ void __launch_bounds__(256) k_r1b_tc(R1Args a, const double* __restri
       hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
       lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
     }
-    *reinterpret_cast<uint4*>(zhi + jr) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    *reinterpret_cast<uint4*>(zlo + jr) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    *reinterpret_cast<uint4*>(zhi) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(zlo) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
 }
 
@@ -624,6 +827,7 @@ struct P2Args {
   int tiles_per_split;
   float* P2;                // [split * njt + jt][m][B][P2_LD]
   float qscale[BAGEL_MAX_P][BAGEL_MAX_D];
+  unsigned long long* dbg;  // nullable: per-CTA %globaltimer event stamps (16 per CTA)
 };
 
 template <int D>
@@ -654,6 +858,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   constexpr uint32_t ZC = 2 * NT2;
   constexpr uint32_t NCOLS = 512;
 
+  if (tid == 0) stamp(a.dbg, 0);
   if (tid == 0) {
     tc::mbar_init(&zready, 32 * GEN_WARPS);
     for (int s = 0; s < ST2; ++s) {
@@ -675,6 +880,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base;
+  if (tid == 0) stamp(a.dbg, 7);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -706,6 +912,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       const uint32_t zhi = tmem + ZC, zlo = tmem + ZC + (uint32_t)(KJ / 2);
       tc::mbar_wait(&zready, 0);
       tc::tc_fence_after();
+      stamp(a.dbg, 1);
       int q = 0;
       for (int i = 0; i < ntile; ++i) {
         const int b = i & 1;
@@ -730,7 +937,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
           tc::umma_commit(&empty_s[s]);
         }
         tc::umma_commit(&tfull[b]);
+        if (i == 0) stamp(a.dbg, 2);
       }
+      stamp(a.dbg, 3);
     }
   } else {
     const int quarter = warp % 4, cg = (warp - CTRL_WARPS) / 4;  // lane quarter, 32-column group
@@ -739,18 +948,35 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
     // ---- Z hi/lo of this CTA's rows -> TMEM (8-word chunks dealt round-robin to the column groups)
     {
       const int rt = blockIdx.x;
-      const uint32_t* zrow = reinterpret_cast<const uint32_t*>(
-          a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * (size_t)128 * KJ * 2 * 2 +
-          (size_t)r * KJ * 2 * 2);  // KJ words: [hi KJ/2 words | lo KJ/2 words]
-      for (int w0 = cg * 8; w0 < KJ; w0 += 32) {
-        const uint4 q0 = *reinterpret_cast<const uint4*>(zrow + w0);
-        const uint4 q1 = *reinterpret_cast<const uint4*>(zrow + w0 + 4);
-        const uint32_t v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        tc::tmem_st8(tmem + ((uint32_t)(quarter * 32) << 16) + ZC + (uint32_t)w0, v);
+      // [group of 4 words][row][4 words] (see k_r1b_tc); this row's group gi is at zrow + gi * 128
+      const uint4* zrow = reinterpret_cast<const uint4*>(
+          a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * (size_t)128 * KJ * 2 * 2) + r;
+      // batches of 8 chunks: all loads of a batch are in flight before the first TMEM store
+      for (int base = cg * 8; base < KJ; base += 8 * 32) {
+        uint4 q[8][2];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int w0 = base + it * 32;
+          if (w0 < KJ) {
+            q[it][0] = __ldg(zrow + (size_t)(w0 / 4) * 128);
+            q[it][1] = __ldg(zrow + (size_t)(w0 / 4 + 1) * 128);
+          }
+        }
+        if (tid == 32 * CTRL_WARPS && base == cg * 8) stamp(a.dbg, 8 + (q[0][0].x == 0x12345678u));
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int w0 = base + it * 32;
+          if (w0 < KJ) {
+            const uint32_t v[8] = {q[it][0].x, q[it][0].y, q[it][0].z, q[it][0].w,
+                                   q[it][1].x, q[it][1].y, q[it][1].z, q[it][1].w};
+            tc::tmem_st8(tmem + ((uint32_t)(quarter * 32) << 16) + ZC + (uint32_t)w0, v);
+          }
+        }
       }
       tc::tmem_st_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&zready);
+      if (tid == 32 * CTRL_WARPS) stamp(a.dbg, 6);
     }
     // ------------------------------------------------ epilogue: sum_n (s w_n) ktilde_n [1 | X_n]
     float xq[D], sc[D];
@@ -797,6 +1023,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       __threadfence_block();  // every aux load above has returned before the stage is released
       tc::mbar_arrive(&empty_x[x]);
     }
+    if (tid == 32 * CTRL_WARPS) stamp(a.dbg, 4);
     // combine the four column groups of each row (fixed order), undo the Z row scale
     if (cg > 0)
       for (int c = 0; c <= D; ++c) asum[cg - 1][r][c] = acc[c];
@@ -808,6 +1035,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (tid == 0) stamp(a.dbg, 5);
   if (warp == 1) tc::tmem_dealloc(tmem, NCOLS);
 }
 
@@ -870,7 +1098,11 @@ int tc_pack(bagel_ctx* c, int m, cudaStream_t st) {
   return 3;
 }
 
-void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2) {
+
+// Pass-1 N splits: one wave of (row tile, m, ct, split) CTAs.  With nct == 1 the whole wave is
+// launched cooperatively and reduce 1 runs inside pass 1 after a grid barrier (k_p1_tc<D, true>);
+// BAGEL_P1_FUSED=0 forces the separate reduce launches.
+void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2, int* p1_fused) {
   const Geo g = geo_of(c);
   const int rt = cdiv(B, 128);
   const int target = c->num_sms;  // one CTA per SM (smem-bound), one wave
@@ -878,6 +1110,9 @@ void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, in
   s1 = s1 < 1 ? 1 : (s1 > g.nt1 ? g.nt1 : s1);
   *tps1 = cdiv(g.nt1, s1);
   *S1 = cdiv(g.nt1, *tps1);
+  const char* env = getenv("BAGEL_P1_FUSED");
+  *p1_fused = g.nct == 1 && rt * g.p * *S1 <= target && rt * g.p * *S1 <= GB_GROUP * GB_MAXGROUPS &&
+              !(env && env[0] == '0');
   int s2 = target / (rt * g.p * g.njt);
   s2 = s2 < 1 ? 1 : (s2 > g.nt2 ? g.nt2 : s2);
   *tps2 = cdiv(g.nt2, s2);
@@ -894,6 +1129,7 @@ size_t tc_zp_bytes(const bagel_ctx* c, int B) {
 }
 int tc_njt(const bagel_ctx* c) { return geo_of(c).njt; }
 size_t tc_zpart_count(const bagel_ctx* c, int B) { return (size_t)c->p * cdiv(c->k, R1_JG) * B; }
+size_t tc_gbar_count() { return (size_t)GB_STRIDE * (1 + GB_MAXGROUPS); }
 
 static void set_attrs() {
   static bool done = false;
@@ -901,13 +1137,15 @@ static void set_attrs() {
   done = true;
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
-      bagel_set_smem_attr(k_p1_tc<D>, 220 * 1024);
+      bagel_set_smem_attr(k_p1_tc<D, false>, 220 * 1024);
+      bagel_set_smem_attr(k_p1_tc<D, true>, 220 * 1024);
       bagel_set_smem_attr(k_p2_tc<D>, 220 * 1024);
     }));
   }
+  cudaGetLastError();
 }
 
-int tc_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
+int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st) {
   set_attrs();
   const Geo g = geo_of(c);
   const TcState& T = c->tcs;
@@ -921,14 +1159,44 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
   a.tiles_per_split = c->ws.tps1;
   a.P1z = T.P1z;
   a.P1h = T.P1h;
+  a.dbg = T.dbg1;
   for (int m = 0; m < c->p; ++m)
     for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
   dim3 grid(cdiv(B, 128), c->p * g.nct, c->ws.S1tc);
-  DISPATCH_D(c->d, (k_p1_tc<D><<<grid, THREADS, p1_smem(g), st>>>(a)));
+  if (c->ws.p1_fused) {
+    a.colscale = T.colscale;
+    for (int m = 0; m < c->p; ++m) {
+      a.s[m] = c->gp.s[m];
+      for (int j = 0; j < BAGEL_MAX_D; ++j) a.ell2inv[m][j] = c->gp.ell2inv[m][j];
+    }
+    a.Zp = T.Zp;
+    a.zrow_inv = T.zrow_inv;
+    a.mu = c->ws.mu;
+    a.var = c->ws.var;
+    a.jmu = jmu_out;
+    a.sig = sig_out;
+    a.P1h = T.P1h;
+    a.gbar = T.gbar;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.dynamicSmemBytes = p1_smem(g);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // a launch error is recorded as the last CUDA error (checked by the caller)
+    DISPATCH_D(c->d, ((void)cudaLaunchKernelEx(&cfg, k_p1_tc<D, true>, a)));
+  } else {
+    DISPATCH_D(c->d, (k_p1_tc<D, false><<<grid, THREADS, p1_smem(g), st>>>(a)));
+  }
   return 1;
 }
 
 int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st) {
+  if (c->ws.p1_fused) return 0;  // done inside pass 1
   const Geo g = geo_of(c);
   const TcState& T = c->tcs;
   R1Args a{};
@@ -970,6 +1238,7 @@ int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
   a.zrow_inv = T.zrow_inv;
   a.tiles_per_split = c->ws.tps2;
   a.P2 = c->ws.P2;
+  a.dbg = T.dbg2;
   for (int m = 0; m < c->p; ++m)
     for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
   dim3 grid(cdiv(B, 128), c->p * g.njt, c->ws.S2tc);

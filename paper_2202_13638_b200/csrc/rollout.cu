@@ -3,22 +3,31 @@
 //   epilogue   per step: finish J^v, eps (Philox), x' = x + mu + sigma eps (Eq.9-10),
 //              G += r(x', g), tape row (a8), next action u' = pi(x', g)
 //   reverse    hand-written reverse mode over the tape, t = T-1..0 (SURVEY
-//              Appendix B): MLP recomputed, theta-bar accumulated per CTA in smem
+//              Appendix B): one warp per trajectory; theta-bar as one contraction over
+//              the (t, b) adjoint tape afterwards
 //   reduce     fixed-order sum of the per-CTA theta-bar partials and of the returns
 //              (L = -(1/B_global) sum_b G_b)
 // The policy is the tanh MLP of P:149 (hidden and output tanh, reading R13);
 // phi = [x, g] or [x, g, g - x] (R14).  These kernels are latency / L2 bound
-// (|theta| and the tape are small); no tensor-core work here in v0.
+// (|theta| and the tape are small); no tensor-core work here.
+#include <algorithm>
+
 #include "bagel_internal.h"
 #include "philox.cuh"
+#include "tc.cuh"
 
 namespace {
 
 constexpr int EPI_ROWS = 8;
-constexpr int REV_ROWS = 8, REV_THREADS = 256;
 constexpr int P2_LD = 1 + BAGEL_MAX_D;
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+__device__ __forceinline__ unsigned long long gtimer_ro() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ float reward_fn(const RewardDesc& rw, const float* x, const float* g, int p) {
   float q = 0.0f;
@@ -27,58 +36,6 @@ __device__ __forceinline__ float reward_fn(const RewardDesc& rw, const float* x,
     q = fmaf(rw.Q[c] * df, df, q);
   }
   return expf(-q * rw.inv_two_sr2);
-}
-
-// act: rows x act_total (smem).  Layer l activations start at aoff(l) = sum_{i<l} sizes[i].
-__device__ __forceinline__ int act_off(const PolicyDesc& P, int l) {
-  int o = 0;
-  for (int i = 0; i < l; ++i) o += P.sizes[i];
-  return o;
-}
-
-// h0 = phi(x, g) for `nrows` rows whose x and g are given (row-major B x p slices).
-__device__ void phi_rows(const PolicyDesc& P, int p, const float* x, const float* g, int nrows,
-                         int valid, float* act) {
-  for (int idx = threadIdx.x; idx < nrows * P.sizes[0]; idx += blockDim.x) {
-    const int r = idx / P.sizes[0], i = idx % P.sizes[0];
-    float v = 0.0f;
-    if (r < valid) {
-      if (i < p) v = x[(size_t)r * p + i];
-      else if (i < 2 * p) v = g[(size_t)r * p + i - p];
-      else v = g[(size_t)r * p + i - 2 * p] - x[(size_t)r * p + i - 2 * p];
-    }
-    act[r * P.act_total + i] = v;
-  }
-}
-
-// h_{l+1} = tanh(W_l h_l + b_l) for every layer (block-cooperative; act in smem).
-// thetaT holds every W_l transposed (Wt[i][o], same offsets as theta) so that the
-// threads of a warp (consecutive o) read consecutive weights: coalesced, L1-resident.
-__device__ void mlp_forward_rows(const PolicyDesc& P, const float* __restrict__ thetaT, int nrows, float* act) {
-  int off_in = 0;
-  for (int l = 0; l < P.n_layers; ++l) {
-    const int in = P.sizes[l], out = P.sizes[l + 1];
-    const int off_out = off_in + in;
-    const float* Wt = thetaT + P.w_off[l];
-    const float* bb = thetaT + P.b_off[l];
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nrows * out; idx += blockDim.x) {
-      const int r = idx / out, o = idx % out;
-      const float* h = act + r * P.act_total + off_in;
-      float a0 = bb[o], a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;  // 4 independent chains (ILP)
-      int i = 0;
-      for (; i + 4 <= in; i += 4) {
-        a0 = fmaf(Wt[(size_t)i * out + o], h[i], a0);
-        a1 = fmaf(Wt[(size_t)(i + 1) * out + o], h[i + 1], a1);
-        a2 = fmaf(Wt[(size_t)(i + 2) * out + o], h[i + 2], a2);
-        a3 = fmaf(Wt[(size_t)(i + 3) * out + o], h[i + 3], a3);
-      }
-      for (; i < in; ++i) a0 = fmaf(Wt[(size_t)i * out + o], h[i], a0);
-      act[r * P.act_total + off_out + o] = tanhf((a0 + a1) + (a2 + a3));
-    }
-    off_in = off_out;
-  }
-  __syncthreads();
 }
 
 // thetaT: per layer W_l^T (in x out), biases copied.
@@ -93,17 +50,6 @@ __global__ void k_transpose_theta(PolicyDesc P, const float* __restrict__ theta,
         thetaT[P.b_off[l] + idx - in * out] = theta[P.b_off[l] + idx - in * out];
       }
     }
-  }
-}
-
-template <int D>
-__device__ void write_xstar(const PolicyDesc& P, int p, const float* act, int nrows, int row0, int B,
-                            float* __restrict__ xstar, const float* xrows) {
-  const int uoff = act_off(P, P.n_layers);
-  for (int idx = threadIdx.x; idx < nrows * D; idx += blockDim.x) {
-    const int r = idx / D, c = idx % D;
-    if (row0 + r >= B) continue;
-    xstar[(size_t)(row0 + r) * D + c] = c < p ? xrows[(size_t)r * p + c] : act[r * P.act_total + uoff + c - p];
   }
 }
 
@@ -124,9 +70,11 @@ __device__ void stage_theta(const PolicyDesc& P, const float* __restrict__ theta
   __syncthreads();
 }
 
-// rows r < nr of this warp: x[r], g[r] (p each); u_out[r] (q each).  buf: RPW x 2 x BAGEL_MAX_WIDTH
+// rows r < nr of this warp: x[r], g[r] (p each); u_out[r] (q each).  buf: RPW x 2 x BAGEL_MAX_WIDTH.
+// act_out (nullable): every activation of row r, [phi | h_1 | ... | u] (segments at P.aoff,
+// row stride P.act_ld), the reverse pass's tape.
 __device__ void warp_policy(const PolicyDesc& P, int p, const float* th_s, const float* x, const float* g, int nr,
-                            float* buf, float* u_out) {
+                            float* buf, float* u_out, float* __restrict__ act_out = nullptr) {
   const int lane = threadIdx.x % 32;
   constexpr int W2 = 2 * BAGEL_MAX_WIDTH;
   for (int r = 0; r < RPW; ++r)
@@ -138,6 +86,7 @@ __device__ void warp_policy(const PolicyDesc& P, int p, const float* th_s, const
         if (i < p) v = xr[i];
         else if (i < 2 * p) v = gr[i - p];
         else v = gr[i - 2 * p] - xr[i - 2 * p];
+        if (act_out) act_out[(size_t)r * P.act_ld + i] = v;
       }
       buf[r * W2 + i] = v;
     }
@@ -172,7 +121,11 @@ __device__ void warp_policy(const PolicyDesc& P, int p, const float* th_s, const
           for (int r = 0; r < RPW; ++r) acc[r][0] = fmaf(w0, buf[r * W2 + cur + i], acc[r][0]);
         }
 #pragma unroll
-        for (int r = 0; r < RPW; ++r) buf[r * W2 + nxt + o] = tanhf(acc[r][0] + acc[r][1]);
+        for (int r = 0; r < RPW; ++r) {
+          const float h = tanhf(acc[r][0] + acc[r][1]);
+          buf[r * W2 + nxt + o] = h;
+          if (act_out && r < nr) act_out[(size_t)r * P.act_ld + P.aoff[l + 1] + o] = h;
+        }
       }
     } else {
       // narrow layer (e.g. the action head): lanes over inputs, butterfly reduction
@@ -189,7 +142,11 @@ __device__ void warp_policy(const PolicyDesc& P, int p, const float* th_s, const
         for (int r = 0; r < RPW; ++r) {
 #pragma unroll
           for (int sh = 16; sh > 0; sh >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], sh);
-          if (lane == 0) buf[r * W2 + nxt + o] = tanhf(acc[r] + bb[o]);
+          if (lane == 0) {
+            const float h = tanhf(acc[r] + bb[o]);
+            buf[r * W2 + nxt + o] = h;
+            if (act_out && r < nr) act_out[(size_t)r * P.act_ld + P.aoff[l + 1] + o] = h;
+          }
         }
       }
     }
@@ -212,7 +169,7 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_init(PolicyDesc P, Rew
                                                               const float* __restrict__ x0,
                                                               const float* __restrict__ goals, int B,
                                                               float* __restrict__ tape_x0, double* __restrict__ G,
-                                                              float* __restrict__ xstar) {
+                                                              float* __restrict__ xstar, float* __restrict__ act0) {
   extern __shared__ __align__(16) float sm[];
   float* th_s = sm;
   float* bufs = sm + ((P.n_params + 3) & ~3);
@@ -226,7 +183,8 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_init(PolicyDesc P, Rew
   const float* g = goals + (size_t)b0 * p;
   if (lane < nr) G[b0 + lane] = (double)reward_fn(rw, x + lane * p, g + lane * p, p);
   for (int i = lane; i < nr * p; i += 32) tape_x0[(size_t)b0 * p + i] = x[i];
-  warp_policy(P, p, th_s, x, g, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0]);
+  warp_policy(P, p, th_s, x, g, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0],
+              act0 + (size_t)b0 * P.act_ld);
   for (int i = lane; i < nr * D; i += 32) {
     const int r = i / D, c = i % D;
     xstar[(size_t)(b0 + r) * D + c] = c < p ? x[r * p + c] : us[w][r][c - p];
@@ -238,15 +196,19 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(
     PolicyDesc P, RewardDesc rw, GpDesc g, const float* __restrict__ thetaT, const float* __restrict__ goals,
     int B, int t, int S2, const float* __restrict__ P2, const float* __restrict__ mu,
     const float* __restrict__ var, const float* __restrict__ tape_x_t, const float* __restrict__ sig_t,
-    float* __restrict__ jv_t, float* __restrict__ tape_x_next, double* __restrict__ G,
+    float* __restrict__ jv_t, const float* __restrict__ jmu_t, float* __restrict__ A_t,
+    float* __restrict__ act_next, float* __restrict__ tape_x_next, double* __restrict__ G,
     float* __restrict__ xstar, uint64_t seed, long long traj_offset, int policy_next,
-    int* __restrict__ err_flag, float* __restrict__ trace_mu, float* __restrict__ trace_var) {
+    int* __restrict__ err_flag, float* __restrict__ trace_mu, float* __restrict__ trace_var,
+    unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(16) float sm[];
   float* th_s = sm;
   float* bufs = sm + ((P.n_params + 3) & ~3);
   __shared__ float us[WARP_ROWS_BLOCK][RPW][BAGEL_MAX_D];
   __shared__ float xn_s[WARP_ROWS_BLOCK][RPW * BAGEL_MAX_P];
+  if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 0] = gtimer_ro();
   if (policy_next) stage_theta(P, thetaT, th_s);
+  if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 1] = gtimer_ro();
   const int p = g.p;
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
@@ -255,40 +217,66 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(
   // lane = r * p * (D + 1) + m * (D + 1) + c: pass-2 partial of (row r, output m, column c)
   const int per_row = p * (D + 1);
   const int nl = nr * per_row;  // <= 2 * 4 * 9 = 72 > 32 possible: loop
+  __shared__ float psum[WARP_ROWS_BLOCK][RPW * BAGEL_MAX_P * (BAGEL_MAX_D + 1)];
   for (int base = 0; base < RPW * per_row; base += 32) {
     const int li = base + lane;
     const bool act = li < nl;
     const int r = act ? li / per_row : 0, m = act ? (li % per_row) / (D + 1) : 0, c = act ? li % (D + 1) : 0;
     const int b = b0 + r;
+    // sum of the S2 pass-2 partials in split order, 8 loads in flight
     float part = 0.0f;
-    if (act)
-      for (int s = 0; s < S2; ++s) part += P2[((size_t)(s * p + m) * B + b) * P2_LD + c];
-    // the c = 0 partial (sum w k) of the same (r, m) sits at lane li - c (same 32-lane window
-    // only when aligned; fetch it from global instead to keep lanes independent)
-    float s0 = part;
-    if (act && c > 0) {
-      s0 = 0.0f;
-      for (int s = 0; s < S2; ++s) s0 += P2[((size_t)(s * p + m) * B + b) * P2_LD];
-      jv_t[((size_t)b * p + m) * D + c - 1] = 2.0f * g.ell2inv[m][c - 1] * (xstar[(size_t)b * D + c - 1] * s0 - part);
+    if (act) {
+      const float* src = P2 + ((size_t)m * B + b) * P2_LD + c;
+      const size_t sstride = (size_t)p * B * P2_LD;
+      for (int s0 = 0; s0 < S2; s0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = s0 + u < S2 ? __ldcg(src + (s0 + u) * sstride) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) part += v[u];
+      }
     }
+    psum[w][li < RPW * per_row ? li : 0] = part;
   }
+  __syncwarp();
+  if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 2] = gtimer_ro();
+  __shared__ float f_s[WARP_ROWS_BLOCK][RPW * BAGEL_MAX_P];
   if (lane < nr * p) {
     const int r = lane / p, m = lane % p, b = b0 + r;
     const float4 e4 = bagel_rollout_eps4(seed, (uint32_t)(traj_offset + b), (uint32_t)t);
-    const float sg = fabsf(sig_t[(size_t)b * p + m]);
+    const float sgr = sig_t[(size_t)b * p + m];
+    const float sg = fabsf(sgr);
+    const float e = bagel_f4get(e4, m & 3);
     const float mum = mu[(size_t)m * B + b];
-    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * bagel_f4get(e4, m & 3);
+    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * e;
     if (!isfinite(xn)) atomicMin(err_flag, t * B + b);
     tape_x_next[(size_t)b * p + m] = xn;
     xn_s[w][r * p + m] = xn;
+    // d x'/d sigma^2 = eps / (2 sigma) where the variance is not clamped (R19), else 0
+    f_s[w][r * p + m] = sgr > 0.0f ? e / (2.0f * sgr) : 0.0f;
     if (trace_mu) trace_mu[(size_t)b * p + m] = mum;
     if (trace_var) trace_var[(size_t)b * p + m] = var[(size_t)m * B + b];
   }
   __syncwarp();
+  // J^v from the (r, m) row of sums [sum w k | sum w k X_c]; tape A = J^mu + f J^v (reverse input)
+  for (int li = lane; li < nl; li += 32) {
+    const int r = li / per_row, m = (li % per_row) / (D + 1), c = li % (D + 1);
+    if (c == 0) continue;
+    const int b = b0 + r;
+    const float s0 = psum[w][li - c], part = psum[w][li];
+    const float jv = 2.0f * g.ell2inv[m][c - 1] * (xstar[(size_t)b * D + c - 1] * s0 - part);
+    const size_t o = ((size_t)b * p + m) * D + c - 1;
+    jv_t[o] = jv;
+    A_t[o] = fmaf(f_s[w][r * p + m], jv, jmu_t[o]);
+  }
+  __syncwarp();
   const float* gb = goals + (size_t)b0 * p;
   if (lane < nr) G[b0 + lane] += (double)reward_fn(rw, &xn_s[w][lane * p], gb + lane * p, p);
+  if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 3] = gtimer_ro();
   if (!policy_next) return;
-  warp_policy(P, p, th_s, xn_s[w], gb, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0]);
+  warp_policy(P, p, th_s, xn_s[w], gb, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0],
+              act_next + (size_t)b0 * P.act_ld);
+  if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 4] = gtimer_ro();
   for (int i = lane; i < nr * D; i += 32) {
     const int r = i / D, c = i % D;
     xstar[(size_t)(b0 + r) * D + c] = c < p ? xn_s[w][r * p + c] : us[w][r][c - p];
@@ -296,145 +284,304 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(
 }
 
 // ------------------------------------------------------------------ reverse
-// smem: gacc[n_params] | act[REV_ROWS x act_total] | dl[2][REV_ROWS x max_width] | xbar | xsbar
+// The adjoint recursion couples the steps of ONE trajectory only, so it
+// runs as one warp per row over t = T-1..0 with everything it needs on the tape: the combined
+// state Jacobian A_t = J^mu + (eps / 2 sigma) J^v (epilogue) and every policy activation
+// (forward).  The recursion emits delta_l (the pre-activation adjoints) to a tape; the parameter
+// gradient sum_{t,b} delta_l h_l^T is a separate contraction over all (t, b) (k_theta_grad).
+//   xs-bar_c = sum_m xbar_m A_t[m][c]                                       (c < d)
+//   delta_L  = xs-bar[p:] (1 - u^2);  delta_{l-1} = (W_l^T delta_l) (1 - h_l^2)
+//   xbar_t   = xbar_{t+1} + xs-bar[:p] + dphi/dx^T (W_0^T delta_0) + d(r_t / B)/dx_t
+// W (row-major, as theta) is staged in shared memory once per block; each step's tape row
+// (activations, A, x) is prefetched one step ahead with cp.async into a per-warp double buffer, so
+// the recursion itself only touches shared memory.
+constexpr int REV2_WARPS = 8;
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// per-warp shared region of k_reverse2: 2 adjoint buffers + 2 tape rows [act | A | x]
+__host__ __device__ inline int rev2_row_floats(const PolicyDesc& P, int p, int d) {
+  return (P.act_ld + p * d + p + 3) & ~3;
+}
+__host__ __device__ inline int rev2_warp_floats(const PolicyDesc& P, int p, int d) {
+  return 2 * ((P.max_width + 3) & ~3) + 2 * rev2_row_floats(P, p, d);
+}
+
 template <int D>
-__global__ void __launch_bounds__(REV_THREADS) k_reverse(
-    PolicyDesc P, RewardDesc rw, int p, const float* __restrict__ theta, const float* __restrict__ thetaT,
-    const float* __restrict__ goals, int B, int T, const float* __restrict__ tape_x, const float* __restrict__ tape_sig,
-    const float* __restrict__ tape_jmu, const float* __restrict__ tape_jv, uint64_t seed,
-    long long traj_offset, float invB, float* __restrict__ theta_part) {
+__global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
+    PolicyDesc P, RewardDesc rw, int p, const float* __restrict__ theta, const float* __restrict__ goals, int B,
+    int T, const float* __restrict__ tape_x, const float* __restrict__ tape_A, const float* __restrict__ tape_act,
+    float* __restrict__ tape_delta, float invB) {
   extern __shared__ __align__(16) float sm[];
   const int np4 = (P.n_params + 3) & ~3;
-  float* th_s = sm;                 // theta (W_l row-major) for h-bar = W^T delta
-  float* thT_s = th_s + np4;        // theta^T for the forward recompute
-  float* gacc = thT_s + np4;
-  float* act = gacc + np4;
-  float* dl0 = act + REV_ROWS * P.act_total;
-  float* dl1 = dl0 + REV_ROWS * P.max_width;
-  float* xbar = dl1 + REV_ROWS * P.max_width;  // REV_ROWS x p
-  float* xsbar = xbar + REV_ROWS * BAGEL_MAX_P;  // REV_ROWS x D
-  __shared__ float gs[REV_ROWS * BAGEL_MAX_P];
-
-  const int tid = threadIdx.x;
-  const int row0 = blockIdx.x * REV_ROWS;
-  const int valid = min(REV_ROWS, B - row0);
-  const float inv_sr2 = 2.0f * rw.inv_two_sr2;
-  for (int i = tid; i < P.n_params; i += blockDim.x) {
-    gacc[i] = 0.0f;
-    th_s[i] = __ldg(theta + i);
-    thT_s[i] = __ldg(thetaT + i);
-  }
-  for (int i = tid; i < REV_ROWS * p; i += blockDim.x) {
-    const int r = i / p, c = i % p;
-    gs[i] = r < valid ? goals[(size_t)(row0 + r) * p + c] : 0.0f;
-  }
+  const int RF = rev2_row_floats(P, p, D);
+  const int mw4 = (P.max_width + 3) & ~3;
+  float* th_s = sm;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float* d0 = th_s + np4 + (size_t)w * rev2_warp_floats(P, p, D);  // this warp's region
+  float* d1 = d0 + mw4;
+  float* rows = d1 + mw4;  // 2 x RF: [act | A | x] of one step
+  for (int i = threadIdx.x; i < P.n_params; i += blockDim.x) th_s[i] = __ldg(theta + i);
   __syncthreads();
-  // xbar_T = (1/B) r_T Q (x_T - g) / sigma_r^2
-  if (tid < REV_ROWS) {
-    const int r = tid;
-    for (int c = 0; c < p; ++c) xbar[r * p + c] = 0.0f;
-    if (r < valid) {
-      const float* xT = tape_x + ((size_t)T * B + row0 + r) * p;
-      const float rr = reward_fn(rw, xT, gs + r * p, p);
-      for (int c = 0; c < p; ++c) xbar[r * p + c] = invB * rr * rw.Q[c] * (xT[c] - gs[r * p + c]) * inv_sr2;
-    }
-  }
+  const int b = blockIdx.x * REV2_WARPS + w;
+  if (b >= B || T <= 0) return;  // warp-uniform
   const int L = P.n_layers;
-  const int uoff = act_off(P, L);
+  const int q = P.sizes[L];
+  const int AL = P.act_ld, pd = p * D;
+  const float inv_sr2 = 2.0f * rw.inv_two_sr2;
+  auto prefetch = [&](int t, float* dst) {
+    const float* act = tape_act + ((size_t)t * B + b) * AL;
+    const float* A = tape_A + ((size_t)t * B + b) * pd;
+    const float* x = tape_x + ((size_t)t * B + b) * p;
+    for (int i = lane * 4; i < AL; i += 128) cp_async16(dst + i, act + i);
+    if (lane < pd) cp_async4(dst + AL + lane, A + lane);
+    if (lane < p) cp_async4(dst + AL + pd + lane, x + lane);
+    cp_async_commit();
+  };
+  prefetch(T - 1, rows);
+  const float gl = lane < p ? goals[(size_t)b * p + lane] : 0.0f;
+  float xb = 0.0f;
+  {
+    // xbar_T = (1/B) r(x_T) Q (x_T - g) / sigma_r^2
+    const float xT = lane < p ? tape_x[((size_t)T * B + b) * p + lane] : 0.0f;
+    float qd = lane < p ? rw.Q[lane] * (xT - gl) * (xT - gl) : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) qd += __shfl_xor_sync(0xffffffffu, qd, o);
+    const float rr = expf(-qd * rw.inv_two_sr2);
+    if (lane < p) xb = invB * rr * rw.Q[lane] * (xT - gl) * inv_sr2;
+  }
   for (int t = T - 1; t >= 0; --t) {
-    __syncthreads();
-    const float* xt = tape_x + ((size_t)t * B + row0) * p;
-    // xs_bar = sum_m xbar_m (Jmu_m + [v > floor] eps_m / (2 sigma_m) Jv_m)
-    if (tid < REV_ROWS) {
-      const int r = tid;
-      for (int c = 0; c < D; ++c) xsbar[r * D + c] = 0.0f;
-      if (r < valid) {
-        const int b = row0 + r;
-        const float4 e4 = bagel_rollout_eps4(seed, (uint32_t)(traj_offset + b), (uint32_t)t);
-        for (int m = 0; m < p; ++m) {
-          const float sg = tape_sig[((size_t)t * B + b) * p + m];
-          const float f = sg > 0.0f ? bagel_f4get(e4, m & 3) / (2.0f * sg) : 0.0f;
-          const float* jm = tape_jmu + (((size_t)t * B + b) * p + m) * D;
-          const float* jv = tape_jv + (((size_t)t * B + b) * p + m) * D;
-          const float xb = xbar[r * p + m];
-#pragma unroll
-          for (int c = 0; c < D; ++c) xsbar[r * D + c] = fmaf(xb, jm[c] + f * jv[c], xsbar[r * D + c]);
-        }
+    float* cur = rows + ((T - 1 - t) & 1) * RF;
+    if (t > 0) {
+      prefetch(t - 1, rows + ((T - t) & 1) * RF);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const float* act = cur;
+    const float* At = cur + AL;
+    const float xt = lane < p ? cur[AL + pd + lane] : 0.0f;
+    float* dl = tape_delta + ((size_t)t * B + b) * P.d_ld;
+    // xs-bar_c (lane c < D)
+    float xs = 0.0f;
+    for (int m = 0; m < p; ++m) {
+      const float xbm = __shfl_sync(0xffffffffu, xb, m);
+      if (lane < D) xs = fmaf(xbm, At[m * D + lane], xs);
+    }
+    // delta_L = ubar (1 - u^2), ubar = xs-bar[p + o]
+    for (int o = 0; o < q; o += 32) {
+      const float ub = __shfl_sync(0xffffffffu, xs, min(p + o + lane, 31));
+      if (o + lane < q) {
+        const float u = act[P.aoff[L] + o + lane];
+        d0[o + lane] = ub * (1.0f - u * u);
       }
     }
-    phi_rows(P, p, xt, gs, REV_ROWS, valid, act);
-    mlp_forward_rows(P, thT_s, REV_ROWS, act);  // ends with __syncthreads
-    // delta_L = ubar (1 - u^2)
-    {
-      const int q = P.sizes[L];
-      for (int idx = tid; idx < REV_ROWS * q; idx += blockDim.x) {
-        const int r = idx / q, o = idx % q;
-        const float u = act[r * P.act_total + uoff + o];
-        dl0[r * P.max_width + o] = r < valid ? xsbar[r * D + p + o] * (1.0f - u * u) : 0.0f;
-      }
-    }
-    float* dcur = dl0;
-    float* dprev = dl1;
-    int off_in = uoff;
+    __syncwarp();
+    float* dc = d0;
+    float* dn = d1;
     for (int l = L - 1; l >= 0; --l) {
-      __syncthreads();
       const int in = P.sizes[l], out = P.sizes[l + 1];
-      off_in -= in;
       const float* W = th_s + P.w_off[l];
-      // theta-bar: W_l[o][i] += sum_r delta[r][o] h_l[r][i];  b_l[o] += sum_r delta[r][o]
-      for (int idx = tid; idx < out * in + out; idx += blockDim.x) {
+      for (int o = lane; o < out; o += 32) dl[P.doff[l] + o] = dc[o];
+      const float* hin = act + P.aoff[l];  // layer l's input activations
+      if (in >= 32) {
+        // lanes over inputs, two inputs per pass, 4 o's per iteration (8 independent chains)
+        for (int i = lane; i < in; i += 64) {
+          const bool two = i + 32 < in;
+          const int i2 = two ? i + 32 : i;
+          float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+          int o = 0;
+#pragma unroll 2
+          for (; o + 4 <= out; o += 4) {
+            const float e0 = dc[o], e1 = dc[o + 1], e2 = dc[o + 2], e3 = dc[o + 3];
+            a0 = fmaf(W[(o + 0) * in + i], e0, a0);
+            a1 = fmaf(W[(o + 1) * in + i], e1, a1);
+            a2 = fmaf(W[(o + 2) * in + i], e2, a2);
+            a3 = fmaf(W[(o + 3) * in + i], e3, a3);
+            c0 = fmaf(W[(o + 0) * in + i2], e0, c0);
+            c1 = fmaf(W[(o + 1) * in + i2], e1, c1);
+            c2 = fmaf(W[(o + 2) * in + i2], e2, c2);
+            c3 = fmaf(W[(o + 3) * in + i2], e3, c3);
+          }
+          for (; o < out; ++o) {
+            a0 = fmaf(W[o * in + i], dc[o], a0);
+            c0 = fmaf(W[o * in + i2], dc[o], c0);
+          }
+          const float hb = (a0 + a1) + (a2 + a3), hb2 = (c0 + c1) + (c2 + c3);
+          if (l > 0) {
+            const float h = hin[i];
+            dn[i] = hb * (1.0f - h * h);
+            if (two) {
+              const float h2 = hin[i2];
+              dn[i2] = hb2 * (1.0f - h2 * h2);
+            }
+          } else {
+            dn[i] = hb;
+            if (two) dn[i2] = hb2;
+          }
+        }
+      } else {
+        // narrow input: lane = (o group, i); groups of the o range, xor-reduced (fixed tree)
+        int ip = 1;
+        while (ip < in) ip <<= 1;
+        const int ng = 32 / ip, i = lane % ip, grp = lane / ip;
         float a = 0.0f;
-        if (idx < out * in) {
-          const int o = idx / in, i = idx % in;
-#pragma unroll
-          for (int r = 0; r < REV_ROWS; ++r) a = fmaf(dcur[r * P.max_width + o], act[r * P.act_total + off_in + i], a);
-          gacc[P.w_off[l] + idx] += a;
-        } else {
-          const int o = idx - out * in;
-#pragma unroll
-          for (int r = 0; r < REV_ROWS; ++r) a += dcur[r * P.max_width + o];
-          gacc[P.b_off[l] + o] += a;
+        if (i < in)
+          for (int o = grp; o < out; o += ng) a = fmaf(W[o * in + i], dc[o], a);
+        for (int sh = 16; sh >= ip; sh >>= 1) a += __shfl_xor_sync(0xffffffffu, a, sh);
+        if (lane < in) {
+          const float h = l > 0 ? hin[lane] : 0.0f;
+          dn[lane] = l > 0 ? a * (1.0f - h * h) : a;
         }
       }
-      // h-bar_l = W_l^T delta; delta_{l-1} = h-bar (1 - h^2) for hidden layers
-      for (int idx = tid; idx < REV_ROWS * in; idx += blockDim.x) {
-        const int r = idx / in, i = idx % in;
-        float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-        int o = 0;
-        for (; o + 4 <= out; o += 4) {
-          a0 = fmaf(W[(size_t)o * in + i], dcur[r * P.max_width + o], a0);
-          a1 = fmaf(W[(size_t)(o + 1) * in + i], dcur[r * P.max_width + o + 1], a1);
-          a2 = fmaf(W[(size_t)(o + 2) * in + i], dcur[r * P.max_width + o + 2], a2);
-          a3 = fmaf(W[(size_t)(o + 3) * in + i], dcur[r * P.max_width + o + 3], a3);
-        }
-        for (; o < out; ++o) a0 = fmaf(W[(size_t)o * in + i], dcur[r * P.max_width + o], a0);
-        float a = (a0 + a1) + (a2 + a3);
-        if (l > 0) {
-          const float h = act[r * P.act_total + off_in + i];
-          a *= (1.0f - h * h);
-        }
-        dprev[r * P.max_width + i] = a;
-      }
-      float* tmp = dcur;
-      dcur = dprev;
-      dprev = tmp;
+      __syncwarp();
+      float* tmp = dc;
+      dc = dn;
+      dn = tmp;
     }
-    __syncthreads();
-    // xbar_t = xbar_{t+1} + xs_bar[:p] + d phi/dx^T h0-bar + d(r_t / B)/dx_t
-    if (tid < REV_ROWS && tid < valid) {
-      const int r = tid;
-      const float* x = xt + (size_t)r * p;
-      const float rr = reward_fn(rw, x, gs + r * p, p);
-      for (int c = 0; c < p; ++c) {
-        float hb = dcur[r * P.max_width + c];
-        if (P.phi_mode == 1) hb -= dcur[r * P.max_width + 2 * p + c];
-        xbar[r * p + c] += xsbar[r * D + c] + hb + invB * rr * rw.Q[c] * (x[c] - gs[r * p + c]) * inv_sr2;
+    // xbar_t = xbar_{t+1} + xs-bar[:p] + dphi/dx^T h0-bar + d(r_t / B)/dx_t; phi = [x, g] or [x, g, g - x]
+    float hb_phi = 0.0f;
+    if (lane < p) {
+      hb_phi = dc[lane];
+      if (P.phi_mode == 1) hb_phi -= dc[2 * p + lane];
+    }
+    float qd = lane < p ? rw.Q[lane] * (xt - gl) * (xt - gl) : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) qd += __shfl_xor_sync(0xffffffffu, qd, o);
+    const float rr = expf(-qd * rw.inv_two_sr2);
+    if (lane < p) xb += xs + hb_phi + invB * rr * rw.Q[lane] * (xt - gl) * inv_sr2;
+    __syncwarp();
+  }
+}
+
+// theta-bar = sum over (t, b) of delta_l h_l^T (weights) and delta_l (biases): a K = T B
+// contraction split over the CTAs (contiguous K ranges, one partial per CTA, summed in CTA order
+// by k_reduce_grad).  The tape rows of a range are contiguous, so TG_KC-row chunks of both tapes
+// arrive by 1-D bulk copies (TMA engine) into a TG_ST-stage ring; each thread owns up to TG_JOBS
+// 4 x 4 (o, i) weight tiles (or 4-bias groups) with register accumulators and reads its float4
+// slices of every staged row.
+constexpr int TG_THREADS = 256, TG_KC = 32, TG_ST = 3, TG_JOBS = 2;
+
+__global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long long K, const float* __restrict__ tape_act,
+                                                          const float* __restrict__ tape_delta,
+                                                          float* __restrict__ theta_part) {
+  extern __shared__ __align__(16) float sm[];
+  __shared__ __align__(8) uint64_t full[TG_ST];
+  const int AL = P.act_ld, DL = P.d_ld;
+  const int stage_f = TG_KC * (AL + DL);
+  const long long per = (K + gridDim.x - 1) / gridDim.x;
+  const long long k0 = blockIdx.x * per, k1 = min(K, k0 + per);
+  const int nchunks = k1 > k0 ? (int)((k1 - k0 + TG_KC - 1) / TG_KC) : 0;
+  float* out = theta_part + (size_t)blockIdx.x * P.n_params;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TG_ST; ++s) tc::mbar_init(&full[s], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  int njobs = 0;
+  for (int l = 0; l < P.n_layers; ++l) njobs += ((P.sizes[l + 1] + 3) / 4) * ((P.sizes[l] + 3) / 4 + 1);
+  const int nbatch = (njobs + TG_THREADS * TG_JOBS - 1) / (TG_THREADS * TG_JOBS);
+  const int total = nbatch * nchunks;  // the K range is streamed once per job batch
+  // chunk g of the whole sequence: batch g / nchunks, rows of chunk g % nchunks; stage g % TG_ST
+  auto issue = [&](int g) {
+    const int s = g % TG_ST, c = g % nchunks;
+    const long long r0 = k0 + (long long)c * TG_KC;
+    const int rows = (int)min((long long)TG_KC, k1 - r0);
+    const uint32_t ba = (uint32_t)rows * AL * 4, bd = (uint32_t)rows * DL * 4;
+    tc::mbar_arrive_expect_tx(&full[s], ba + bd);
+    float* dst = sm + (size_t)s * stage_f;
+    tc::bulk_g2s(dst, tape_act + r0 * AL, ba, &full[s]);
+    tc::bulk_g2s(dst + TG_KC * AL, tape_delta + r0 * DL, bd, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int g = 0; g < TG_ST && g < total; ++g) issue(g);
+  for (int batch = 0; batch < nbatch; ++batch) {
+    const int jbase = batch * TG_THREADS * TG_JOBS;
+    // job u of this thread: delta slice offset, activation slice offset (-1: bias group)
+    int jd[TG_JOBS], ja[TG_JOBS];
+#pragma unroll
+    for (int u = 0; u < TG_JOBS; ++u) {
+      int j = jbase + u * TG_THREADS + threadIdx.x;
+      jd[u] = -1;
+      ja[u] = -1;
+      for (int l = 0; l < P.n_layers && j >= 0; ++l) {
+        const int no = (P.sizes[l + 1] + 3) / 4, ni = (P.sizes[l] + 3) / 4 + 1;
+        if (j < no * ni) {
+          jd[u] = P.doff[l] + (j / ni) * 4;
+          ja[u] = (j % ni) == ni - 1 ? -1 : P.aoff[l] + (j % ni) * 4;
+        }
+        j -= no * ni;
+      }
+    }
+    float acc[TG_JOBS][16];
+#pragma unroll
+    for (int u = 0; u < TG_JOBS; ++u)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[u][e] = 0.0f;
+    for (int c = 0; c < nchunks; ++c) {
+      const int g = batch * nchunks + c, s = g % TG_ST;
+      const int rows = (int)min((long long)TG_KC, k1 - (k0 + (long long)c * TG_KC));
+      tc::mbar_wait(&full[s], (uint32_t)(g / TG_ST) & 1u);
+      const float* hs = sm + (size_t)s * stage_f;
+      const float* ds = hs + TG_KC * AL;
+#pragma unroll
+      for (int u = 0; u < TG_JOBS; ++u) {
+        if (jd[u] < 0) continue;
+        if (ja[u] >= 0) {
+          for (int r = 0; r < rows; ++r) {
+            const float4 d4 = *reinterpret_cast<const float4*>(ds + r * DL + jd[u]);
+            const float4 h4 = *reinterpret_cast<const float4*>(hs + r * AL + ja[u]);
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hv[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+            for (int eo = 0; eo < 4; ++eo)
+#pragma unroll
+              for (int ei = 0; ei < 4; ++ei) acc[u][eo * 4 + ei] = fmaf(dv[eo], hv[ei], acc[u][eo * 4 + ei]);
+          }
+        } else {
+          for (int r = 0; r < rows; ++r) {
+            const float4 d4 = *reinterpret_cast<const float4*>(ds + r * DL + jd[u]);
+            acc[u][0] += d4.x;
+            acc[u][1] += d4.y;
+            acc[u][2] += d4.z;
+            acc[u][3] += d4.w;
+          }
+        }
+      }
+      __syncthreads();  // every thread is done with stage s
+      if (threadIdx.x == 0 && g + TG_ST < total) issue(g + TG_ST);
+    }
+    // write this CTA's partial (every parameter exactly once over the batches)
+#pragma unroll
+    for (int u = 0; u < TG_JOBS; ++u) {
+      int j = jbase + u * TG_THREADS + threadIdx.x;
+      for (int l = 0; l < P.n_layers && j >= 0; ++l) {
+        const int in = P.sizes[l], outw = P.sizes[l + 1];
+        const int no = (outw + 3) / 4, ni = (in + 3) / 4 + 1;
+        if (j < no * ni) {
+          const int o0 = (j / ni) * 4, it = j % ni;
+          for (int eo = 0; eo < 4; ++eo) {
+            if (o0 + eo >= outw) continue;
+            if (it == ni - 1) {
+              out[P.b_off[l] + o0 + eo] = nchunks ? acc[u][eo] : 0.0f;
+            } else {
+              for (int ei = 0; ei < 4; ++ei)
+                if (it * 4 + ei < in) out[P.w_off[l] + (o0 + eo) * in + it * 4 + ei] = acc[u][eo * 4 + ei];
+            }
+          }
+        }
+        j -= no * ni;
       }
     }
   }
-  __syncthreads();
-  float* out = theta_part + (size_t)blockIdx.x * P.n_params;
-  for (int i = tid; i < P.n_params; i += blockDim.x) out[i] = gacc[i];
 }
 
 __global__ void k_reduce_grad(const float* __restrict__ part, int nblk, int n_params,
@@ -501,21 +648,25 @@ size_t epi_smem(const PolicyDesc& P) { return sizeof(float) * EPI_ROWS * P.act_t
 
 }  // namespace
 
-size_t ro_reverse_smem(const PolicyDesc& P) {
-  return sizeof(float) * (3 * ((P.n_params + 3) & ~3) + REV_ROWS * P.act_total + 2 * REV_ROWS * P.max_width +
-                          REV_ROWS * BAGEL_MAX_P + REV_ROWS * BAGEL_MAX_D);
+size_t ro_reverse_smem(const PolicyDesc& P, int p, int d) {
+  return sizeof(float) * (((P.n_params + 3) & ~3) + (size_t)REV2_WARPS * rev2_warp_floats(P, p, d));
+}
+size_t ro_theta_grad_smem(const PolicyDesc& P) { return sizeof(float) * (size_t)TG_ST * TG_KC * (P.act_ld + P.d_ld); }
+int ro_theta_blocks(const bagel_ctx* c, int B, int T) {
+  const long long K = (long long)B * std::max(T, 1);
+  return (int)std::max(1LL, std::min((long long)c->num_sms, K / 64));
 }
 size_t ro_policy_smem(const PolicyDesc& P) { return policy_smem(P); }
 size_t ro_epilogue_smem(const PolicyDesc& P) { return epi_smem(P); }
-int ro_reverse_block_rows() { return REV_ROWS; }
 
 void ro_set_attributes() {
   static bool done = false;
   if (done) return;
   done = true;
+  bagel_set_smem_attr(k_theta_grad, 200 * 1024);
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
-      bagel_set_smem_attr(k_reverse<D>, 200 * 1024);
+      bagel_set_smem_attr(k_reverse2<D>, 200 * 1024);
       bagel_set_smem_attr(k_epilogue<D>, 200 * 1024);
       bagel_set_smem_attr(k_init<D>, 200 * 1024);
 
@@ -528,7 +679,8 @@ int ro_init(const bagel_ctx* c, const float* theta, const float* x0, const float
   ro_set_attributes();
   k_transpose_theta<<<cdiv(c->pol.n_params, 256), 256, 0, st>>>(c->pol, theta, c->ws.thetaT);
   DISPATCH_D(c->gp.d, (k_init<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
-                          c->pol, c->rw, c->gp.p, c->ws.thetaT, x0, goals, B, c->ws.tape_x, c->ws.G, c->ws.xstar)));
+                          c->pol, c->rw, c->gp.p, c->ws.thetaT, x0, goals, B, c->ws.tape_x, c->ws.G, c->ws.xstar,
+                          c->ws.tape_act)));
   return 2;
 }
 
@@ -541,20 +693,31 @@ int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals,
   DISPATCH_D(d, (k_epilogue<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
                     c->pol, c->rw, c->gp, w.thetaT, goals, B, t, w.S2eff, w.P2, w.mu, w.var,
                     w.tape_x + (size_t)t * B * p, w.tape_sig + (size_t)t * B * p,
-                    w.tape_jv + (size_t)t * B * p * d, w.tape_x + (size_t)(t + 1) * B * p, w.G, w.xstar,
-                    seed, traj_offset, policy_next ? 1 : 0, w.err_flag, trace_mu, trace_var)));
+                    w.tape_jv + (size_t)t * B * p * d, w.tape_jmu + (size_t)t * B * p * d,
+                    w.tape_A + (size_t)t * B * p * d, w.tape_act + (size_t)(t + 1) * B * c->pol.act_ld,
+                    w.tape_x + (size_t)(t + 1) * B * p, w.G, w.xstar,
+                    seed, traj_offset, policy_next ? 1 : 0, w.err_flag, trace_mu, trace_var,
+                    t == T - 2 ? c->tcs.dbg3 : nullptr)));
   return 1;
 }
 
 int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B, int T, uint64_t seed,
                long long traj_offset, long long B_global, int* nblk_out, cudaStream_t st) {
+  (void)seed;
+  (void)traj_offset;
   ro_set_attributes();
-  const int nblk = cdiv(B, REV_ROWS);
-  *nblk_out = nblk;
   const Workspace& w = c->ws;
-  DISPATCH_D(c->gp.d, (k_reverse<D><<<nblk, REV_THREADS, ro_reverse_smem(c->pol), st>>>(
-                          c->pol, c->rw, c->gp.p, theta, w.thetaT, goals, B, T, w.tape_x, w.tape_sig, w.tape_jmu,
-                          w.tape_jv, seed, traj_offset, (float)(1.0 / (double)B_global), w.theta_part)));
+  DISPATCH_D(c->gp.d, (k_reverse2<D><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, ro_reverse_smem(c->pol, c->gp.p, c->gp.d), st>>>(
+                          c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
+                          (float)(1.0 / (double)B_global))));
+  *nblk_out = ro_theta_blocks(c, B, T);
+  return 1;
+}
+
+int ro_theta_grad(const bagel_ctx* c, int B, int T, int nblk, cudaStream_t st) {
+  const Workspace& w = c->ws;
+  k_theta_grad<<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(c->pol, (long long)T * B, w.tape_act,
+                                                                      w.tape_delta, w.theta_part);
   return 1;
 }
 

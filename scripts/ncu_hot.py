@@ -1,33 +1,31 @@
-"""Top SASS lines by stall samples for one kernel of an ncu report (needs -lineinfo / --import-source)."""
+"""Summarise an ncu report: key metrics per kernel and the hottest SASS lines (stall samples)."""
 import csv
+import io
 import subprocess
 import sys
 
-
-def main(path, kregex, n=30, ctx=0):
-    out = subprocess.check_output(["ncu", "-i", path, "--page", "source", "--csv", "--kernel-name", "regex:" + kregex,
-                                   "--print-source", "sass"], text=True)
-    rows = list(csv.reader(out.splitlines()))
-    hdr = rows[1]
-    data, seen = [], set()
-    for r in rows[2:]:
-        if len(r) < 3 or r[0] in seen:
-            continue
-        seen.add(r[0])
-        data.append(r)
-    i_s = hdr.index("Warp Stall Sampling (All Samples)")
-    tot = sum(int(r[i_s]) for r in data if r[i_s].isdigit())
-    order = sorted(range(len(data)), key=lambda i: -int(data[i][i_s]) if data[i][i_s].isdigit() else 0)
-    print("total samples", tot)
-    for i in order[:n]:
-        if ctx:
-            for j in range(max(0, i - ctx), i):
-                print("      ", data[j][0][-5:], data[j][1][:100])
-        print(data[i][i_s].rjust(6), data[i][0][-5:], data[i][1][:100])
-        if ctx:
-            print()
-
-
-if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30,
-         int(sys.argv[4]) if len(sys.argv) > 4 else 0)
+rep = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h = rows[0]
+want = ["Kernel Name", "gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "smsp__inst_executed.sum", "launch__occupancy_limit_shared_mem", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active"]
+for r in rows[2:]:
+    print({n: r[h.index(n)] for n in want if n in h})
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+                     text=True).stdout
+blocks = src.split('"Kernel Name"')
+for b in blocks[1:]:
+    lines = list(csv.reader(io.StringIO('"Kernel Name"' + b)))
+    name = lines[0][1]
+    hh = lines[1]
+    data = lines[2:]
+    si = hh.index("Warp Stall Sampling (All Samples)")
+    tot = sum(int(r[si]) for r in data if len(r) > si and r[si].isdigit())
+    print("\n==", name[:80], "samples", tot)
+    idx = sorted(range(len(data)), key=lambda i: -(int(data[i][si]) if len(data[i]) > si and data[i][si].isdigit() else 0))[:top]
+    for i in sorted(idx):
+        print(f"{i:5d} {data[i][si]:>5s}  {data[i][1][:100]}")
