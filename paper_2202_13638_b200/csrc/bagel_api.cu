@@ -204,9 +204,9 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
       dev_alloc(c, c->tcs.Zp, tc_zp_bytes(c, B));
       CK(cudaMemsetAsync(c->tcs.Zp, 0, tc_zp_bytes(c, B), c->stream));  // padding rows / j stay zero
       dev_alloc(c, c->tcs.zrow_inv, (size_t)p * Bs);
-      if (!c->tcs.gbar) dev_alloc(c, c->tcs.gbar, tc_gbar_count());
+      if (!c->tcs.gbar) dev_alloc(c, c->tcs.gbar, 2 * tc_gbar_count());  // pass 1 | pass 2
       // the barrier's counters assume a fixed grid: restart them with every new split layout
-      CK(cudaMemsetAsync(c->tcs.gbar, 0, tc_gbar_count() * sizeof(unsigned long long), c->stream));
+      CK(cudaMemsetAsync(c->tcs.gbar, 0, 2 * tc_gbar_count() * sizeof(unsigned long long), c->stream));
       dev_alloc(c, c->tcs.zz_part, tc_zpart_count(c, B));
       dev_alloc(c, c->tcs.zmax_part, tc_zpart_count(c, B));
     }
@@ -320,6 +320,7 @@ int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goal
   launches += timed(c, PC_INIT, [&] { return ro_init(c, theta, x0, goals, B, st); });
   const bool tc = use_tc(c);
   w.S2eff = tc ? w.S2tc * tc_njt(c) : w.S2;
+  const bool fuse_epi = tc && tc_pass2_epi_ok(c, B);
   for (int t = 0; t < T; ++t) {
     float* jm = w.tape_jmu + (size_t)t * B * p * d;
     float* sg = w.tape_sig + (size_t)t * B * p;
@@ -328,12 +329,17 @@ int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goal
       launches += timed(c, PC_REDUCE1, [&] {
         return tc ? tc_reduce1(c, w.xstar, B, jm, sg, st) : gs_reduce1(c, w.xstar, B, jm, sg, st);
       });
-    launches += timed(c, PC_PASS2, [&] { return tc ? tc_pass2(c, w.xstar, B, st) : gs_pass2(c, w.xstar, B, st); });
-    launches += timed(c, PC_EPI, [&] {
-      return ro_step_epilogue(c, theta, goals, B, t, T, seed, traj_offset, t + 1 < T,
-                              trace_mu ? trace_mu + (size_t)t * B * p : nullptr,
-                              trace_var ? trace_var + (size_t)t * B * p : nullptr, st);
-    });
+    float* tmu = trace_mu ? trace_mu + (size_t)t * B * p : nullptr;
+    float* tvar = trace_var ? trace_var + (size_t)t * B * p : nullptr;
+    if (fuse_epi) {
+      const EpiArgs e = ro_epi_args(c, goals, B, t, seed, traj_offset, t + 1 < T, tmu, tvar);
+      launches += timed(c, PC_PASS2, [&] { return tc_pass2(c, w.xstar, B, &e, st); });
+    } else {
+      launches += timed(c, PC_PASS2, [&] { return tc ? tc_pass2(c, w.xstar, B, nullptr, st) : gs_pass2(c, w.xstar, B, st); });
+      launches += timed(c, PC_EPI, [&] {
+        return ro_step_epilogue(c, theta, goals, B, t, T, seed, traj_offset, t + 1 < T, tmu, tvar, st);
+      });
+    }
   }
   CK(cudaGetLastError());
   return launches;
@@ -719,7 +725,7 @@ extern "C" int bagel_gp_predict(bagel_ctx* c, const float* xstar, int M, float* 
     n += tc ? tc_pass1(c, xstar, M, jmu, c->ws.tape_sig, st) : gs_pass1(c, xstar, M, st);
     if (!(tc && c->ws.p1_fused))
       n += tc ? tc_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st) : gs_reduce1(c, xstar, M, jmu, c->ws.tape_sig, st);
-    n += tc ? tc_pass2(c, xstar, M, st) : gs_pass2(c, xstar, M, st);
+    n += tc ? tc_pass2(c, xstar, M, nullptr, st) : gs_pass2(c, xstar, M, st);
     n += gs_finish_predict(c, xstar, M, mean, var, dmean, dvar, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));

@@ -26,6 +26,7 @@
 #include <algorithm>
 
 #include "bagel_internal.h"
+#include "policy_rows.cuh"
 #include "tc.cuh"
 
 namespace tcg {
@@ -828,9 +829,16 @@ struct P2Args {
   float* P2;                // [split * njt + jt][m][B][P2_LD]
   float qscale[BAGEL_MAX_P][BAGEL_MAX_D];
   unsigned long long* dbg;  // nullable: per-CTA %globaltimer event stamps (16 per CTA)
+  // EPI: the step epilogue fused in after a grid barrier (cooperative launch)
+  unsigned long long* gbar;
+  EpiArgs e;
 };
 
-template <int D>
+// EPI (cooperative launch, every CTA resident): after its tiles, each CTA's control warps stage
+// theta^T in the idle stage memory while the epilogue warps finish; after a grid barrier (all
+// pass-2 partials written), warp w of CTA c runs the step epilogue (policy_rows.cuh) of rows
+// c * R + w, ... (R = ceil(B / CTAs)) -- the separate epilogue launch disappears.
+template <int D, bool EPI>
 __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const Geo& g = a.g;
@@ -840,7 +848,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   constexpr size_t slab_bytes = (size_t)4 * NT2 * KS2;  // hi + lo of one slab
   constexpr size_t x_bytes = (size_t)NT2 * AUXW * 4;    // aux rows of one tile
   __shared__ __align__(8) uint64_t zready, full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2],
-      tempty[2];
+      tempty[2], mma_done;
   __shared__ uint32_t tmem_base;
   __shared__ float asum[3][128][1 + D];
 
@@ -873,6 +881,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], 32 * GEN_WARPS);
     }
+    tc::mbar_init(&mma_done, 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(&tmem_base, NCOLS);
@@ -939,6 +948,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
         tc::umma_commit(&tfull[b]);
         if (i == 0) stamp(a.dbg, 2);
       }
+      tc::umma_commit(&mma_done);  // single phase: every MMA of this CTA has completed
       stamp(a.dbg, 3);
     }
   } else {
@@ -1033,10 +1043,35 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       for (int c = 0; c <= D; ++c) o[c] = (((acc[c] + asum[0][r][c]) + asum[1][r][c]) + asum[2][r][c]) * zinv;
     }
   }
+  if (EPI && warp < CTRL_WARPS && a.e.policy_next) {
+    // stage theta^T once every MMA of this CTA has completed (stage memory no longer read)
+    // (a dedicated one-phase barrier: waiting on tfull's parity could alias an earlier phase)
+    tc::mbar_wait(&mma_done, 0);
+    const int n4 = (a.e.P.n_params + 3) / 4;
+    const float4* src = reinterpret_cast<const float4*>(a.e.thetaT);
+    float4* dst = reinterpret_cast<float4*>(sm);
+    for (int i = tid; i < n4; i += 32 * CTRL_WARPS) dst[i] = __ldg(src + i);
+  }
   tc::tc_fence_before();
   __syncthreads();
   if (tid == 0) stamp(a.dbg, 5);
   if (warp == 1) tc::tmem_dealloc(tmem, NCOLS);
+  if (EPI) {
+    grid_barrier(a.gbar);
+    if (tid == 0) stamp(a.dbg, 9);
+    const int G = (int)(gridDim.x * gridDim.y * gridDim.z);
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int R = (a.B + G - 1) / G;
+    const float* th_s = reinterpret_cast<const float*>(sm);
+    float* wbase = reinterpret_cast<float*>(sm) + ((a.e.P.n_params + 3) & ~3) +
+                   (size_t)warp * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<D, 1>());
+    for (int rr = warp; rr < R; rr += THREADS / 32) {
+      const int b = cta * R + rr;
+      if (b >= a.B) break;
+      rows::epi_warp_rows<D, 1>(a.e, b, 1, th_s, wbase, wbase + 2 * BAGEL_MAX_WIDTH);
+    }
+    if (tid == 0) stamp(a.dbg, 10);
+  }
 }
 
 }  // namespace tcg
@@ -1139,7 +1174,8 @@ static void set_attrs() {
     DISPATCH_D(dv, ({
       bagel_set_smem_attr(k_p1_tc<D, false>, 220 * 1024);
       bagel_set_smem_attr(k_p1_tc<D, true>, 220 * 1024);
-      bagel_set_smem_attr(k_p2_tc<D>, 220 * 1024);
+      bagel_set_smem_attr(k_p2_tc<D, false>, 220 * 1024);
+      bagel_set_smem_attr(k_p2_tc<D, true>, 220 * 1024);
     }));
   }
   cudaGetLastError();
@@ -1223,7 +1259,18 @@ int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, fl
   return 2;
 }
 
-int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
+// Can the step epilogue run inside pass 2 (cooperative: one resident wave; theta^T and the
+// per-warp buffers fit the stage memory)?
+bool tc_pass2_epi_ok(const bagel_ctx* c, int B) {
+  const Geo g = geo_of(c);
+  const long long ctas = (long long)cdiv(B, 128) * c->p * g.njt * c->ws.S2tc;
+  const size_t need = sizeof(float) * (((size_t)c->pol.n_params + 3) / 4 * 4 +
+                                       (size_t)(THREADS / 32) * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<8, 1>()));
+  const char* env = getenv("BAGEL_P2_EPI");
+  return ctas <= c->num_sms && ctas <= GB_GROUP * GB_MAXGROUPS && need <= p2_smem(g) && !(env && env[0] == '0');
+}
+
+int tc_pass2(const bagel_ctx* c, const float* xstar, int B, const EpiArgs* epi, cudaStream_t st) {
   set_attrs();
   const Geo g = geo_of(c);
   const TcState& T = c->tcs;
@@ -1242,6 +1289,22 @@ int tc_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
   for (int m = 0; m < c->p; ++m)
     for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
   dim3 grid(cdiv(B, 128), c->p * g.njt, c->ws.S2tc);
-  DISPATCH_D(c->d, (k_p2_tc<D><<<grid, THREADS, p2_smem(g), st>>>(a)));
+  if (epi) {
+    a.e = *epi;
+    a.gbar = T.gbar + tc_gbar_count();  // pass 2's own counters (pass 1 has another grid shape)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.dynamicSmemBytes = p2_smem(g);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    DISPATCH_D(c->d, ((void)cudaLaunchKernelEx(&cfg, k_p2_tc<D, true>, a)));
+  } else {
+    DISPATCH_D(c->d, (k_p2_tc<D, false><<<grid, THREADS, p2_smem(g), st>>>(a)));
+  }
   return 1;
 }

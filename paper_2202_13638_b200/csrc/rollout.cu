@@ -14,12 +14,12 @@
 
 #include "bagel_internal.h"
 #include "philox.cuh"
+#include "policy_rows.cuh"
 #include "tc.cuh"
 
 namespace {
 
 constexpr int EPI_ROWS = 8;
-constexpr int P2_LD = 1 + BAGEL_MAX_D;
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
@@ -27,15 +27,6 @@ __device__ __forceinline__ unsigned long long gtimer_ro() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-__device__ __forceinline__ float reward_fn(const RewardDesc& rw, const float* x, const float* g, int p) {
-  float q = 0.0f;
-  for (int c = 0; c < p; ++c) {
-    const float df = x[c] - g[c];
-    q = fmaf(rw.Q[c] * df, df, q);
-  }
-  return expf(-q * rw.inv_two_sr2);
 }
 
 // thetaT: per layer W_l^T (in x out), biases copied.
@@ -70,95 +61,6 @@ __device__ void stage_theta(const PolicyDesc& P, const float* __restrict__ theta
   __syncthreads();
 }
 
-// rows r < nr of this warp: x[r], g[r] (p each); u_out[r] (q each).  buf: RPW x 2 x BAGEL_MAX_WIDTH.
-// act_out (nullable): every activation of row r, [phi | h_1 | ... | u] (segments at P.aoff,
-// row stride P.act_ld), the reverse pass's tape.
-__device__ void warp_policy(const PolicyDesc& P, int p, const float* th_s, const float* x, const float* g, int nr,
-                            float* buf, float* u_out, float* __restrict__ act_out = nullptr) {
-  const int lane = threadIdx.x % 32;
-  constexpr int W2 = 2 * BAGEL_MAX_WIDTH;
-  for (int r = 0; r < RPW; ++r)
-    for (int i = lane; i < P.sizes[0]; i += 32) {
-      float v = 0.0f;
-      if (r < nr) {
-        const float* xr = x + r * p;
-        const float* gr = g + r * p;
-        if (i < p) v = xr[i];
-        else if (i < 2 * p) v = gr[i - p];
-        else v = gr[i - 2 * p] - xr[i - 2 * p];
-        if (act_out) act_out[(size_t)r * P.act_ld + i] = v;
-      }
-      buf[r * W2 + i] = v;
-    }
-  __syncwarp();
-  int cur = 0;
-  for (int l = 0; l < P.n_layers; ++l) {
-    const int in = P.sizes[l], out = P.sizes[l + 1];
-    const float* Wt = th_s + P.w_off[l];
-    const float* bb = th_s + P.b_off[l];
-    const int nxt = BAGEL_MAX_WIDTH - cur;
-    if (out >= 16) {
-      // lanes over output units; 2 interleaved chains per row
-      for (int o = lane; o < out; o += 32) {
-        float acc[RPW][2];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          acc[r][0] = bb[o];
-          acc[r][1] = 0.0f;
-        }
-        int i = 0;
-        for (; i + 2 <= in; i += 2) {
-          const float w0 = Wt[i * out + o], w1 = Wt[(i + 1) * out + o];
-#pragma unroll
-          for (int r = 0; r < RPW; ++r) {
-            acc[r][0] = fmaf(w0, buf[r * W2 + cur + i], acc[r][0]);
-            acc[r][1] = fmaf(w1, buf[r * W2 + cur + i + 1], acc[r][1]);
-          }
-        }
-        if (i < in) {
-          const float w0 = Wt[i * out + o];
-#pragma unroll
-          for (int r = 0; r < RPW; ++r) acc[r][0] = fmaf(w0, buf[r * W2 + cur + i], acc[r][0]);
-        }
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          const float h = tanhf(acc[r][0] + acc[r][1]);
-          buf[r * W2 + nxt + o] = h;
-          if (act_out && r < nr) act_out[(size_t)r * P.act_ld + P.aoff[l + 1] + o] = h;
-        }
-      }
-    } else {
-      // narrow layer (e.g. the action head): lanes over inputs, butterfly reduction
-      for (int o = 0; o < out; ++o) {
-        float acc[RPW];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) acc[r] = 0.0f;
-        for (int i = lane; i < in; i += 32) {
-          const float wv = Wt[i * out + o];
-#pragma unroll
-          for (int r = 0; r < RPW; ++r) acc[r] = fmaf(wv, buf[r * W2 + cur + i], acc[r]);
-        }
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-#pragma unroll
-          for (int sh = 16; sh > 0; sh >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], sh);
-          if (lane == 0) {
-            const float h = tanhf(acc[r] + bb[o]);
-            buf[r * W2 + nxt + o] = h;
-            if (act_out && r < nr) act_out[(size_t)r * P.act_ld + P.aoff[l + 1] + o] = h;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    cur = nxt;
-  }
-  const int q = P.sizes[P.n_layers];
-  for (int r = 0; r < nr; ++r)
-    for (int o = lane; o < q; o += 32) u_out[r * BAGEL_MAX_D + o] = buf[r * W2 + cur + o];
-  __syncwarp();
-}
-
 size_t policy_smem(const PolicyDesc& P) {
   return sizeof(float) * (((P.n_params + 3) & ~3) + (size_t)WARP_ROWS_BLOCK * RPW * 2 * BAGEL_MAX_WIDTH);
 }
@@ -181,9 +83,9 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_init(PolicyDesc P, Rew
   const int nr = min(RPW, B - b0);
   const float* x = x0 + (size_t)b0 * p;
   const float* g = goals + (size_t)b0 * p;
-  if (lane < nr) G[b0 + lane] = (double)reward_fn(rw, x + lane * p, g + lane * p, p);
+  if (lane < nr) G[b0 + lane] = (double)rows::reward_fn(rw, x + lane * p, g + lane * p, p);
   for (int i = lane; i < nr * p; i += 32) tape_x0[(size_t)b0 * p + i] = x[i];
-  warp_policy(P, p, th_s, x, g, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0],
+  rows::warp_policy<RPW>(P, p, th_s, x, g, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0],
               act0 + (size_t)b0 * P.act_ld);
   for (int i = lane; i < nr * D; i += 32) {
     const int r = i / D, c = i % D;
@@ -192,95 +94,20 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_init(PolicyDesc P, Rew
 }
 
 template <int D>
-__global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(
-    PolicyDesc P, RewardDesc rw, GpDesc g, const float* __restrict__ thetaT, const float* __restrict__ goals,
-    int B, int t, int S2, const float* __restrict__ P2, const float* __restrict__ mu,
-    const float* __restrict__ var, const float* __restrict__ tape_x_t, const float* __restrict__ sig_t,
-    float* __restrict__ jv_t, const float* __restrict__ jmu_t, float* __restrict__ A_t,
-    float* __restrict__ act_next, float* __restrict__ tape_x_next, double* __restrict__ G,
-    float* __restrict__ xstar, uint64_t seed, long long traj_offset, int policy_next,
-    int* __restrict__ err_flag, float* __restrict__ trace_mu, float* __restrict__ trace_var,
-    unsigned long long* __restrict__ dbg) {
+__global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(EpiArgs e, unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(16) float sm[];
   float* th_s = sm;
-  float* bufs = sm + ((P.n_params + 3) & ~3);
-  __shared__ float us[WARP_ROWS_BLOCK][RPW][BAGEL_MAX_D];
-  __shared__ float xn_s[WARP_ROWS_BLOCK][RPW * BAGEL_MAX_P];
+  float* bufs = sm + ((e.P.n_params + 3) & ~3);
+  __shared__ float scratch[WARP_ROWS_BLOCK][rows::epi_scratch_floats<D, RPW>()];
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 0] = gtimer_ro();
-  if (policy_next) stage_theta(P, thetaT, th_s);
+  if (e.policy_next) stage_theta(e.P, e.thetaT, th_s);
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 1] = gtimer_ro();
-  const int p = g.p;
-  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int w = threadIdx.x / 32;
   const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
-  if (b0 >= B) return;  // warp-uniform
-  const int nr = min(RPW, B - b0);
-  // lane = r * p * (D + 1) + m * (D + 1) + c: pass-2 partial of (row r, output m, column c)
-  const int per_row = p * (D + 1);
-  const int nl = nr * per_row;  // <= 2 * 4 * 9 = 72 > 32 possible: loop
-  __shared__ float psum[WARP_ROWS_BLOCK][RPW * BAGEL_MAX_P * (BAGEL_MAX_D + 1)];
-  for (int base = 0; base < RPW * per_row; base += 32) {
-    const int li = base + lane;
-    const bool act = li < nl;
-    const int r = act ? li / per_row : 0, m = act ? (li % per_row) / (D + 1) : 0, c = act ? li % (D + 1) : 0;
-    const int b = b0 + r;
-    // sum of the S2 pass-2 partials in split order, 8 loads in flight
-    float part = 0.0f;
-    if (act) {
-      const float* src = P2 + ((size_t)m * B + b) * P2_LD + c;
-      const size_t sstride = (size_t)p * B * P2_LD;
-      for (int s0 = 0; s0 < S2; s0 += 8) {
-        float v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = s0 + u < S2 ? __ldcg(src + (s0 + u) * sstride) : 0.0f;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) part += v[u];
-      }
-    }
-    psum[w][li < RPW * per_row ? li : 0] = part;
-  }
-  __syncwarp();
-  if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 2] = gtimer_ro();
-  __shared__ float f_s[WARP_ROWS_BLOCK][RPW * BAGEL_MAX_P];
-  if (lane < nr * p) {
-    const int r = lane / p, m = lane % p, b = b0 + r;
-    const float4 e4 = bagel_rollout_eps4(seed, (uint32_t)(traj_offset + b), (uint32_t)t);
-    const float sgr = sig_t[(size_t)b * p + m];
-    const float sg = fabsf(sgr);
-    const float e = bagel_f4get(e4, m & 3);
-    const float mum = mu[(size_t)m * B + b];
-    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * e;
-    if (!isfinite(xn)) atomicMin(err_flag, t * B + b);
-    tape_x_next[(size_t)b * p + m] = xn;
-    xn_s[w][r * p + m] = xn;
-    // d x'/d sigma^2 = eps / (2 sigma) where the variance is not clamped (R19), else 0
-    f_s[w][r * p + m] = sgr > 0.0f ? e / (2.0f * sgr) : 0.0f;
-    if (trace_mu) trace_mu[(size_t)b * p + m] = mum;
-    if (trace_var) trace_var[(size_t)b * p + m] = var[(size_t)m * B + b];
-  }
-  __syncwarp();
-  // J^v from the (r, m) row of sums [sum w k | sum w k X_c]; tape A = J^mu + f J^v (reverse input)
-  for (int li = lane; li < nl; li += 32) {
-    const int r = li / per_row, m = (li % per_row) / (D + 1), c = li % (D + 1);
-    if (c == 0) continue;
-    const int b = b0 + r;
-    const float s0 = psum[w][li - c], part = psum[w][li];
-    const float jv = 2.0f * g.ell2inv[m][c - 1] * (xstar[(size_t)b * D + c - 1] * s0 - part);
-    const size_t o = ((size_t)b * p + m) * D + c - 1;
-    jv_t[o] = jv;
-    A_t[o] = fmaf(f_s[w][r * p + m], jv, jmu_t[o]);
-  }
-  __syncwarp();
-  const float* gb = goals + (size_t)b0 * p;
-  if (lane < nr) G[b0 + lane] += (double)reward_fn(rw, &xn_s[w][lane * p], gb + lane * p, p);
-  if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 3] = gtimer_ro();
-  if (!policy_next) return;
-  warp_policy(P, p, th_s, xn_s[w], gb, nr, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH, &us[w][0][0],
-              act_next + (size_t)b0 * P.act_ld);
+  if (b0 >= e.B) return;  // warp-uniform
+  rows::epi_warp_rows<D, RPW>(e, b0, min(RPW, e.B - b0), th_s, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH,
+                              scratch[w]);
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 4] = gtimer_ro();
-  for (int i = lane; i < nr * D; i += 32) {
-    const int r = i / D, c = i % D;
-    xstar[(size_t)(b0 + r) * D + c] = c < p ? xn_s[w][r * p + c] : us[w][r][c - p];
-  }
 }
 
 // ------------------------------------------------------------------ reverse
@@ -684,20 +511,47 @@ int ro_init(const bagel_ctx* c, const float* theta, const float* x0, const float
   return 2;
 }
 
+EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, uint64_t seed, long long traj_offset,
+                    bool policy_next, float* trace_mu, float* trace_var) {
+  const int p = c->gp.p, d = c->gp.d;
+  const Workspace& w = c->ws;
+  EpiArgs e{};
+  e.P = c->pol;
+  e.rw = c->rw;
+  e.g = c->gp;
+  e.thetaT = w.thetaT;
+  e.goals = goals;
+  e.B = B;
+  e.t = t;
+  e.S2 = w.S2eff;
+  e.P2 = w.P2;
+  e.mu = w.mu;
+  e.var = w.var;
+  e.tape_x_t = w.tape_x + (size_t)t * B * p;
+  e.sig_t = w.tape_sig + (size_t)t * B * p;
+  e.jv_t = w.tape_jv + (size_t)t * B * p * d;
+  e.jmu_t = w.tape_jmu + (size_t)t * B * p * d;
+  e.A_t = w.tape_A + (size_t)t * B * p * d;
+  e.act_next = w.tape_act + (size_t)(t + 1) * B * c->pol.act_ld;
+  e.tape_x_next = w.tape_x + (size_t)(t + 1) * B * p;
+  e.G = w.G;
+  e.xstar = w.xstar;
+  e.seed = seed;
+  e.traj_offset = traj_offset;
+  e.policy_next = policy_next ? 1 : 0;
+  e.err_flag = w.err_flag;
+  e.trace_mu = trace_mu;
+  e.trace_var = trace_var;
+  return e;
+}
+
 int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, int T,
                      uint64_t seed, long long traj_offset, bool policy_next, float* trace_mu,
                      float* trace_var, cudaStream_t st) {
-  (void)T;
-  const int p = c->gp.p, d = c->gp.d;
-  const Workspace& w = c->ws;
-  DISPATCH_D(d, (k_epilogue<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
-                    c->pol, c->rw, c->gp, w.thetaT, goals, B, t, w.S2eff, w.P2, w.mu, w.var,
-                    w.tape_x + (size_t)t * B * p, w.tape_sig + (size_t)t * B * p,
-                    w.tape_jv + (size_t)t * B * p * d, w.tape_jmu + (size_t)t * B * p * d,
-                    w.tape_A + (size_t)t * B * p * d, w.tape_act + (size_t)(t + 1) * B * c->pol.act_ld,
-                    w.tape_x + (size_t)(t + 1) * B * p, w.G, w.xstar,
-                    seed, traj_offset, policy_next ? 1 : 0, w.err_flag, trace_mu, trace_var,
-                    t == T - 2 ? c->tcs.dbg3 : nullptr)));
+  (void)theta;
+  const EpiArgs e = ro_epi_args(c, goals, B, t, seed, traj_offset, policy_next, trace_mu, trace_var);
+  DISPATCH_D(c->gp.d, (k_epilogue<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
+                          e, t == T - 2 ? c->tcs.dbg3 : nullptr)));
   return 1;
 }
 
