@@ -73,6 +73,11 @@ inline Geo make_geo(int N, int d, int p, int k) {
   return g;
 }
 
+// Per-training-point side data ("aux") of a stage tile, pair-interleaved: points 2j and 2j + 1
+// share a block of 2 x AUXW floats, field-major, point-minor -- so one float4 holds two fields
+// of both points, i.e. the two lanes of two fp32x2 operands.
+__host__ __device__ inline int aux_idx(int nn, int f) { return ((nn >> 1) * AUXW + f) * 2 + (nn & 1); }
+
 __device__ __forceinline__ void split_f16(float v, __half& hi, __half& lo) {
   hi = __float2half_rn(v);
   lo = __float2half_rn(v - __half2float(hi));
@@ -123,7 +128,7 @@ __global__ void k_pack1(Geo g, const float* __restrict__ X, const double* __rest
     } else if (f < g.d) {
       v = 1e18f;  // padded training point: infinitely far, ktilde = 0
     }
-    aux[idx] = v;
+    aux[aux_idx(nn, f)] = v;
   }
 }
 
@@ -198,7 +203,7 @@ __global__ void k_pack2(Geo g, const float* __restrict__ X, const double* __rest
     } else if (f < g.d) {
       v = 1e18f;
     }
-    aux[idx] = v;
+    aux[aux_idx(nn, f)] = v;
   }
 }
 
@@ -226,6 +231,7 @@ struct P1Args {
   float* jmu;                // nullable
   float* sig;                // nullable
   unsigned long long* gbar;  // grid barrier counter
+  int diag;                  // timing experiments only (results invalid): 1 skip generator math, 2 skip MMAs
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -240,36 +246,56 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int k) {
   }
 }
 
-// Grid-wide barrier for a cooperative launch (every CTA resident).  Two levels so that at most
-// GB_GROUP atomics serialise on one address (L2 atomics serialise per address): CTA i arrives on
-// group counter i / GB_GROUP; the group's last arriver arrives on the top counter.  Counters only
-// grow (each launch adds one round; they are zeroed when the grid shape changes) and live on
-// separate 256-byte lines.
-constexpr int GB_GROUP = 12;
-constexpr int GB_STRIDE = 32;   // unsigned long longs between counters
-constexpr int GB_MAXGROUPS = 64;
+// Grid-wide barrier for a cooperative launch (every CTA resident): one release-add per CTA on a
+// counter that only grows (each launch adds G; it is zeroed whenever the grid shape changes),
+// then an acquire-poll until the count reaches the next multiple of G.  The release (cumulative
+// over the CTA's writes ordered before it by bar.sync) and the acquire make every CTA's writes
+// before the barrier visible to every CTA after it.
+constexpr int GB_STRIDE = 32;   // unsigned long longs reserved per counter set
 __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int G = (int)(gridDim.x * gridDim.y * gridDim.z);
-    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int grp = cta / GB_GROUP, ngroups = (G + GB_GROUP - 1) / GB_GROUP;
-    const unsigned long long gs = (unsigned long long)min(GB_GROUP, G - grp * GB_GROUP);
-    __threadfence();
-    const unsigned long long old = atomicAdd(ctr + GB_STRIDE * (1 + grp), 1ull);
-    const unsigned long long round = old / gs;
-    if (old % gs == gs - 1) {
-      __threadfence();
-      atomicAdd(ctr, 1ull);
-    }
-    const unsigned long long target = (round + 1) * (unsigned long long)ngroups;
+    const unsigned long long G = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    unsigned long long old;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+    const unsigned long long target = (old / G + 1) * G;
     unsigned long long cur;
     do {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(ctr) : "memory");
     } while (cur < target);
-    __threadfence();
   }
   __syncthreads();
+}
+
+// Packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2 on sm_100a): two independent lanes, each
+// rounded exactly as the scalar instruction would.
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -278,16 +304,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// aux row of one training point as registers (float4 loads; rows are 16-byte aligned)
+// fields 0 .. NV-1 of training points 2j, 2j + 1 (pair block at `pair`) as float2 lanes
 template <int NV>
-__device__ __forceinline__ void load_aux(const float* row, float* out) {
+__device__ __forceinline__ void load_aux2(const float* pair, float2* out) {
 #pragma unroll
-  for (int v = 0; v < (NV + 3) / 4; ++v) {
-    const float4 f = *reinterpret_cast<const float4*>(row + 4 * v);
-    out[4 * v] = f.x;
-    if (4 * v + 1 < NV) out[4 * v + 1] = f.y;
-    if (4 * v + 2 < NV) out[4 * v + 2] = f.z;
-    if (4 * v + 3 < NV) out[4 * v + 3] = f.w;
+  for (int v = 0; v < (NV + 1) / 2; ++v) {
+    const float4 f = *reinterpret_cast<const float4*>(pair + 4 * v);
+    out[2 * v] = make_float2(f.x, f.y);
+    if (2 * v + 1 < NV) out[2 * v + 1] = make_float2(f.z, f.w);
   }
 }
 
@@ -334,13 +358,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
 
   uint32_t ncols = 32;
   while ((int)ncols < NZ) ncols <<= 1;
+  // clusters of csize CTAs along the row tiles share (m, split) and hence every B tile: each CTA
+  // loads 1/csize of a tile multicast to all, and a stage is refilled once every CTA's MMAs
+  // released it (empty_b counts csize arrivals)
+  const uint32_t csize = tc::cluster_size(), crank = tc::cluster_rank();
+  const uint16_t cmask = (uint16_t)((1u << csize) - 1u);
   if (tid == 0) stamp(a.dbg, 0);
   if (tid == 0) {
     for (int s = 0; s < ST1; ++s) {
       tc::mbar_init(&full_a[s], 32 * GEN_WARPS);
       tc::mbar_init(&empty_a[s], 1);
       tc::mbar_init(&full_b[s], 1);
-      tc::mbar_init(&empty_b[s], 1);
+      tc::mbar_init(&empty_b[s], csize);
     }
     for (int s = 0; s < STA; ++s) {
       tc::mbar_init(&full_x[s], 1);
@@ -352,18 +381,23 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   if (warp == 1) tc::tmem_alloc(&tmem_base, ncols);
   tc::tc_fence_before();
   __syncthreads();
+  if (csize > 1) tc::cluster_sync();  // the partners' barriers exist before any multicast lands
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
     // ------------------------------------------------ B-tile producer (one elected lane)
     if (lane == 0) {
+      const uint32_t slice = (uint32_t)b_bytes / csize;
       for (int i = 0; i < ntile; ++i) {
         const int s = i % ST1;
         tc::mbar_wait(&empty_b[s], ((uint32_t)(i / ST1) & 1u) ^ 1u);
         tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)b_bytes);
-        tc::bulk_g2s(bsm + (size_t)s * b_bytes, tiles + (size_t)(t_begin + i) * g.t1_bytes, (uint32_t)b_bytes,
-                     &full_b[s]);
+        const uint8_t* src = tiles + (size_t)(t_begin + i) * g.t1_bytes;
+        if (csize == 1)
+          tc::bulk_g2s(bsm + (size_t)s * b_bytes, src, (uint32_t)b_bytes, &full_b[s]);
+        else
+          tc::bulk_g2s_mc(bsm + (size_t)s * b_bytes + crank * slice, src + crank * slice, slice, &full_b[s], cmask);
       }
     }
   } else if (warp == 2) {
@@ -394,16 +428,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
         const uint64_t dalo = tc::umma_desc(abase + (uint32_t)a_bytes, 128, SBO);
         const uint64_t dbhi = tc::umma_desc(bbase, 128, SBO);
         const uint64_t dblo = tc::umma_desc(bbase + (uint32_t)NZ * KT1 * 2u, 128, SBO);
+        if (!(a.diag & 2)) {
 #pragma unroll
-        for (int ks = 0; ks < KT1 / 16; ++ks) {
-          const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
-          const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
-          tc::mma_f16(tmem, dahi + o, dbhi + o, idesc, acc0);
-          tc::mma_f16(tmem, dahi + o, dblo + o, idesc, 1u);
-          tc::mma_f16(tmem, dalo + o, dbhi + o, idesc, 1u);
+          for (int ks = 0; ks < KT1 / 16; ++ks) {
+            const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
+            const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
+            tc::mma_f16(tmem, dahi + o, dbhi + o, idesc, acc0);
+            tc::mma_f16(tmem, dahi + o, dblo + o, idesc, 1u);
+            tc::mma_f16(tmem, dalo + o, dbhi + o, idesc, 1u);
+          }
         }
         tc::umma_commit(&empty_a[s]);
-        tc::umma_commit(&empty_b[s]);
+        if (csize == 1) tc::umma_commit(&empty_b[s]);
+        else tc::umma_commit_mc(&empty_b[s], cmask);
         if (i == 0) stamp(a.dbg, 1);
       }
       tc::umma_commit(&done);
@@ -422,9 +459,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
       xq[c] = row < a.B ? a.xstar[(size_t)row * D + c] : 0.0f;
       sc[c] = a.qscale[m][c];
     }
-    float hacc[1 + D];
+    // mean columns, two partial sums per column (even / odd training points: one FFMA2 lane each)
+    float2 hacc2[1 + D];
 #pragma unroll
-    for (int c = 0; c <= D; ++c) hacc[c] = 0.0f;
+    for (int c = 0; c <= D; ++c) hacc2[c] = make_float2(0.0f, 0.0f);
     for (int i = 0; i < ntile; ++i) {
       const int s = i % ST1, x = i % STA;
       tc::mbar_wait(&full_x[x], (uint32_t)(i / STA) & 1u);             // aux rows of tile i landed
@@ -433,28 +471,25 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
       __half* alo = ahi + 128 * KT1;
       const float* aux = reinterpret_cast<const float*>(xsm + (size_t)x * x_bytes);
       uint32_t hw[4], lw[4];
+      if (!(a.diag & 1))
 #pragma unroll
       for (int e = 0; e < 8; e += 2) {
-        float kv[2];
+        // training points e and e + 1 of this thread's 8 as the two lanes of fp32x2 operations
+        float2 an[NAUX];
+        load_aux2<NAUX>(aux + ((qd * 8 + e) >> 1) * (2 * AUXW), an);
+        float2 q = make_float2(0.0f, 0.0f);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          float an[NAUX];
-          load_aux<NAUX>(aux + (qd * 8 + e + u) * AUXW, an);
-          float q = 0.0f;
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            const float df = (xq[c] - an[c]) * sc[c];
-            q = fmaf(df, df, q);
-          }
-          const float kt = ex2_approx(-q);
-          kv[u] = kt;
-          hacc[0] = fmaf(kt, an[D], hacc[0]);
-#pragma unroll
-          for (int c = 0; c < D; ++c) hacc[1 + c] = fmaf(kt, an[D + 1 + c], hacc[1 + c]);
+        for (int c = 0; c < D; ++c) {
+          const float2 df = mul2(sub2(make_float2(xq[c], xq[c]), an[c]), make_float2(sc[c], sc[c]));
+          q = fma2(df, df, q);
         }
-        const __half2 h2 = __floats2half2_rn(kv[0], kv[1]);
-        const float2 hf = __half22float2(h2);
-        const __half2 l2 = __floats2half2_rn(kv[0] - hf.x, kv[1] - hf.y);
+        const float2 kt = make_float2(ex2_approx(-q.x), ex2_approx(-q.y));
+        hacc2[0] = fma2(kt, an[D], hacc2[0]);
+#pragma unroll
+        for (int c = 0; c < D; ++c) hacc2[1 + c] = fma2(kt, an[D + 1 + c], hacc2[1 + c]);
+        const __half2 h2 = __floats2half2_rn(kt.x, kt.y);
+        const float2 res = sub2(kt, __half22float2(h2));
+        const __half2 l2 = __floats2half2_rn(res.x, res.y);
         hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
       }
@@ -463,11 +498,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
       *reinterpret_cast<uint4*>(alo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       // MEMBAR.CTA + proxy fence: the A stores are visible to the MMA, and every aux load above
       // has returned before the aux stage is released (SYNCS.ARRIVE does not wait for pending LDS)
-      tc::fence_proxy_async();
+      if (!(a.diag & 4)) tc::fence_proxy_async();
       tc::mbar_arrive(&full_a[s]);
       tc::mbar_arrive(&empty_x[x]);
     }
     if (gt == 0) stamp(a.dbg, 3);
+    float hacc[1 + D];
+#pragma unroll
+    for (int c = 0; c <= D; ++c) hacc[c] = hacc2[c].x + hacc2[c].y;
     // ---- mean columns: combine the four quarters of each row (fixed order)
     if (qd > 0)
       for (int c = 0; c <= D; ++c) hsum[qd - 1][r][c] = hacc[c];
@@ -517,6 +555,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   __syncthreads();
   if (tid == 0) stamp(a.dbg, 5);
   if (warp == 1) tc::tmem_dealloc(tmem, ncols);
+  if (csize > 1) tc::cluster_sync();  // no CTA leaves while multicasts / remote arrivals may target it
   if (FUSED) {
     const int LDZ = NZ + 4;
     const int rtn = cdiv_dev(a.B, 128);
@@ -996,9 +1035,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       sc[c] = a.qscale[m][c];
     }
     const float zinv = row < a.B ? a.zrow_inv[(size_t)m * a.B + row] : 0.0f;
-    float acc[1 + D];
+    float2 acc2[1 + D];  // even / odd columns
 #pragma unroll
-    for (int c = 0; c <= D; ++c) acc[c] = 0.0f;
+    for (int c = 0; c <= D; ++c) acc2[c] = make_float2(0.0f, 0.0f);
     for (int i = 0; i < ntile; ++i) {
       const int b = i & 1, x = i % STX2;
       tc::mbar_wait(&tfull[b], (uint32_t)(i / 2) & 1u);
@@ -1016,24 +1055,28 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       tc::mbar_wait(&full_x[x], (uint32_t)(i / STX2) & 1u);
       const float* aux = reinterpret_cast<const float*>(xsm + (size_t)x * x_bytes);
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        float an[NAUX];
-        load_aux<NAUX>(aux + (cg * 32 + u) * AUXW, an);
-        float q = 0.0f;
+      for (int u = 0; u < 32; u += 2) {
+        // columns u, u + 1 as the two lanes of fp32x2 operations
+        float2 an[NAUX];
+        load_aux2<NAUX>(aux + ((cg * 32 + u) >> 1) * (2 * AUXW), an);
+        float2 q = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const float df = (xq[c] - an[c]) * sc[c];
-          q = fmaf(df, df, q);
+          const float2 df = mul2(sub2(make_float2(xq[c], xq[c]), an[c]), make_float2(sc[c], sc[c]));
+          q = fma2(df, df, q);
         }
-        const float t = w[u] * an[D] * ex2_approx(-q);
-        acc[0] += t;
+        const float2 t = mul2(mul2(make_float2(w[u], w[u + 1]), an[D]), make_float2(ex2_approx(-q.x), ex2_approx(-q.y)));
+        acc2[0] = add2(acc2[0], t);
 #pragma unroll
-        for (int c = 0; c < D; ++c) acc[1 + c] = fmaf(t, an[c], acc[1 + c]);
+        for (int c = 0; c < D; ++c) acc2[1 + c] = fma2(t, an[c], acc2[1 + c]);
       }
       __threadfence_block();  // every aux load above has returned before the stage is released
       tc::mbar_arrive(&empty_x[x]);
     }
     if (tid == 32 * CTRL_WARPS) stamp(a.dbg, 4);
+    float acc[1 + D];
+#pragma unroll
+    for (int c = 0; c <= D; ++c) acc[c] = acc2[c].x + acc2[c].y;
     // combine the four column groups of each row (fixed order), undo the Z row scale
     if (cg > 0)
       for (int c = 0; c <= D; ++c) asum[cg - 1][r][c] = acc[c];
@@ -1146,8 +1189,7 @@ void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, in
   *tps1 = cdiv(g.nt1, s1);
   *S1 = cdiv(g.nt1, *tps1);
   const char* env = getenv("BAGEL_P1_FUSED");
-  *p1_fused = g.nct == 1 && rt * g.p * *S1 <= target && rt * g.p * *S1 <= GB_GROUP * GB_MAXGROUPS &&
-              !(env && env[0] == '0');
+  *p1_fused = g.nct == 1 && rt * g.p * *S1 <= target && !(env && env[0] == '0');
   int s2 = target / (rt * g.p * g.njt);
   s2 = s2 < 1 ? 1 : (s2 > g.nt2 ? g.nt2 : s2);
   *tps2 = cdiv(g.nt2, s2);
@@ -1164,7 +1206,7 @@ size_t tc_zp_bytes(const bagel_ctx* c, int B) {
 }
 int tc_njt(const bagel_ctx* c) { return geo_of(c).njt; }
 size_t tc_zpart_count(const bagel_ctx* c, int B) { return (size_t)c->p * cdiv(c->k, R1_JG) * B; }
-size_t tc_gbar_count() { return (size_t)GB_STRIDE * (1 + GB_MAXGROUPS); }
+size_t tc_gbar_count() { return (size_t)GB_STRIDE; }
 
 static void set_attrs() {
   static bool done = false;
@@ -1181,6 +1223,15 @@ static void set_attrs() {
   cudaGetLastError();
 }
 
+// Cluster size along the row tiles (TMA multicast of the shared B operand tiles): 2 when the
+// row-tile count is even (BAGEL_TC_CLUSTER=1 disables).
+int tc_cluster_x(const bagel_ctx* c, int B) {
+  (void)c;
+  const char* env = getenv("BAGEL_TC_CLUSTER");
+  if (env && env[0] == '1') return 1;
+  return cdiv(B, 128) % 2 == 0 ? 2 : 1;
+}
+
 int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st) {
   set_attrs();
   const Geo g = geo_of(c);
@@ -1193,6 +1244,10 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, floa
   a.tiles = T.tiles1;
   a.m_stride = T.t1_stride;
   a.tiles_per_split = c->ws.tps1;
+  {
+    const char* dg = getenv("BAGEL_P1_DIAG");
+    a.diag = dg ? atoi(dg) : 0;
+  }
   a.P1z = T.P1z;
   a.P1h = T.P1h;
   a.dbg = T.dbg1;
@@ -1213,20 +1268,34 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, floa
     a.sig = sig_out;
     a.P1h = T.P1h;
     a.gbar = T.gbar;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(THREADS, 1, 1);
-    cfg.dynamicSmemBytes = p1_smem(g);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    // a launch error is recorded as the last CUDA error (checked by the caller)
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS, 1, 1);
+  cfg.dynamicSmemBytes = p1_smem(g);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  const int cl = tc_cluster_x(c, B);
+  if (cl > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = (unsigned)cl;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (c->ws.p1_fused) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  // a launch error is recorded as the last CUDA error (checked by the caller)
+  if (c->ws.p1_fused) {
     DISPATCH_D(c->d, ((void)cudaLaunchKernelEx(&cfg, k_p1_tc<D, true>, a)));
   } else {
-    DISPATCH_D(c->d, (k_p1_tc<D, false><<<grid, THREADS, p1_smem(g), st>>>(a)));
+    DISPATCH_D(c->d, ((void)cudaLaunchKernelEx(&cfg, k_p1_tc<D, false>, a)));
   }
   return 1;
 }
@@ -1267,7 +1336,7 @@ bool tc_pass2_epi_ok(const bagel_ctx* c, int B) {
   const size_t need = sizeof(float) * (((size_t)c->pol.n_params + 3) / 4 * 4 +
                                        (size_t)(THREADS / 32) * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<8, 1>()));
   const char* env = getenv("BAGEL_P2_EPI");
-  return ctas <= c->num_sms && ctas <= GB_GROUP * GB_MAXGROUPS && need <= p2_smem(g) && !(env && env[0] == '0');
+  return ctas <= c->num_sms && need <= p2_smem(g) && !(env && env[0] == '0');
 }
 
 int tc_pass2(const bagel_ctx* c, const float* xstar, int B, const EpiArgs* epi, cudaStream_t st) {
