@@ -329,15 +329,13 @@ int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goal
       launches += timed(c, PC_REDUCE1, [&] {
         return tc ? tc_reduce1(c, w.xstar, B, jm, sg, st) : gs_reduce1(c, w.xstar, B, jm, sg, st);
       });
-    float* tmu = trace_mu ? trace_mu + (size_t)t * B * p : nullptr;
-    float* tvar = trace_var ? trace_var + (size_t)t * B * p : nullptr;
     if (fuse_epi) {
-      const EpiArgs e = ro_epi_args(c, goals, B, t, seed, traj_offset, t + 1 < T, tmu, tvar);
+      const EpiArgs e = ro_epi_args(c, goals, B, t, T, seed, traj_offset, trace_mu, trace_var);
       launches += timed(c, PC_PASS2, [&] { return tc_pass2(c, w.xstar, B, &e, st); });
     } else {
       launches += timed(c, PC_PASS2, [&] { return tc ? tc_pass2(c, w.xstar, B, nullptr, st) : gs_pass2(c, w.xstar, B, st); });
       launches += timed(c, PC_EPI, [&] {
-        return ro_step_epilogue(c, theta, goals, B, t, T, seed, traj_offset, t + 1 < T, tmu, tvar, st);
+        return ro_step_epilogue(c, theta, goals, B, t, T, seed, traj_offset, trace_mu, trace_var, st);
       });
     }
   }

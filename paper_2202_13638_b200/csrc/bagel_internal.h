@@ -49,33 +49,32 @@ struct GpDesc {
   float s[BAGEL_MAX_P];
 };
 
-// Arguments of the step epilogue (policy_rows.cuh epi_warp_rows) for step t: pass-2 partial
-// sums -> J^v, eps, x' = x + mu + sigma eps, G += r, tapes (x, J^v, A, activations), next action.
+// Arguments of the step epilogue (policy_rows.cuh epi_warp_rows) for step t of T: pass-2
+// partial sums -> J^v, eps, x' = x + mu + sigma eps, G += r, tapes (x, J^v, A, activations),
+// next action.  Tape pointers are the bases of the whole rollout; step t's rows are derived.
 struct EpiArgs {
   PolicyDesc P;
   RewardDesc rw;
   GpDesc g;
   const float* thetaT;
   const float* goals;
-  int B, t, S2;
+  int B, t, T, S2;
   const float* P2;       // S2 x p x B x (1 + MAX_D)
   const float* mu;       // p x B
   const float* var;      // p x B
-  const float* tape_x_t; // B x p
-  const float* sig_t;    // B x p (negative: clamped)
-  float* jv_t;           // B x p x d
-  const float* jmu_t;    // B x p x d
-  float* A_t;            // B x p x d
-  float* act_next;       // B x act_ld (tape row t + 1)
-  float* tape_x_next;    // B x p
+  float* tape_x;         // (T + 1) x B x p
+  const float* tape_sig; // T x B x p (negative: clamped)
+  float* tape_jv;        // T x B x p x d
+  const float* tape_jmu; // T x B x p x d
+  float* tape_A;         // T x B x p x d
+  float* tape_act;       // T x B x act_ld
   double* G;             // B
   float* xstar;          // B x d (read: this step's query; written: the next one)
   uint64_t seed;
   long long traj_offset;
-  int policy_next;
   int* err_flag;
-  float* trace_mu;       // nullable
-  float* trace_var;      // nullable
+  float* trace_mu;       // nullable, T x B x p
+  float* trace_var;      // nullable, T x B x p
 };
 
 // Tensor-core (tcgen05) path state: packed operand tiles (cache-build time) and
@@ -226,11 +225,10 @@ void gs_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2);
 // rollout.cu
 int ro_init(const bagel_ctx* c, const float* theta, const float* x0, const float* goals, int B,
             cudaStream_t st);
-EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, uint64_t seed, long long traj_offset,
-                    bool policy_next, float* trace_mu, float* trace_var);
-int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals, int B, int t,
-                     int T, uint64_t seed, long long traj_offset, bool policy_next,
-                     float* trace_mu, float* trace_var, cudaStream_t st);
+EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, int T, uint64_t seed, long long traj_offset,
+                    float* trace_mu, float* trace_var);
+int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, int T,
+                     uint64_t seed, long long traj_offset, float* trace_mu, float* trace_var, cudaStream_t st);
 int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B, int T,
                uint64_t seed, long long traj_offset, long long B_global, int* nblk_out,
                cudaStream_t st);

@@ -298,6 +298,12 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   return d;
 }
 
+// Programmatic dependent launch: let the next kernel of the stream be scheduled now (its CTAs
+// land as SMs free up), and wait for the previous kernel's completion and memory flush before
+// touching anything it wrote.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -330,9 +336,19 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 // finishes them as reduce 1 does (v, sigma, J^mu, row scale, packed Z): the two reduce launches
 // (and their column-strided passes over the partials) disappear.  (A DSMEM cluster reduction was
 // measured first: cluster residency caps S1 at 6 here and DSMEM moves ~20 B/clk/SM -- slower.)
+template <int D>
+struct P1Shared {
+  uint64_t full_a[ST1], empty_a[ST1], full_b[ST1], empty_b[ST1], full_x[STA], empty_x[STA], done;
+  float hsum[3][128][1 + D];
+};
+
+// Pass 1 of the CTA with grid coordinates (bx, by, bz): the N-split partial z tile of 128 rows
+// (TMEM accumulator at column `tmem`) and the mean columns.  FUSED: the partial tile is parked
+// in shared memory and the rows this CTA does not finish are written to P1z (p1_reduce runs
+// after a grid barrier).  Ends with every thread past a __syncthreads and the barriers retired.
 template <int D, bool FUSED>
-__global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
-  extern __shared__ __align__(1024) uint8_t sm[];
+__device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int by, const int bz, const int nbz,
+                                        uint8_t* sm, P1Shared<D>& sh, const uint32_t tmem) {
   const Geo& g = a.g;
   const int NZ = g.NZ;
   constexpr int NAUX = 2 * D + 1;
@@ -342,22 +358,24 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   uint8_t* asm_ = sm;                            // ST1 x (A hi | A lo)
   uint8_t* bsm = asm_ + ST1 * 2 * a_bytes;       // ST1 x (B hi | B lo)
   uint8_t* xsm = bsm + ST1 * b_bytes;            // STA x aux
-  __shared__ __align__(8) uint64_t full_a[ST1], empty_a[ST1], full_b[ST1], empty_b[ST1], full_x[STA], empty_x[STA],
-      done;
-  __shared__ uint32_t tmem_base;
-  __shared__ float hsum[3][128][1 + D];
+  uint64_t* full_a = sh.full_a;
+  uint64_t* empty_a = sh.empty_a;
+  uint64_t* full_b = sh.full_b;
+  uint64_t* empty_b = sh.empty_b;
+  uint64_t* full_x = sh.full_x;
+  uint64_t* empty_x = sh.empty_x;
+  uint64_t& done = sh.done;
+  float (*hsum)[128][1 + D] = sh.hsum;
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const int row0 = blockIdx.x * 128;
-  const int m = blockIdx.y / g.nct, ct = blockIdx.y % g.nct;
-  const int split = blockIdx.z;
+  const int row0 = bx * 128;
+  const int m = by / g.nct, ct = by % g.nct;
+  const int split = bz;
   const int t_begin = split * a.tiles_per_split;
   const int t_end = min(g.nt1, t_begin + a.tiles_per_split);
   const int ntile = max(0, t_end - t_begin);
   const uint8_t* tiles = a.tiles + (size_t)m * a.m_stride + ((size_t)ct * g.nt1) * g.t1_bytes;
 
-  uint32_t ncols = 32;
-  while ((int)ncols < NZ) ncols <<= 1;
   // clusters of csize CTAs along the row tiles share (m, split) and hence every B tile: each CTA
   // loads 1/csize of a tile multicast to all, and a stage is refilled once every CTA's MMAs
   // released it (empty_b counts csize arrivals)
@@ -378,12 +396,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
     tc::mbar_init(&done, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, ncols);
-  tc::tc_fence_before();
   __syncthreads();
   if (csize > 1) tc::cluster_sync();  // the partners' barriers exist before any multicast lands
   tc::tc_fence_after();
-  const uint32_t tmem = tmem_base;
+  pdl_launch_dependents();
+  // the operand tiles are static (cache build): the producers start now; everything that reads
+  // the previous kernel's outputs (x*) or writes this step's outputs waits for it first
+  if (warp >= CTRL_WARPS) pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------ B-tile producer (one elected lane)
@@ -551,30 +570,58 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
       }
     }
   }
+  if (warp < CTRL_WARPS) pdl_wait();
   tc::tc_fence_before();
   __syncthreads();
-  if (tid == 0) stamp(a.dbg, 5);
-  if (warp == 1) tc::tmem_dealloc(tmem, ncols);
+  if (tid == 0) {
+    stamp(a.dbg, 5);
+    for (int s = 0; s < ST1; ++s) {
+      tc::mbar_inval(&full_a[s]);
+      tc::mbar_inval(&empty_a[s]);
+      tc::mbar_inval(&full_b[s]);
+      tc::mbar_inval(&empty_b[s]);
+    }
+    for (int s = 0; s < STA; ++s) {
+      tc::mbar_inval(&full_x[s]);
+      tc::mbar_inval(&empty_x[s]);
+    }
+    tc::mbar_inval(&done);
+  }
   if (csize > 1) tc::cluster_sync();  // no CTA leaves while multicasts / remote arrivals may target it
   if (FUSED) {
     const int LDZ = NZ + 4;
     const int rtn = cdiv_dev(a.B, 128);
-    const int S = (int)gridDim.z;
+    const int S = nbz;
     const float* zs = reinterpret_cast<const float*>(sm);
     // CTA (row tile, m, split) finishes rows rr = split, split + S, ... of its tile; the partials
     // of all other rows go to P1z row-major [split][m][row tile][128][NZ] (one warp per row:
     // 512-byte contiguous segments)
-    {
-      float* dst = a.P1z + ((size_t)(split * a.m_count + m) * rtn + blockIdx.x) * 128 * NZ;
-      for (int rr = warp; rr < 128 && row0 + rr < a.B; rr += THREADS / 32)
-        if (rr % S != split)
-          for (int c4 = lane; c4 * 4 < NZ; c4 += 32)
-            *reinterpret_cast<float4*>(dst + (size_t)rr * NZ + c4 * 4) =
-                *reinterpret_cast<const float4*>(zs + rr * LDZ + c4 * 4);
-    }
+    float* dst = a.P1z + ((size_t)(split * a.m_count + m) * rtn + bx) * 128 * NZ;
+    for (int rr = warp; rr < 128 && row0 + rr < a.B; rr += THREADS / 32)
+      if (rr % S != split)
+        for (int c4 = lane; c4 * 4 < NZ; c4 += 32)
+          *reinterpret_cast<float4*>(dst + (size_t)rr * NZ + c4 * 4) =
+              *reinterpret_cast<const float4*>(zs + rr * LDZ + c4 * 4);
     if (tid == 0) stamp(a.dbg, 8);
-    grid_barrier(a.gbar);
-    if (tid == 0) stamp(a.dbg, 6);
+  }
+}
+
+// Reduce 1 fused into pass 1 (after the grid barrier that follows p1_main<D, true> of every
+// CTA): CTA (bx, by, bz) finishes rows bz, bz + S, ... of row tile bx, output m = by: sums the S
+// partials in split order, then v = s - ||z||^2, sigma, J^mu, the row scale and the packed Z.
+// jmu / sig: this step's rows of the tapes (nullable).
+template <int D>
+__device__ __forceinline__ void p1_reduce(const P1Args& a, const int bx, const int by, const int bz, const int S,
+                                          const uint8_t* sm, float* jmu, float* sig) {
+  const Geo& g = a.g;
+  const int NZ = g.NZ;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int row0 = bx * 128;
+  const int m = by, split = bz;
+  const int LDZ = NZ + 4;
+  const int rtn = cdiv_dev(a.B, 128);
+  const float* zs = reinterpret_cast<const float*>(sm);
+  {
     const bool act = lane * 8 < NZ;
     const size_t sstride = (size_t)a.m_count * rtn * 128 * NZ;  // floats per split
     for (int rr = split + S * warp; rr < 128 && row0 + rr < a.B; rr += S * (THREADS / 32)) {
@@ -645,10 +692,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
         a.zrow_inv[(size_t)mm * a.B + row] = inv;
         a.mu[(size_t)mm * a.B + row] = h0;
         a.var[(size_t)mm * a.B + row] = v;
-        if (a.sig) a.sig[(size_t)row * g.p + mm] = v > BAGEL_VAR_FLOOR ? sg : -sg;
+        if (sig) sig[(size_t)row * g.p + mm] = v > BAGEL_VAR_FLOOR ? sg : -sg;
       }
-      if (a.jmu && lane >= 1 && lane <= D)
-        a.jmu[((size_t)row * g.p + mm) * D + lane - 1] =
+      if (jmu && lane >= 1 && lane <= D)
+        jmu[((size_t)row * g.p + mm) * D + lane - 1] =
             (hv - a.xstar[(size_t)row * D + lane - 1] * h0) * a.ell2inv[mm][lane - 1];
       if (act) {
         // packed pass-2 A operand (see k_r1b_tc): hi group `lane`, lo group KJ/8 + lane
@@ -671,6 +718,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
     if (tid == 0) stamp(a.dbg, 7);
   }
 }
+
+template <int D, bool FUSED>
+__global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ P1Shared<D> sh;
+  __shared__ uint32_t tmem_base;
+  uint32_t ncols = 32;
+  while ((int)ncols < a.g.NZ) ncols <<= 1;
+  if (threadIdx.x / 32 == 1) tc::tmem_alloc(&tmem_base, ncols);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  p1_main<D, FUSED>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, sm, sh, tmem_base);
+  if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, ncols);
+  if (FUSED) {
+    grid_barrier(a.gbar);
+    if (threadIdx.x == 0) stamp(a.dbg, 6);
+    p1_reduce<D>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, sm, a.jmu, a.sig);
+  }
+}
+
 
 // ====================================================================== reduce 1
 struct R1Args {
@@ -877,24 +945,38 @@ struct P2Args {
 // theta^T in the idle stage memory while the epilogue warps finish; after a grid barrier (all
 // pass-2 partials written), warp w of CTA c runs the step epilogue (policy_rows.cuh) of rows
 // c * R + w, ... (R = ceil(B / CTAs)) -- the separate epilogue launch disappears.
+template <int D>
+struct P2Shared {
+  uint64_t zready, full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2], tempty[2], mma_done;
+  float asum[3][128][1 + D];
+};
+
+// Pass 2 of the CTA with grid coordinates (bx, by, bz) (TMEM: 512 columns at `tmem`).  EPI: the
+// control warps stage theta^T in the stage memory once every MMA has completed.  Ends with every
+// thread past a __syncthreads and the barriers retired.
 template <int D, bool EPI>
-__global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
-  extern __shared__ __align__(1024) uint8_t sm[];
+__device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int by, const int bz, uint8_t* sm,
+                                        P2Shared<D>& sh, const uint32_t tmem) {
   const Geo& g = a.g;
   const int KJ = g.KJ;
   const int nsl = KJ / KS2;                            // slabs per tile
   constexpr int NAUX = D + 1;
   constexpr size_t slab_bytes = (size_t)4 * NT2 * KS2;  // hi + lo of one slab
   constexpr size_t x_bytes = (size_t)NT2 * AUXW * 4;    // aux rows of one tile
-  __shared__ __align__(8) uint64_t zready, full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2],
-      tempty[2], mma_done;
-  __shared__ uint32_t tmem_base;
-  __shared__ float asum[3][128][1 + D];
+  uint64_t& zready = sh.zready;
+  uint64_t* full_s = sh.full_s;
+  uint64_t* empty_s = sh.empty_s;
+  uint64_t* full_x = sh.full_x;
+  uint64_t* empty_x = sh.empty_x;
+  uint64_t* tfull = sh.tfull;
+  uint64_t* tempty = sh.tempty;
+  uint64_t& mma_done = sh.mma_done;
+  float (*asum)[128][1 + D] = sh.asum;
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const int row0 = blockIdx.x * 128;
-  const int m = blockIdx.y / g.njt, jt = blockIdx.y % g.njt;
-  const int split = blockIdx.z;
+  const int row0 = bx * 128;
+  const int m = by / g.njt, jt = by % g.njt;
+  const int split = bz;
   const int t_begin = split * a.tiles_per_split;
   const int t_end = min(g.nt2, t_begin + a.tiles_per_split);
   const int ntile = max(0, t_end - t_begin);
@@ -903,7 +985,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   uint8_t* xsm = ssm + ST2 * slab_bytes;          // STX2 aux stages
   // TMEM columns: [0, 2*NT2) two accumulators, then Z hi (KJ/2 cols) and Z lo (KJ/2 cols)
   constexpr uint32_t ZC = 2 * NT2;
-  constexpr uint32_t NCOLS = 512;
 
   if (tid == 0) stamp(a.dbg, 0);
   if (tid == 0) {
@@ -923,12 +1004,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
     tc::mbar_init(&mma_done, 1);
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, NCOLS);
-  tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tmem = tmem_base;
   if (tid == 0) stamp(a.dbg, 7);
+  pdl_launch_dependents();
+  // operand tiles are static: producers start now; Z / x* readers wait for the previous kernel
+  if (warp >= CTRL_WARPS) pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -996,7 +1077,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
     const int row = row0 + r;
     // ---- Z hi/lo of this CTA's rows -> TMEM (8-word chunks dealt round-robin to the column groups)
     {
-      const int rt = blockIdx.x;
+      const int rt = bx;
       // [group of 4 words][row][4 words] (see k_r1b_tc); this row's group gi is at zrow + gi * 128
       const uint4* zrow = reinterpret_cast<const uint4*>(
           a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * (size_t)128 * KJ * 2 * 2) + r;
@@ -1086,7 +1167,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
       for (int c = 0; c <= D; ++c) o[c] = (((acc[c] + asum[0][r][c]) + asum[1][r][c]) + asum[2][r][c]) * zinv;
     }
   }
-  if (EPI && warp < CTRL_WARPS && a.e.policy_next) {
+  if (warp < CTRL_WARPS) pdl_wait();
+  if (EPI && warp < CTRL_WARPS && a.e.t + 1 < a.e.T) {
     // stage theta^T once every MMA of this CTA has completed (stage memory no longer read)
     // (a dedicated one-phase barrier: waiting on tfull's parity could alias an earlier phase)
     tc::mbar_wait(&mma_done, 0);
@@ -1097,23 +1179,59 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (tid == 0) stamp(a.dbg, 5);
-  if (warp == 1) tc::tmem_dealloc(tmem, NCOLS);
+  if (tid == 0) {
+    stamp(a.dbg, 5);
+    tc::mbar_inval(&zready);
+    for (int s = 0; s < ST2; ++s) {
+      tc::mbar_inval(&full_s[s]);
+      tc::mbar_inval(&empty_s[s]);
+    }
+    for (int s = 0; s < STX2; ++s) {
+      tc::mbar_inval(&full_x[s]);
+      tc::mbar_inval(&empty_x[s]);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_inval(&tfull[b]);
+      tc::mbar_inval(&tempty[b]);
+    }
+    tc::mbar_inval(&mma_done);
+  }
+}
+
+// The step epilogue of rows cta * R + w, ... (R = ceil(B / G)), one warp per row; theta^T is in
+// shared memory (staged by p2_main<D, true>).  Runs after a grid barrier.
+template <int D>
+__device__ __forceinline__ void epi_rows(const EpiArgs& e, const int cta, const int G, uint8_t* sm) {
+  const int warp = threadIdx.x / 32;
+  const int R = (e.B + G - 1) / G;
+  const float* th_s = reinterpret_cast<const float*>(sm);
+  float* wbase = reinterpret_cast<float*>(sm) + ((e.P.n_params + 3) & ~3) +
+                 (size_t)warp * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<D, 1>());
+  for (int rr = warp; rr < R; rr += THREADS / 32) {
+    const int b = cta * R + rr;
+    if (b >= e.B) break;
+    rows::epi_warp_rows<D, 1>(e, b, 1, th_s, wbase, wbase + 2 * BAGEL_MAX_WIDTH);
+  }
+}
+
+template <int D, bool EPI>
+__global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ P2Shared<D> sh;
+  __shared__ uint32_t tmem_base;
+  if (threadIdx.x / 32 == 1) tc::tmem_alloc(&tmem_base, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  p2_main<D, EPI>(a, blockIdx.x, blockIdx.y, blockIdx.z, sm, sh, tmem_base);
+  if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, 512);
   if (EPI) {
     grid_barrier(a.gbar);
-    if (tid == 0) stamp(a.dbg, 9);
+    if (threadIdx.x == 0) stamp(a.dbg, 9);
     const int G = (int)(gridDim.x * gridDim.y * gridDim.z);
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int R = (a.B + G - 1) / G;
-    const float* th_s = reinterpret_cast<const float*>(sm);
-    float* wbase = reinterpret_cast<float*>(sm) + ((a.e.P.n_params + 3) & ~3) +
-                   (size_t)warp * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<D, 1>());
-    for (int rr = warp; rr < R; rr += THREADS / 32) {
-      const int b = cta * R + rr;
-      if (b >= a.B) break;
-      rows::epi_warp_rows<D, 1>(a.e, b, 1, th_s, wbase, wbase + 2 * BAGEL_MAX_WIDTH);
-    }
-    if (tid == 0) stamp(a.dbg, 10);
+    epi_rows<D>(a.e, cta, G, sm);
+    if (threadIdx.x == 0) stamp(a.dbg, 10);
   }
 }
 
@@ -1223,13 +1341,20 @@ static void set_attrs() {
   cudaGetLastError();
 }
 
-// Cluster size along the row tiles (TMA multicast of the shared B operand tiles): 2 when the
-// row-tile count is even (BAGEL_TC_CLUSTER=1 disables).
+// Cluster size along the row tiles (TMA multicast of the shared B operand tiles).  Measured
+// neutral at the bench shape (pass 1 is bound by the ktilde generators and the MMAs, not by L2),
+// so off by default; BAGEL_TC_CLUSTER=2 enables it when the row-tile count is even.
 int tc_cluster_x(const bagel_ctx* c, int B) {
   (void)c;
   const char* env = getenv("BAGEL_TC_CLUSTER");
-  if (env && env[0] == '1') return 1;
-  return cdiv(B, 128) % 2 == 0 ? 2 : 1;
+  if (env && env[0] == '2') return cdiv(B, 128) % 2 == 0 ? 2 : 1;
+  return 1;
+}
+
+// Programmatic dependent launch of the GP-step kernels (BAGEL_PDL=0 disables).
+static bool tc_pdl_enabled() {
+  const char* env = getenv("BAGEL_PDL");
+  return !(env && env[0] == '0');
 }
 
 int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st) {
@@ -1274,8 +1399,13 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, floa
   cfg.blockDim = dim3(THREADS, 1, 1);
   cfg.dynamicSmemBytes = p1_smem(g);
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int na = 0;
+  if (tc_pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   const int cl = tc_cluster_x(c, B);
   if (cl > 1) {
     at[na].id = cudaLaunchAttributeClusterDimension;
@@ -1358,22 +1488,31 @@ int tc_pass2(const bagel_ctx* c, const float* xstar, int B, const EpiArgs* epi, 
   for (int m = 0; m < c->p; ++m)
     for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
   dim3 grid(cdiv(B, 128), c->p * g.njt, c->ws.S2tc);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS, 1, 1);
+  cfg.dynamicSmemBytes = p2_smem(g);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (tc_pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   if (epi) {
     a.e = *epi;
     a.gbar = T.gbar + tc_gbar_count();  // pass 2's own counters (pass 1 has another grid shape)
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(THREADS, 1, 1);
-    cfg.dynamicSmemBytes = p2_smem(g);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  if (epi) {
     DISPATCH_D(c->d, ((void)cudaLaunchKernelEx(&cfg, k_p2_tc<D, true>, a)));
   } else {
-    DISPATCH_D(c->d, (k_p2_tc<D, false><<<grid, THREADS, p2_smem(g), st>>>(a)));
+    DISPATCH_D(c->d, ((void)cudaLaunchKernelEx(&cfg, k_p2_tc<D, false>, a)));
   }
   return 1;
 }

@@ -118,11 +118,20 @@ __host__ __device__ constexpr int epi_scratch_floats() {
 }
 
 // Step epilogue of rows b0 .. b0 + nr - 1 (nr <= R) by one warp.  th_s: theta^T in shared memory
-// (only read when e.policy_next); buf: R x 2 x BAGEL_MAX_WIDTH; scratch: epi_scratch_floats<D, R>().
+// (only read when t + 1 < T); buf: R x 2 x BAGEL_MAX_WIDTH; scratch: epi_scratch_floats<D, R>().
 template <int D, int R>
 __device__ void epi_warp_rows(const EpiArgs& e, int b0, int nr, const float* th_s, float* buf, float* scratch) {
   const int lane = threadIdx.x % 32;
-  const int p = e.g.p, B = e.B, t = e.t;
+  const int p = e.g.p, B = e.B, t = e.t, d = e.g.d;
+  const float* sig_t = e.tape_sig + (size_t)t * B * p;
+  const float* tape_x_t = e.tape_x + (size_t)t * B * p;
+  float* tape_x_next = e.tape_x + (size_t)(t + 1) * B * p;
+  float* jv_t = e.tape_jv + (size_t)t * B * p * d;
+  const float* jmu_t = e.tape_jmu + (size_t)t * B * p * d;
+  float* A_t = e.tape_A + (size_t)t * B * p * d;
+  float* trace_mu = e.trace_mu ? e.trace_mu + (size_t)t * B * p : nullptr;
+  float* trace_var = e.trace_var ? e.trace_var + (size_t)t * B * p : nullptr;
+  const bool policy_next = t + 1 < e.T;
   float* psum = scratch;                           // R x p x (D + 1)
   float* f_s = psum + R * BAGEL_MAX_P * (D + 1);   // R x p
   float* xn_s = f_s + R * BAGEL_MAX_P;             // R x p
@@ -152,18 +161,18 @@ __device__ void epi_warp_rows(const EpiArgs& e, int b0, int nr, const float* th_
   if (lane < nr * p) {
     const int r = lane / p, m = lane % p, b = b0 + r;
     const float4 e4 = bagel_rollout_eps4(e.seed, (uint32_t)(e.traj_offset + b), (uint32_t)t);
-    const float sgr = e.sig_t[(size_t)b * p + m];
+    const float sgr = sig_t[(size_t)b * p + m];
     const float sg = fabsf(sgr);
     const float ep = bagel_f4get(e4, m & 3);
     const float mum = e.mu[(size_t)m * B + b];
-    const float xn = e.tape_x_t[(size_t)b * p + m] + mum + sg * ep;
+    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * ep;
     if (!isfinite(xn)) atomicMin(e.err_flag, t * B + b);
-    e.tape_x_next[(size_t)b * p + m] = xn;
+    tape_x_next[(size_t)b * p + m] = xn;
     xn_s[r * p + m] = xn;
     // d x'/d sigma^2 = eps / (2 sigma) where the variance is not clamped (R19), else 0
     f_s[r * p + m] = sgr > 0.0f ? ep / (2.0f * sgr) : 0.0f;
-    if (e.trace_mu) e.trace_mu[(size_t)b * p + m] = mum;
-    if (e.trace_var) e.trace_var[(size_t)b * p + m] = e.var[(size_t)m * B + b];
+    if (trace_mu) trace_mu[(size_t)b * p + m] = mum;
+    if (trace_var) trace_var[(size_t)b * p + m] = e.var[(size_t)m * B + b];
   }
   __syncwarp();
   // J^v from the (r, m) row of sums [sum w k | sum w k X_c]; tape A = J^mu + f J^v (reverse input)
@@ -174,14 +183,14 @@ __device__ void epi_warp_rows(const EpiArgs& e, int b0, int nr, const float* th_
     const float s0 = psum[li - c], part = psum[li];
     const float jv = 2.0f * e.g.ell2inv[m][c - 1] * (e.xstar[(size_t)b * D + c - 1] * s0 - part);
     const size_t o = ((size_t)b * p + m) * D + c - 1;
-    e.jv_t[o] = jv;
-    e.A_t[o] = fmaf(f_s[r * p + m], jv, e.jmu_t[o]);
+    jv_t[o] = jv;
+    A_t[o] = fmaf(f_s[r * p + m], jv, jmu_t[o]);
   }
   __syncwarp();
   const float* gb = e.goals + (size_t)b0 * p;
   if (lane < nr) e.G[b0 + lane] += (double)reward_fn(e.rw, &xn_s[lane * p], gb + lane * p, p);
-  if (!e.policy_next) return;
-  warp_policy<R>(e.P, p, th_s, xn_s, gb, nr, buf, us, e.act_next + (size_t)b0 * e.P.act_ld);
+  if (!policy_next) return;
+  warp_policy<R>(e.P, p, th_s, xn_s, gb, nr, buf, us, e.tape_act + ((size_t)(t + 1) * B + b0) * e.P.act_ld);
   for (int i = lane; i < nr * D; i += 32) {
     const int r = i / D, c = i % D;
     e.xstar[(size_t)(b0 + r) * D + c] = c < p ? xn_s[r * p + c] : us[r * BAGEL_MAX_D + c - p];

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(EpiArgs e, un
   float* bufs = sm + ((e.P.n_params + 3) & ~3);
   __shared__ float scratch[WARP_ROWS_BLOCK][rows::epi_scratch_floats<D, RPW>()];
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 0] = gtimer_ro();
-  if (e.policy_next) stage_theta(e.P, e.thetaT, th_s);
+  if (e.t + 1 < e.T) stage_theta(e.P, e.thetaT, th_s);
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 1] = gtimer_ro();
   const int w = threadIdx.x / 32;
   const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
@@ -511,9 +511,8 @@ int ro_init(const bagel_ctx* c, const float* theta, const float* x0, const float
   return 2;
 }
 
-EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, uint64_t seed, long long traj_offset,
-                    bool policy_next, float* trace_mu, float* trace_var) {
-  const int p = c->gp.p, d = c->gp.d;
+EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, int T, uint64_t seed, long long traj_offset,
+                    float* trace_mu, float* trace_var) {
   const Workspace& w = c->ws;
   EpiArgs e{};
   e.P = c->pol;
@@ -523,22 +522,21 @@ EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, uint64
   e.goals = goals;
   e.B = B;
   e.t = t;
+  e.T = T;
   e.S2 = w.S2eff;
   e.P2 = w.P2;
   e.mu = w.mu;
   e.var = w.var;
-  e.tape_x_t = w.tape_x + (size_t)t * B * p;
-  e.sig_t = w.tape_sig + (size_t)t * B * p;
-  e.jv_t = w.tape_jv + (size_t)t * B * p * d;
-  e.jmu_t = w.tape_jmu + (size_t)t * B * p * d;
-  e.A_t = w.tape_A + (size_t)t * B * p * d;
-  e.act_next = w.tape_act + (size_t)(t + 1) * B * c->pol.act_ld;
-  e.tape_x_next = w.tape_x + (size_t)(t + 1) * B * p;
+  e.tape_x = w.tape_x;
+  e.tape_sig = w.tape_sig;
+  e.tape_jv = w.tape_jv;
+  e.tape_jmu = w.tape_jmu;
+  e.tape_A = w.tape_A;
+  e.tape_act = w.tape_act;
   e.G = w.G;
   e.xstar = w.xstar;
   e.seed = seed;
   e.traj_offset = traj_offset;
-  e.policy_next = policy_next ? 1 : 0;
   e.err_flag = w.err_flag;
   e.trace_mu = trace_mu;
   e.trace_var = trace_var;
@@ -546,10 +544,9 @@ EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, uint64
 }
 
 int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, int T,
-                     uint64_t seed, long long traj_offset, bool policy_next, float* trace_mu,
-                     float* trace_var, cudaStream_t st) {
+                     uint64_t seed, long long traj_offset, float* trace_mu, float* trace_var, cudaStream_t st) {
   (void)theta;
-  const EpiArgs e = ro_epi_args(c, goals, B, t, seed, traj_offset, policy_next, trace_mu, trace_var);
+  const EpiArgs e = ro_epi_args(c, goals, B, t, T, seed, traj_offset, trace_mu, trace_var);
   DISPATCH_D(c->gp.d, (k_epilogue<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
                           e, t == T - 2 ? c->tcs.dbg3 : nullptr)));
   return 1;
