@@ -956,7 +956,7 @@ struct P2Shared {
 // thread past a __syncthreads and the barriers retired.
 template <int D, bool EPI>
 __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int by, const int bz, uint8_t* sm,
-                                        P2Shared<D>& sh, const uint32_t tmem) {
+                                        P2Shared<D>& sh, const uint32_t tmem, const bool stage_theta) {
   const Geo& g = a.g;
   const int KJ = g.KJ;
   const int nsl = KJ / KS2;                            // slabs per tile
@@ -1088,8 +1088,9 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
         for (int it = 0; it < 8; ++it) {
           const int w0 = base + it * 32;
           if (w0 < KJ) {
-            q[it][0] = __ldg(zrow + (size_t)(w0 / 4) * 128);
-            q[it][1] = __ldg(zrow + (size_t)(w0 / 4 + 1) * 128);
+            // L2 loads (not the read-only path): in the persistent rollout kernel Z changes every step
+            q[it][0] = __ldcg(zrow + (size_t)(w0 / 4) * 128);
+            q[it][1] = __ldcg(zrow + (size_t)(w0 / 4 + 1) * 128);
           }
         }
         if (tid == 32 * CTRL_WARPS && base == cg * 8) stamp(a.dbg, 8 + (q[0][0].x == 0x12345678u));
@@ -1168,7 +1169,7 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
     }
   }
   if (warp < CTRL_WARPS) pdl_wait();
-  if (EPI && warp < CTRL_WARPS && a.e.t + 1 < a.e.T) {
+  if (EPI && warp < CTRL_WARPS && stage_theta) {
     // stage theta^T once every MMA of this CTA has completed (stage memory no longer read)
     // (a dedicated one-phase barrier: waiting on tfull's parity could alias an earlier phase)
     tc::mbar_wait(&mma_done, 0);
@@ -1201,7 +1202,7 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
 // The step epilogue of rows cta * R + w, ... (R = ceil(B / G)), one warp per row; theta^T is in
 // shared memory (staged by p2_main<D, true>).  Runs after a grid barrier.
 template <int D>
-__device__ __forceinline__ void epi_rows(const EpiArgs& e, const int cta, const int G, uint8_t* sm) {
+__device__ __forceinline__ void epi_rows(const EpiArgs& e, const int t, const int cta, const int G, uint8_t* sm) {
   const int warp = threadIdx.x / 32;
   const int R = (e.B + G - 1) / G;
   const float* th_s = reinterpret_cast<const float*>(sm);
@@ -1210,7 +1211,7 @@ __device__ __forceinline__ void epi_rows(const EpiArgs& e, const int cta, const 
   for (int rr = warp; rr < R; rr += THREADS / 32) {
     const int b = cta * R + rr;
     if (b >= e.B) break;
-    rows::epi_warp_rows<D, 1>(e, b, 1, th_s, wbase, wbase + 2 * BAGEL_MAX_WIDTH);
+    rows::epi_warp_rows<D, 1>(e, t, b, 1, th_s, wbase, wbase + 2 * BAGEL_MAX_WIDTH);
   }
 }
 
@@ -1223,14 +1224,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  p2_main<D, EPI>(a, blockIdx.x, blockIdx.y, blockIdx.z, sm, sh, tmem_base);
+  p2_main<D, EPI>(a, blockIdx.x, blockIdx.y, blockIdx.z, sm, sh, tmem_base, a.e.t + 1 < a.e.T);
   if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, 512);
   if (EPI) {
     grid_barrier(a.gbar);
     if (threadIdx.x == 0) stamp(a.dbg, 9);
     const int G = (int)(gridDim.x * gridDim.y * gridDim.z);
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    epi_rows<D>(a.e, cta, G, sm);
+    epi_rows<D>(a.e, a.e.t, cta, G, sm);
     if (threadIdx.x == 0) stamp(a.dbg, 10);
   }
 }

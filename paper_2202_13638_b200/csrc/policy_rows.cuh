@@ -117,12 +117,13 @@ __host__ __device__ constexpr int epi_scratch_floats() {
   return R * BAGEL_MAX_P * (D + 1) + 2 * R * BAGEL_MAX_P + R * BAGEL_MAX_D;
 }
 
-// Step epilogue of rows b0 .. b0 + nr - 1 (nr <= R) by one warp.  th_s: theta^T in shared memory
+// Step epilogue (step t; e.t is ignored) of rows b0 .. b0 + nr - 1 (nr <= R) by one warp.  th_s: theta^T in shared memory
 // (only read when t + 1 < T); buf: R x 2 x BAGEL_MAX_WIDTH; scratch: epi_scratch_floats<D, R>().
 template <int D, int R>
-__device__ void epi_warp_rows(const EpiArgs& e, int b0, int nr, const float* th_s, float* buf, float* scratch) {
+__device__ void epi_warp_rows(const EpiArgs& e, const int t, int b0, int nr, const float* th_s, float* buf,
+                              float* scratch) {
   const int lane = threadIdx.x % 32;
-  const int p = e.g.p, B = e.B, t = e.t, d = e.g.d;
+  const int p = e.g.p, B = e.B, d = e.g.d;
   const float* sig_t = e.tape_sig + (size_t)t * B * p;
   const float* tape_x_t = e.tape_x + (size_t)t * B * p;
   float* tape_x_next = e.tape_x + (size_t)(t + 1) * B * p;

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(EpiArgs e, un
   const int w = threadIdx.x / 32;
   const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
   if (b0 >= e.B) return;  // warp-uniform
-  rows::epi_warp_rows<D, RPW>(e, b0, min(RPW, e.B - b0), th_s, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH,
+  rows::epi_warp_rows<D, RPW>(e, e.t, b0, min(RPW, e.B - b0), th_s, bufs + (size_t)w * RPW * 2 * BAGEL_MAX_WIDTH,
                               scratch[w]);
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 4] = gtimer_ro();
 }

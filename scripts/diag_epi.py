@@ -39,7 +39,9 @@ for which, nm in ((6, "epilogue"), (4, "pass1"), (5, "pass2")):
             print(f"   [{k:2d}] {names[k] if nm == 'epilogue' and k < len(names) else '':14s} min {v.min():7.2f}  "
                   f"median {np.median(v):7.2f}  max {v.max():7.2f} us")
 
-e0, e1 = allst["epilogue"]
 a0, a1 = allst["pass1"]
 b0, b1 = allst["pass2"]
-print(f"epilogue(T-2) end -> pass1(T-1) start: {(a0 - e1) / 1e3:.2f} us;  pass1 end -> pass2 start: {(b0 - a1) / 1e3:.2f} us")
+print(f"last step: pass1 end -> pass2 start: {(b0 - a1) / 1e3:.2f} us")
+if "epilogue" in allst:
+    e0, e1 = allst["epilogue"]
+    print(f"epilogue(T-2) end -> pass1(T-1) start: {(a0 - e1) / 1e3:.2f} us")
