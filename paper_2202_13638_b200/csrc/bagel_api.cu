@@ -262,6 +262,11 @@ void check_numeric(bagel_ctx* c, int B) {
   int flag = kErrNone;
   CK(cudaMemcpyAsync(&flag, c->ws.err_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (flag == BAGEL_BARRIER_TIMEOUT) {
+    set_err(c, "grid barrier timed out: the one-wave GP-step grid was not co-resident (other work on the "
+               "GPU?); set BAGEL_COOP=1 for cooperative launches");
+    throw Fail{BAGEL_E_CUDA};
+  }
   if (flag != kErrNone) {
     set_err(c, "non-finite state at step %d, row %d", flag / B, flag % B);
     throw Fail{BAGEL_E_NUMERIC};
@@ -716,6 +721,7 @@ extern "C" int bagel_gp_predict(bagel_ctx* c, const float* xstar, int M, float* 
     REQUIRE(M >= 1 && xstar, BAGEL_E_ARG, "bagel_gp_predict: need M >= 1 and xstar non-NULL");
     ensure_workspace(c, M, 1);
     cudaStream_t st = c->stream;
+    CK(cudaMemsetAsync(c->ws.err_flag, 0x7f, sizeof(int), st));  // barrier watchdog report
     float* jmu = dmean ? dmean : c->ws.tape_jmu;
     const bool tc = use_tc(c);
     c->ws.S2eff = tc ? c->ws.S2tc * tc_njt(c) : c->ws.S2;
@@ -726,7 +732,7 @@ extern "C" int bagel_gp_predict(bagel_ctx* c, const float* xstar, int M, float* 
     n += tc ? tc_pass2(c, xstar, M, nullptr, st) : gs_pass2(c, xstar, M, st);
     n += gs_finish_predict(c, xstar, M, mean, var, dmean, dvar, st);
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
+    check_numeric(c, M);  // synchronises; only the barrier watchdog can fire here
     c->last_launches = n;
   });
 }

@@ -13,7 +13,8 @@
 #define BAGEL_MAX_WIDTH 256  // widest MLP layer
 #define BAGEL_MAX_LAYERS 8
 #define BAGEL_MAX_RANK 768
-#define BAGEL_VAR_FLOOR 1e-12f  // S:252 clamp (reading R19)
+#define BAGEL_VAR_FLOOR 1e-12f
+#define BAGEL_BARRIER_TIMEOUT (-2)  // err_flag value: a grid barrier timed out (grid not co-resident)  // S:252 clamp (reading R19)
 
 // sqrt(0.5 * log2(e)): x_hat = x * KAPPA / l so that exp(-1/2 sum (dx/l)^2) = exp2(-||x_hat - X_hat||^2)
 #define BAGEL_KAPPA 0.84932180028801907f

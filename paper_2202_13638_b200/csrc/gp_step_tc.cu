@@ -231,6 +231,7 @@ struct P1Args {
   float* jmu;                // nullable
   float* sig;                // nullable
   unsigned long long* gbar;  // grid barrier counter
+  int* err_flag;             // barrier watchdog report
   int diag;                  // timing experiments only (results invalid): 1 skip generator math, 2 skip MMAs
 };
 
@@ -246,23 +247,37 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int k) {
   }
 }
 
-// Grid-wide barrier for a cooperative launch (every CTA resident): one release-add per CTA on a
-// counter that only grows (each launch adds G; it is zeroed whenever the grid shape changes),
-// then an acquire-poll until the count reaches the next multiple of G.  The release (cumulative
-// over the CTA's writes ordered before it by bar.sync) and the acquire make every CTA's writes
-// before the barrier visible to every CTA after it.
+// Grid-wide barrier of a one-wave grid (every CTA resident: grid <= #SM x occupancy, checked on
+// the host; with programmatic dependent launch the next kernel's CTAs are only admitted after
+// every CTA of this one has started).  One release-add per CTA on a counter that only grows
+// (each launch adds G; zeroed whenever the grid shape changes), then an acquire-poll until the
+// count reaches the next multiple of G.  The release (cumulative over the CTA's writes ordered
+// before it by bar.sync) and the acquire make every CTA's writes before the barrier visible to
+// every CTA after it.  Watchdog: if the grid is not co-resident after all (another context or
+// stream holding SMs), the poll gives up after ~2 s and reports BAGEL_BARRIER_TIMEOUT through
+// err_flag instead of hanging the device.
 constexpr int GB_STRIDE = 32;   // unsigned long longs reserved per counter set
-__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr, int* err_flag) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned long long G = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
     unsigned long long old;
     asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
     const unsigned long long target = (old / G + 1) * G;
-    unsigned long long cur;
+    unsigned long long cur, t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned spins = 0;
     do {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(ctr) : "memory");
-    } while (cur < target);
+      if (cur >= target) break;
+      if ((++spins & 1023u) == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > 2000000000ull) {
+          if (err_flag) atomicMin(err_flag, BAGEL_BARRIER_TIMEOUT);
+          break;
+        }
+      }
+    } while (true);
   }
   __syncthreads();
 }
@@ -733,7 +748,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   p1_main<D, FUSED>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, sm, sh, tmem_base);
   if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, ncols);
   if (FUSED) {
-    grid_barrier(a.gbar);
+    grid_barrier(a.gbar, a.err_flag);
     if (threadIdx.x == 0) stamp(a.dbg, 6);
     p1_reduce<D>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, sm, a.jmu, a.sig);
   }
@@ -1227,7 +1242,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   p2_main<D, EPI>(a, blockIdx.x, blockIdx.y, blockIdx.z, sm, sh, tmem_base, a.e.t + 1 < a.e.T);
   if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, 512);
   if (EPI) {
-    grid_barrier(a.gbar);
+    grid_barrier(a.gbar, a.e.err_flag);
     if (threadIdx.x == 0) stamp(a.dbg, 9);
     const int G = (int)(gridDim.x * gridDim.y * gridDim.z);
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -1352,6 +1367,16 @@ int tc_cluster_x(const bagel_ctx* c, int B) {
   return 1;
 }
 
+// The grid-barrier kernels launch WITHOUT the cooperative attribute by default: a cooperative
+// launch disables programmatic dependent launch, which costs ~6 us per step at C2 (measured:
+// 5.59 vs 6.20 ms per iteration).  Co-residency rests on grid <= #SM x occupancy (checked) and the
+// barrier watchdog.  BAGEL_COOP=1 restores cooperative launches (no PDL), e.g. when other
+// streams share the GPU.
+static bool tc_coop_enabled() {
+  const char* env = getenv("BAGEL_COOP");
+  return env && env[0] == '1';
+}
+
 // Programmatic dependent launch of the GP-step kernels (BAGEL_PDL=0 disables).
 static bool tc_pdl_enabled() {
   const char* env = getenv("BAGEL_PDL");
@@ -1394,6 +1419,7 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, floa
     a.sig = sig_out;
     a.P1h = T.P1h;
     a.gbar = T.gbar;
+    a.err_flag = c->ws.err_flag;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -1415,7 +1441,7 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, floa
     at[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (c->ws.p1_fused) {
+  if (c->ws.p1_fused && tc_coop_enabled()) {
     at[na].id = cudaLaunchAttributeCooperative;
     at[na].val.cooperative = 1;
     ++na;
@@ -1504,9 +1530,11 @@ int tc_pass2(const bagel_ctx* c, const float* xstar, int B, const EpiArgs* epi, 
   if (epi) {
     a.e = *epi;
     a.gbar = T.gbar + tc_gbar_count();  // pass 2's own counters (pass 1 has another grid shape)
-    at[na].id = cudaLaunchAttributeCooperative;
-    at[na].val.cooperative = 1;
-    ++na;
+    if (tc_coop_enabled()) {
+      at[na].id = cudaLaunchAttributeCooperative;
+      at[na].val.cooperative = 1;
+      ++na;
+    }
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
