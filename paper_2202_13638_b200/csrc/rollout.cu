@@ -61,8 +61,15 @@ __device__ void stage_theta(const PolicyDesc& P, const float* __restrict__ theta
   __syncthreads();
 }
 
+// Shared-memory budget of the policy kernels.  Policies whose weights do not fit (C3: 133k
+// parameters) read theta^T from global memory (L1/L2-resident, lanes read consecutive weights).
+constexpr size_t kPolicySmemBudget = 200 * 1024;
+__host__ __device__ inline size_t policy_buf_floats() { return (size_t)WARP_ROWS_BLOCK * RPW * 2 * BAGEL_MAX_WIDTH; }
+__host__ __device__ inline bool policy_theta_staged(const PolicyDesc& P) {
+  return sizeof(float) * (((size_t)P.n_params + 3) / 4 * 4 + policy_buf_floats()) <= kPolicySmemBudget;
+}
 size_t policy_smem(const PolicyDesc& P) {
-  return sizeof(float) * (((P.n_params + 3) & ~3) + (size_t)WARP_ROWS_BLOCK * RPW * 2 * BAGEL_MAX_WIDTH);
+  return sizeof(float) * ((policy_theta_staged(P) ? ((size_t)P.n_params + 3) / 4 * 4 : 0) + policy_buf_floats());
 }
 
 template <int D>
@@ -73,10 +80,11 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_init(PolicyDesc P, Rew
                                                               float* __restrict__ tape_x0, double* __restrict__ G,
                                                               float* __restrict__ xstar, float* __restrict__ act0) {
   extern __shared__ __align__(16) float sm[];
-  float* th_s = sm;
-  float* bufs = sm + ((P.n_params + 3) & ~3);
+  const bool staged = policy_theta_staged(P);
+  const float* th_s = staged ? sm : thetaT;
+  float* bufs = sm + (staged ? ((P.n_params + 3) & ~3) : 0);
   __shared__ float us[WARP_ROWS_BLOCK][RPW][BAGEL_MAX_D];
-  stage_theta(P, thetaT, th_s);
+  if (staged) stage_theta(P, thetaT, sm);
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
   if (b0 >= B) return;  // warp-uniform
@@ -96,11 +104,12 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_init(PolicyDesc P, Rew
 template <int D>
 __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(EpiArgs e, unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(16) float sm[];
-  float* th_s = sm;
-  float* bufs = sm + ((e.P.n_params + 3) & ~3);
+  const bool staged = policy_theta_staged(e.P);
+  const float* th_s = staged ? sm : e.thetaT;
+  float* bufs = sm + (staged ? ((e.P.n_params + 3) & ~3) : 0);
   __shared__ float scratch[WARP_ROWS_BLOCK][rows::epi_scratch_floats<D, RPW>()];
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 0] = gtimer_ro();
-  if (e.t + 1 < e.T) stage_theta(e.P, e.thetaT, th_s);
+  if (staged && e.t + 1 < e.T) stage_theta(e.P, e.thetaT, sm);
   if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 16 + 1] = gtimer_ro();
   const int w = threadIdx.x / 32;
   const int b0 = blockIdx.x * ROWS_BLOCK + w * RPW;
@@ -143,6 +152,10 @@ __host__ __device__ inline int rev2_row_floats(const PolicyDesc& P, int p, int d
 __host__ __device__ inline int rev2_warp_floats(const PolicyDesc& P, int p, int d) {
   return 2 * ((P.max_width + 3) & ~3) + 2 * rev2_row_floats(P, p, d);
 }
+__host__ __device__ inline bool rev2_theta_staged(const PolicyDesc& P, int p, int d) {
+  return sizeof(float) * ((((size_t)P.n_params + 3) & ~(size_t)3) + (size_t)REV2_WARPS * rev2_warp_floats(P, p, d)) <=
+         200 * 1024;
+}
 
 template <int D>
 __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
@@ -150,15 +163,17 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     int T, const float* __restrict__ tape_x, const float* __restrict__ tape_A, const float* __restrict__ tape_act,
     float* __restrict__ tape_delta, float invB) {
   extern __shared__ __align__(16) float sm[];
-  const int np4 = (P.n_params + 3) & ~3;
+  const bool staged = rev2_theta_staged(P, p, D);
+  const int np4 = staged ? (P.n_params + 3) & ~3 : 0;
   const int RF = rev2_row_floats(P, p, D);
   const int mw4 = (P.max_width + 3) & ~3;
-  float* th_s = sm;
+  const float* th_s = staged ? sm : theta;  // W row-major, as theta (global when too large)
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-  float* d0 = th_s + np4 + (size_t)w * rev2_warp_floats(P, p, D);  // this warp's region
+  float* d0 = sm + np4 + (size_t)w * rev2_warp_floats(P, p, D);  // this warp's region
   float* d1 = d0 + mw4;
   float* rows = d1 + mw4;  // 2 x RF: [act | A | x] of one step
-  for (int i = threadIdx.x; i < P.n_params; i += blockDim.x) th_s[i] = __ldg(theta + i);
+  if (staged)
+    for (int i = threadIdx.x; i < P.n_params; i += blockDim.x) sm[i] = __ldg(theta + i);
   __syncthreads();
   const int b = blockIdx.x * REV2_WARPS + w;
   if (b >= B || T <= 0) return;  // warp-uniform
@@ -298,16 +313,17 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
 // slices of every staged row.
 constexpr int TG_THREADS = 256, TG_KC = 32, TG_ST = 3, TG_JOBS = 2;
 
-__global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long long K, const float* __restrict__ tape_act,
+__global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long long K, int KC,
+                                                          const float* __restrict__ tape_act,
                                                           const float* __restrict__ tape_delta,
                                                           float* __restrict__ theta_part) {
   extern __shared__ __align__(16) float sm[];
   __shared__ __align__(8) uint64_t full[TG_ST];
   const int AL = P.act_ld, DL = P.d_ld;
-  const int stage_f = TG_KC * (AL + DL);
+  const int stage_f = KC * (AL + DL);
   const long long per = (K + gridDim.x - 1) / gridDim.x;
   const long long k0 = blockIdx.x * per, k1 = min(K, k0 + per);
-  const int nchunks = k1 > k0 ? (int)((k1 - k0 + TG_KC - 1) / TG_KC) : 0;
+  const int nchunks = k1 > k0 ? (int)((k1 - k0 + KC - 1) / KC) : 0;
   float* out = theta_part + (size_t)blockIdx.x * P.n_params;
   if (threadIdx.x == 0) {
     for (int s = 0; s < TG_ST; ++s) tc::mbar_init(&full[s], 1);
@@ -321,13 +337,13 @@ __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long lo
   // chunk g of the whole sequence: batch g / nchunks, rows of chunk g % nchunks; stage g % TG_ST
   auto issue = [&](int g) {
     const int s = g % TG_ST, c = g % nchunks;
-    const long long r0 = k0 + (long long)c * TG_KC;
-    const int rows = (int)min((long long)TG_KC, k1 - r0);
+    const long long r0 = k0 + (long long)c * KC;
+    const int rows = (int)min((long long)KC, k1 - r0);
     const uint32_t ba = (uint32_t)rows * AL * 4, bd = (uint32_t)rows * DL * 4;
     tc::mbar_arrive_expect_tx(&full[s], ba + bd);
     float* dst = sm + (size_t)s * stage_f;
     tc::bulk_g2s(dst, tape_act + r0 * AL, ba, &full[s]);
-    tc::bulk_g2s(dst + TG_KC * AL, tape_delta + r0 * DL, bd, &full[s]);
+    tc::bulk_g2s(dst + KC * AL, tape_delta + r0 * DL, bd, &full[s]);
   };
   if (threadIdx.x == 0)
     for (int g = 0; g < TG_ST && g < total; ++g) issue(g);
@@ -356,10 +372,10 @@ __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long lo
       for (int e = 0; e < 16; ++e) acc[u][e] = 0.0f;
     for (int c = 0; c < nchunks; ++c) {
       const int g = batch * nchunks + c, s = g % TG_ST;
-      const int rows = (int)min((long long)TG_KC, k1 - (k0 + (long long)c * TG_KC));
+      const int rows = (int)min((long long)KC, k1 - (k0 + (long long)c * KC));
       tc::mbar_wait(&full[s], (uint32_t)(g / TG_ST) & 1u);
       const float* hs = sm + (size_t)s * stage_f;
-      const float* ds = hs + TG_KC * AL;
+      const float* ds = hs + KC * AL;
 #pragma unroll
       for (int u = 0; u < TG_JOBS; ++u) {
         if (jd[u] < 0) continue;
@@ -476,9 +492,19 @@ size_t epi_smem(const PolicyDesc& P) { return sizeof(float) * EPI_ROWS * P.act_t
 }  // namespace
 
 size_t ro_reverse_smem(const PolicyDesc& P, int p, int d) {
-  return sizeof(float) * (((P.n_params + 3) & ~3) + (size_t)REV2_WARPS * rev2_warp_floats(P, p, d));
+  return sizeof(float) * ((rev2_theta_staged(P, p, d) ? ((P.n_params + 3) & ~3) : 0) +
+                          (size_t)REV2_WARPS * rev2_warp_floats(P, p, d));
 }
-size_t ro_theta_grad_smem(const PolicyDesc& P) { return sizeof(float) * (size_t)TG_ST * TG_KC * (P.act_ld + P.d_ld); }
+// rows per staged chunk of the theta-gradient contraction: TG_KC, fewer for wide policies so the
+// TG_ST-stage ring stays within 200 KB
+int tg_chunk_rows(const PolicyDesc& P) {
+  const size_t row_bytes = sizeof(float) * (size_t)(P.act_ld + P.d_ld);
+  const int kc = (int)std::min<size_t>(TG_KC, (200 * 1024) / (TG_ST * row_bytes));
+  return std::max(kc, 1);
+}
+size_t ro_theta_grad_smem(const PolicyDesc& P) {
+  return sizeof(float) * (size_t)TG_ST * tg_chunk_rows(P) * (P.act_ld + P.d_ld);
+}
 int ro_theta_blocks(const bagel_ctx* c, int B, int T) {
   const long long K = (long long)B * std::max(T, 1);
   return (int)std::max(1LL, std::min((long long)c->num_sms, K / 64));
@@ -567,8 +593,8 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
 
 int ro_theta_grad(const bagel_ctx* c, int B, int T, int nblk, cudaStream_t st) {
   const Workspace& w = c->ws;
-  k_theta_grad<<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(c->pol, (long long)T * B, w.tape_act,
-                                                                      w.tape_delta, w.theta_part);
+  k_theta_grad<<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(c->pol, (long long)T * B, tg_chunk_rows(c->pol),
+                                                                      w.tape_act, w.tape_delta, w.theta_part);
   return 1;
 }
 

@@ -408,3 +408,17 @@ def test_tc_path_rank_above_256_and_ragged_batch(bagel):
     seed = W.rollout_seed(9)
     cost, grad = _rollout_gpu(ctx, wl, goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "k=300")
+
+
+def test_c3_wide_policy_subset(bagel):
+    """C3's policy (4-256-256-256-1, 133,121 parameters: the weights no longer fit shared memory, so
+    the policy, reverse and theta-gradient kernels take their global-memory / narrow-chunk paths)
+    at full N and rank on a subset of trajectories and a short horizon."""
+    wl = W.config("C3", B=96, T=12)
+    assert W.n_params(wl.sizes) == 133121
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    seed = W.rollout_seed(2)
+    cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), "C3 subset")
