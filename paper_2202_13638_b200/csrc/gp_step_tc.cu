@@ -637,15 +637,17 @@ __device__ __forceinline__ void p1_reduce(const P1Args& a, const int bx, const i
   const int rtn = cdiv_dev(a.B, 128);
   const float* zs = reinterpret_cast<const float*>(sm);
   {
-    const bool act = lane * 8 < NZ;
+    // lane l owns columns 4l .. 4l+3 and 128 + 4l .. 128 + 4l + 3: every float4 load of a warp is
+    // one contiguous 512-byte segment (full 32-byte sectors; the L2-only loads are not re-fetched)
+    const bool act0 = lane * 4 < NZ, act1 = 128 + lane * 4 < NZ;
     const size_t sstride = (size_t)a.m_count * rtn * 128 * NZ;  // floats per split
     for (int rr = split + S * warp; rr < 128 && row0 + rr < a.B; rr += S * (THREADS / 32)) {
       const int mm = m, row = row0 + rr;
-      const float* src = a.P1z + ((size_t)mm * rtn * 128 + row) * NZ + lane * 8;
+      const float* src = a.P1z + ((size_t)mm * rtn * 128 + row) * NZ + lane * 4;
+      const float* own = zs + rr * LDZ + lane * 4;
       const float* hsrc = a.P1h + ((size_t)mm * a.B + row) * (1 + D) + min(lane, D);
       const size_t hstride = (size_t)a.m_count * a.B * (1 + D);
-      // sum the S partials of columns lane*8 .. lane*8+7 in split order (own one from shared
-      // memory; 6 splits' loads in flight)
+      // sum the S partials in split order (own one from shared memory; 6 splits' loads in flight)
       float z[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) z[e] = 0.0f;
@@ -656,26 +658,21 @@ __device__ __forceinline__ void p1_reduce(const P1Args& a, const int bx, const i
 #pragma unroll
         for (int ss = 0; ss < 6; ++ss) {
           if (s0 + ss < S) {
-            if (act) {
-              const float* p = s0 + ss == split ? zs + rr * LDZ + lane * 8 : src + (s0 + ss) * sstride;
-              if (s0 + ss == split) {
-                q[ss][0] = *reinterpret_cast<const float4*>(p);
-                q[ss][1] = *reinterpret_cast<const float4*>(p + 4);
-              } else {
-                q[ss][0] = __ldcg(reinterpret_cast<const float4*>(p));
-                q[ss][1] = __ldcg(reinterpret_cast<const float4*>(p + 4));
-              }
-            }
+            const bool mine = s0 + ss == split;
+            const float* p = src + (s0 + ss) * sstride;
+            q[ss][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            q[ss][1] = q[ss][0];
+            if (act0) q[ss][0] = mine ? *reinterpret_cast<const float4*>(own) : __ldcg(reinterpret_cast<const float4*>(p));
+            if (act1)
+              q[ss][1] = mine ? *reinterpret_cast<const float4*>(own + 128) : __ldcg(reinterpret_cast<const float4*>(p + 128));
             if (lane <= D) hq[ss] = __ldcg(hsrc + (s0 + ss) * hstride);
           }
         }
 #pragma unroll
         for (int ss = 0; ss < 6; ++ss) {
           if (s0 + ss < S) {
-            if (act) {
-              z[0] += q[ss][0].x; z[1] += q[ss][0].y; z[2] += q[ss][0].z; z[3] += q[ss][0].w;
-              z[4] += q[ss][1].x; z[5] += q[ss][1].y; z[6] += q[ss][1].z; z[7] += q[ss][1].w;
-            }
+            z[0] += q[ss][0].x; z[1] += q[ss][0].y; z[2] += q[ss][0].z; z[3] += q[ss][0].w;
+            z[4] += q[ss][1].x; z[5] += q[ss][1].y; z[6] += q[ss][1].z; z[7] += q[ss][1].w;
             if (lane <= D) hv += hq[ss];
           }
         }
@@ -686,8 +683,8 @@ __device__ __forceinline__ void p1_reduce(const P1Args& a, const int bx, const i
       float zm = 0.0f;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int j = lane * 8 + e;
-        const float v = (act && j < g.k) ? z[e] * a.colscale[(size_t)mm * g.k + j] : 0.0f;
+        const int j = (e < 4 ? 0 : 128) + lane * 4 + (e & 3);
+        const float v = j < g.k ? z[e] * a.colscale[(size_t)mm * g.k + j] : 0.0f;
         z[e] = v;
         zz += (double)v * (double)v;
         zm = fmaxf(zm, fabsf(v));
@@ -712,22 +709,27 @@ __device__ __forceinline__ void p1_reduce(const P1Args& a, const int bx, const i
       if (jmu && lane >= 1 && lane <= D)
         jmu[((size_t)row * g.p + mm) * D + lane - 1] =
             (hv - a.xstar[(size_t)row * D + lane - 1] * h0) * a.ell2inv[mm][lane - 1];
-      if (act) {
-        // packed pass-2 A operand (see k_r1b_tc): hi group `lane`, lo group KJ/8 + lane
-        uint32_t hw[4], lw[4];
+      // packed pass-2 A operand (see k_r1b_tc): columns 4l.. of group l/2 (half l%2) and
+      // 128+4l.. of group 16 + l/2; lo groups follow the KJ/8 hi groups
+      const int rrow = row % 128;
+      uint8_t* base = a.Zp + ((size_t)mm * rtn + row / 128) * (size_t)128 * g.KJ * 2 * 2;
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const __half2 h2 = __floats2half2_rn(z[e] * sc, z[e + 1] * sc);
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        if (hlf == 0 ? !act0 : !act1) continue;
+        uint32_t hw[2], lw[2];
+#pragma unroll
+        for (int e = 0; e < 4; e += 2) {
+          const float v0 = z[4 * hlf + e] * sc, v1 = z[4 * hlf + e + 1] * sc;
+          const __half2 h2 = __floats2half2_rn(v0, v1);
           const float2 hf = __half22float2(h2);
-          const __half2 l2 = __floats2half2_rn(z[e] * sc - hf.x, z[e + 1] * sc - hf.y);
+          const __half2 l2 = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
           hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
           lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
         }
-        const int rr = row % 128;
-        uint8_t* base = a.Zp + ((size_t)mm * rtn + row / 128) * (size_t)128 * g.KJ * 2 * 2;
-        *reinterpret_cast<uint4*>(base + ((size_t)lane * 128 + rr) * 16) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(base + ((size_t)(g.KJ / 8 + lane) * 128 + rr) * 16) =
-            make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        const int grp = hlf * 16 + lane / 2;
+        const size_t off = ((size_t)grp * 128 + rrow) * 16 + (lane & 1) * 8;
+        *reinterpret_cast<uint2*>(base + off) = make_uint2(hw[0], hw[1]);
+        *reinterpret_cast<uint2*>(base + off + (size_t)(g.KJ / 8) * 128 * 16) = make_uint2(lw[0], lw[1]);
       }
     }
     if (tid == 0) stamp(a.dbg, 7);

@@ -157,13 +157,13 @@ __host__ __device__ inline bool rev2_theta_staged(const PolicyDesc& P, int p, in
          200 * 1024;
 }
 
-template <int D>
+template <int D, bool STAGED>
 __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     PolicyDesc P, RewardDesc rw, int p, const float* __restrict__ theta, const float* __restrict__ goals, int B,
     int T, const float* __restrict__ tape_x, const float* __restrict__ tape_A, const float* __restrict__ tape_act,
     float* __restrict__ tape_delta, float invB) {
   extern __shared__ __align__(16) float sm[];
-  const bool staged = rev2_theta_staged(P, p, D);
+  constexpr bool staged = STAGED;  // (a compile-time choice: shared-memory W reads stay LDS)
   const int np4 = staged ? (P.n_params + 3) & ~3 : 0;
   const int RF = rev2_row_floats(P, p, D);
   const int mw4 = (P.max_width + 3) & ~3;
@@ -519,7 +519,8 @@ void ro_set_attributes() {
   bagel_set_smem_attr(k_theta_grad, 200 * 1024);
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
-      bagel_set_smem_attr(k_reverse2<D>, 200 * 1024);
+      bagel_set_smem_attr(k_reverse2<D, true>, 200 * 1024);
+      bagel_set_smem_attr(k_reverse2<D, false>, 200 * 1024);
       bagel_set_smem_attr(k_epilogue<D>, 200 * 1024);
       bagel_set_smem_attr(k_init<D>, 200 * 1024);
 
@@ -584,9 +585,17 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
   (void)traj_offset;
   ro_set_attributes();
   const Workspace& w = c->ws;
-  DISPATCH_D(c->gp.d, (k_reverse2<D><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, ro_reverse_smem(c->pol, c->gp.p, c->gp.d), st>>>(
-                          c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
-                          (float)(1.0 / (double)B_global))));
+  const size_t smem = ro_reverse_smem(c->pol, c->gp.p, c->gp.d);
+  const float invB = (float)(1.0 / (double)B_global);
+  if (rev2_theta_staged(c->pol, c->gp.p, c->gp.d)) {
+    DISPATCH_D(c->gp.d, (k_reverse2<D, true><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, smem, st>>>(
+                            c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
+                            invB)));
+  } else {
+    DISPATCH_D(c->gp.d, (k_reverse2<D, false><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, smem, st>>>(
+                            c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
+                            invB)));
+  }
   *nblk_out = ro_theta_blocks(c, B, T);
   return 1;
 }
