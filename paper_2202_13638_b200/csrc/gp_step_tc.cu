@@ -257,6 +257,38 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int k) {
 // stream holding SMs), the poll gives up after ~2 s and reports BAGEL_BARRIER_TIMEOUT through
 // err_flag instead of hanging the device.
 constexpr int GB_STRIDE = 32;   // unsigned long longs reserved per counter set
+// Split phase: grid_arrive (after a __syncthreads: this CTA's writes are released) returns the
+// target thread 0 must see; work that does not depend on other CTAs can run between the two.
+__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long* ctr) {
+  __syncthreads();
+  unsigned long long target = 0;
+  if (threadIdx.x == 0) {
+    const unsigned long long G = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    unsigned long long old;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+    target = (old / G + 1) * G;
+  }
+  return target;
+}
+__device__ __forceinline__ void grid_wait(unsigned long long* ctr, unsigned long long target, int* err_flag) {
+  if (threadIdx.x == 0) {
+    unsigned long long cur, t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    unsigned spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(ctr) : "memory");
+      if (cur >= target) break;
+      if ((++spins & 1023u) == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > 2000000000ull) {
+          if (err_flag) atomicMin(err_flag, BAGEL_BARRIER_TIMEOUT);
+          break;
+        }
+      }
+    } while (true);
+  }
+  __syncthreads();
+}
 __device__ __forceinline__ void grid_barrier(unsigned long long* ctr, int* err_flag) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1218,17 +1250,21 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
 
 // The step epilogue of rows cta * R + w, ... (R = ceil(B / G)), one warp per row; theta^T is in
 // shared memory (staged by p2_main<D, true>).  Runs after a grid barrier.
-template <int D>
+// PHASE 0: epi_pre, 1: epi_post (same warp, same scratch; rows per warp must fit one pass, i.e.
+// R <= warps, which tc_pass2_epi_ok guarantees).
+template <int D, int PHASE>
 __device__ __forceinline__ void epi_rows(const EpiArgs& e, const int t, const int cta, const int G, uint8_t* sm) {
   const int warp = threadIdx.x / 32;
   const int R = (e.B + G - 1) / G;
   const float* th_s = reinterpret_cast<const float*>(sm);
   float* wbase = reinterpret_cast<float*>(sm) + ((e.P.n_params + 3) & ~3) +
                  (size_t)warp * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<D, 1>());
-  for (int rr = warp; rr < R; rr += THREADS / 32) {
-    const int b = cta * R + rr;
-    if (b >= e.B) break;
-    rows::epi_warp_rows<D, 1>(e, t, b, 1, th_s, wbase, wbase + 2 * BAGEL_MAX_WIDTH);
+  if (warp < R) {
+    const int b = cta * R + warp;
+    if (b < e.B) {
+      if (PHASE == 0) rows::epi_pre<D, 1>(e, t, b, 1, wbase + 2 * BAGEL_MAX_WIDTH);
+      else rows::epi_post<D, 1>(e, t, b, 1, th_s, wbase, wbase + 2 * BAGEL_MAX_WIDTH);
+    }
   }
 }
 
@@ -1244,11 +1280,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   p2_main<D, EPI>(a, blockIdx.x, blockIdx.y, blockIdx.z, sm, sh, tmem_base, a.e.t + 1 < a.e.T);
   if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, 512);
   if (EPI) {
-    grid_barrier(a.gbar, a.e.err_flag);
-    if (threadIdx.x == 0) stamp(a.dbg, 9);
+    // arrive, then the pass-1-only half of this CTA's rows while the other CTAs finish pass 2
+    const unsigned long long target = grid_arrive(a.gbar);
     const int G = (int)(gridDim.x * gridDim.y * gridDim.z);
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    epi_rows<D>(a.e, a.e.t, cta, G, sm);
+    epi_rows<D, 0>(a.e, a.e.t, cta, G, sm);
+    grid_wait(a.gbar, target, a.e.err_flag);
+    if (threadIdx.x == 0) stamp(a.dbg, 9);
+    epi_rows<D, 1>(a.e, a.e.t, cta, G, sm);
     if (threadIdx.x == 0) stamp(a.dbg, 10);
   }
 }
@@ -1495,7 +1534,8 @@ bool tc_pass2_epi_ok(const bagel_ctx* c, int B) {
   const size_t need = sizeof(float) * (((size_t)c->pol.n_params + 3) / 4 * 4 +
                                        (size_t)(THREADS / 32) * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<8, 1>()));
   const char* env = getenv("BAGEL_P2_EPI");
-  return ctas <= c->num_sms && need <= p2_smem(g) && !(env && env[0] == '0');
+  const long long rows_per_cta = ctas > 0 ? (B + ctas - 1) / ctas : 0;
+  return ctas <= c->num_sms && need <= p2_smem(g) && rows_per_cta <= THREADS / 32 && !(env && env[0] == '0');
 }
 
 int tc_pass2(const bagel_ctx* c, const float* xstar, int B, const EpiArgs* epi, cudaStream_t st) {

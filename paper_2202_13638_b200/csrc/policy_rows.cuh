@@ -114,29 +114,82 @@ __device__ void warp_policy(const PolicyDesc& P, int p, const float* th_s, const
 // Per-warp scratch of epi_warp_rows (floats)
 template <int D, int R>
 __host__ __device__ constexpr int epi_scratch_floats() {
-  return R * BAGEL_MAX_P * (D + 1) + 2 * R * BAGEL_MAX_P + R * BAGEL_MAX_D;
+  return R * BAGEL_MAX_P * (D + 1) + 2 * R * BAGEL_MAX_P + R * BAGEL_MAX_D + R * BAGEL_MAX_P * BAGEL_MAX_D +
+         R * BAGEL_MAX_D;
 }
 
-// Step epilogue (step t; e.t is ignored) of rows b0 .. b0 + nr - 1 (nr <= R) by one warp.  th_s: theta^T in shared memory
-// (only read when t + 1 < T); buf: R x 2 x BAGEL_MAX_WIDTH; scratch: epi_scratch_floats<D, R>().
+// The step epilogue (step t; e.t is ignored) of rows b0 .. b0 + nr - 1 (nr <= R) by one warp, in
+// two halves so that the first can overlap a grid barrier:
+//   epi_pre   everything that needs only pass 1 of this step: eps (Philox), x' = x + mu + sigma eps,
+//             the tapes of x', f = eps / (2 sigma), and the J^mu / x* rows into scratch;
+//   epi_post  pass-2 sums -> J^v, A = J^mu + f J^v, r(x'), the next action.
+// scratch: epi_scratch_floats<D, R>() floats; buf (post): R x 2 x BAGEL_MAX_WIDTH; th_s: theta^T
+// (read when t + 1 < T).
 template <int D, int R>
-__device__ void epi_warp_rows(const EpiArgs& e, const int t, int b0, int nr, const float* th_s, float* buf,
-                              float* scratch) {
+struct EpiScratch {
+  float* psum;  // R x p x (D + 1)
+  float* f_s;   // R x p
+  float* xn_s;  // R x p
+  float* us;    // R x MAX_D
+  float* jmu;   // R x p x D
+  float* xq;    // R x MAX_D (this step's x*)
+  __device__ explicit EpiScratch(float* s) {
+    psum = s;
+    f_s = psum + R * BAGEL_MAX_P * (D + 1);
+    xn_s = f_s + R * BAGEL_MAX_P;
+    us = xn_s + R * BAGEL_MAX_P;
+    jmu = us + R * BAGEL_MAX_D;
+    xq = jmu + R * BAGEL_MAX_P * BAGEL_MAX_D;
+  }
+};
+
+template <int D, int R>
+__device__ void epi_pre(const EpiArgs& e, const int t, int b0, int nr, float* scratch) {
   const int lane = threadIdx.x % 32;
   const int p = e.g.p, B = e.B, d = e.g.d;
+  EpiScratch<D, R> sc(scratch);
   const float* sig_t = e.tape_sig + (size_t)t * B * p;
   const float* tape_x_t = e.tape_x + (size_t)t * B * p;
   float* tape_x_next = e.tape_x + (size_t)(t + 1) * B * p;
-  float* jv_t = e.tape_jv + (size_t)t * B * p * d;
   const float* jmu_t = e.tape_jmu + (size_t)t * B * p * d;
-  float* A_t = e.tape_A + (size_t)t * B * p * d;
   float* trace_mu = e.trace_mu ? e.trace_mu + (size_t)t * B * p : nullptr;
   float* trace_var = e.trace_var ? e.trace_var + (size_t)t * B * p : nullptr;
+  if (lane < nr * p) {
+    const int r = lane / p, m = lane % p, b = b0 + r;
+    const float4 e4 = bagel_rollout_eps4(e.seed, (uint32_t)(e.traj_offset + b), (uint32_t)t);
+    const float sgr = sig_t[(size_t)b * p + m];
+    const float sg = fabsf(sgr);
+    const float ep = bagel_f4get(e4, m & 3);
+    const float mum = e.mu[(size_t)m * B + b];
+    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * ep;
+    if (!isfinite(xn)) atomicMin(e.err_flag, t * B + b);
+    tape_x_next[(size_t)b * p + m] = xn;
+    sc.xn_s[r * p + m] = xn;
+    // d x'/d sigma^2 = eps / (2 sigma) where the variance is not clamped (R19), else 0
+    sc.f_s[r * p + m] = sgr > 0.0f ? ep / (2.0f * sgr) : 0.0f;
+    if (trace_mu) trace_mu[(size_t)b * p + m] = mum;
+    if (trace_var) trace_var[(size_t)b * p + m] = e.var[(size_t)m * B + b];
+  }
+  for (int i = lane; i < nr * p * D; i += 32) {
+    const int r = i / (p * D), o = i % (p * D);
+    sc.jmu[r * BAGEL_MAX_P * BAGEL_MAX_D + o] = jmu_t[(size_t)(b0 + r) * p * D + o];
+  }
+  for (int i = lane; i < nr * D; i += 32) {
+    const int r = i / D, c = i % D;
+    sc.xq[r * BAGEL_MAX_D + c] = e.xstar[(size_t)(b0 + r) * D + c];
+  }
+  __syncwarp();
+}
+
+template <int D, int R>
+__device__ void epi_post(const EpiArgs& e, const int t, int b0, int nr, const float* th_s, float* buf,
+                         float* scratch) {
+  const int lane = threadIdx.x % 32;
+  const int p = e.g.p, B = e.B, d = e.g.d;
+  EpiScratch<D, R> sc(scratch);
+  float* jv_t = e.tape_jv + (size_t)t * B * p * d;
+  float* A_t = e.tape_A + (size_t)t * B * p * d;
   const bool policy_next = t + 1 < e.T;
-  float* psum = scratch;                           // R x p x (D + 1)
-  float* f_s = psum + R * BAGEL_MAX_P * (D + 1);   // R x p
-  float* xn_s = f_s + R * BAGEL_MAX_P;             // R x p
-  float* us = xn_s + R * BAGEL_MAX_P;              // R x MAX_D
   // lane = r * p * (D + 1) + m * (D + 1) + c: pass-2 partial of (row r, output m, column c)
   const int per_row = p * (D + 1);
   const int nl = nr * per_row;
@@ -156,24 +209,8 @@ __device__ void epi_warp_rows(const EpiArgs& e, const int t, int b0, int nr, con
 #pragma unroll
         for (int u = 0; u < 8; ++u) part += v[u];
       }
-      psum[li] = part;
+      sc.psum[li] = part;
     }
-  }
-  if (lane < nr * p) {
-    const int r = lane / p, m = lane % p, b = b0 + r;
-    const float4 e4 = bagel_rollout_eps4(e.seed, (uint32_t)(e.traj_offset + b), (uint32_t)t);
-    const float sgr = sig_t[(size_t)b * p + m];
-    const float sg = fabsf(sgr);
-    const float ep = bagel_f4get(e4, m & 3);
-    const float mum = e.mu[(size_t)m * B + b];
-    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * ep;
-    if (!isfinite(xn)) atomicMin(e.err_flag, t * B + b);
-    tape_x_next[(size_t)b * p + m] = xn;
-    xn_s[r * p + m] = xn;
-    // d x'/d sigma^2 = eps / (2 sigma) where the variance is not clamped (R19), else 0
-    f_s[r * p + m] = sgr > 0.0f ? ep / (2.0f * sgr) : 0.0f;
-    if (trace_mu) trace_mu[(size_t)b * p + m] = mum;
-    if (trace_var) trace_var[(size_t)b * p + m] = e.var[(size_t)m * B + b];
   }
   __syncwarp();
   // J^v from the (r, m) row of sums [sum w k | sum w k X_c]; tape A = J^mu + f J^v (reverse input)
@@ -181,22 +218,29 @@ __device__ void epi_warp_rows(const EpiArgs& e, const int t, int b0, int nr, con
     const int r = li / per_row, m = (li % per_row) / (D + 1), c = li % (D + 1);
     if (c == 0) continue;
     const int b = b0 + r;
-    const float s0 = psum[li - c], part = psum[li];
-    const float jv = 2.0f * e.g.ell2inv[m][c - 1] * (e.xstar[(size_t)b * D + c - 1] * s0 - part);
+    const float s0 = sc.psum[li - c], part = sc.psum[li];
+    const float jv = 2.0f * e.g.ell2inv[m][c - 1] * (sc.xq[r * BAGEL_MAX_D + c - 1] * s0 - part);
     const size_t o = ((size_t)b * p + m) * D + c - 1;
     jv_t[o] = jv;
-    A_t[o] = fmaf(f_s[r * p + m], jv, jmu_t[o]);
+    A_t[o] = fmaf(sc.f_s[r * p + m], jv, sc.jmu[r * BAGEL_MAX_P * BAGEL_MAX_D + m * D + c - 1]);
   }
   __syncwarp();
   const float* gb = e.goals + (size_t)b0 * p;
-  if (lane < nr) e.G[b0 + lane] += (double)reward_fn(e.rw, &xn_s[lane * p], gb + lane * p, p);
+  if (lane < nr) e.G[b0 + lane] += (double)reward_fn(e.rw, &sc.xn_s[lane * p], gb + lane * p, p);
   if (!policy_next) return;
-  warp_policy<R>(e.P, p, th_s, xn_s, gb, nr, buf, us, e.tape_act + ((size_t)(t + 1) * B + b0) * e.P.act_ld);
+  warp_policy<R>(e.P, p, th_s, sc.xn_s, gb, nr, buf, sc.us, e.tape_act + ((size_t)(t + 1) * B + b0) * e.P.act_ld);
   for (int i = lane; i < nr * D; i += 32) {
     const int r = i / D, c = i % D;
-    e.xstar[(size_t)(b0 + r) * D + c] = c < p ? xn_s[r * p + c] : us[r * BAGEL_MAX_D + c - p];
+    e.xstar[(size_t)(b0 + r) * D + c] = c < p ? sc.xn_s[r * p + c] : sc.us[r * BAGEL_MAX_D + c - p];
   }
   __syncwarp();
+}
+
+template <int D, int R>
+__device__ void epi_warp_rows(const EpiArgs& e, const int t, int b0, int nr, const float* th_s, float* buf,
+                              float* scratch) {
+  epi_pre<D, R>(e, t, b0, nr, scratch);
+  epi_post<D, R>(e, t, b0, nr, th_s, buf, scratch);
 }
 
 }  // namespace rows

@@ -41,7 +41,13 @@ for which, nm in ((6, "epilogue"), (4, "pass1"), (5, "pass2")):
 
 a0, a1 = allst["pass1"]
 b0, b1 = allst["pass2"]
-print(f"last step: pass1 end -> pass2 start: {(b0 - a1) / 1e3:.2f} us")
+s1 = ctx.debug_stamps(4).astype(np.int64)
+s2 = ctx.debug_stamps(5).astype(np.int64)
+s1 = s1[s1[:, 0] > 0]
+s2 = s2[s2[:, 0] > 0]
+p1_end = s1[:, 7].max()
+print(f"last step: pass1 last CTA done -> pass2 median Z loads returned: {(np.median(s2[:, 8]) - p1_end) / 1e3:.2f} us, "
+      f"-> pass2 median zready: {(np.median(s2[:, 6]) - p1_end) / 1e3:.2f} us, -> pass2 median start {(np.median(s2[:, 0]) - p1_end) / 1e3:.2f} us")
 if "epilogue" in allst:
     e0, e1 = allst["epilogue"]
     print(f"epilogue(T-2) end -> pass1(T-1) start: {(a0 - e1) / 1e3:.2f} us")
