@@ -32,7 +32,8 @@
 namespace tcg {
 
 constexpr int KT1 = 32;      // training points per pass-1 stage
-constexpr int ST1 = 4;       // pass-1 A (ktilde) and B (R tile) ring stages
+constexpr int ST1 = 6;       // pass-1 ring stages: A (ktilde, in TMEM) and B (R tile, shared memory)
+constexpr int A1C = 32;      // TMEM columns of one A stage: hi (KT1 / 2 columns) | lo
 constexpr int AUXW = 20;     // floats of per-n side data per stage row
 constexpr int NT2 = 128;     // training points per pass-2 tile (the MMA N dimension)
 constexpr int KS2 = 64;      // j per pass-2 K slab (one pipeline stage)
@@ -399,12 +400,12 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
   const Geo& g = a.g;
   const int NZ = g.NZ;
   constexpr int NAUX = 2 * D + 1;
-  const size_t a_bytes = (size_t)128 * KT1 * 2;  // one fp16 A tile (hi or lo)
   const size_t b_bytes = (size_t)4 * NZ * KT1;   // B hi + lo of one tile
   const size_t x_bytes = (size_t)KT1 * AUXW * 4; // aux rows of one tile
-  uint8_t* asm_ = sm;                            // ST1 x (A hi | A lo)
-  uint8_t* bsm = asm_ + ST1 * 2 * a_bytes;       // ST1 x (B hi | B lo)
+  uint8_t* bsm = sm;                             // ST1 x (B hi | B lo)
   uint8_t* xsm = bsm + ST1 * b_bytes;            // STA x aux
+  // TMEM: the z accumulator in columns [0, NZ), then ST1 A stages of A1C columns
+  const uint32_t acol0 = (uint32_t)((NZ + 31) / 32 * 32);
   uint64_t* full_a = sh.full_a;
   uint64_t* empty_a = sh.empty_a;
   uint64_t* full_b = sh.full_b;
@@ -488,20 +489,19 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         tc::mbar_wait(&full_b[s], ph);
         tc::mbar_wait(&full_a[s], ph);
         tc::tc_fence_after();
-        const uint32_t abase = tc::smem_u32(asm_ + (size_t)s * 2 * a_bytes);
         const uint32_t bbase = tc::smem_u32(bsm + (size_t)s * b_bytes);
-        const uint64_t dahi = tc::umma_desc(abase, 128, SBO);
-        const uint64_t dalo = tc::umma_desc(abase + (uint32_t)a_bytes, 128, SBO);
+        const uint32_t ahi = tmem + acol0 + (uint32_t)(s * A1C), alo = ahi + (uint32_t)(KT1 / 2);
         const uint64_t dbhi = tc::umma_desc(bbase, 128, SBO);
         const uint64_t dblo = tc::umma_desc(bbase + (uint32_t)NZ * KT1 * 2u, 128, SBO);
         if (!(a.diag & 2)) {
 #pragma unroll
           for (int ks = 0; ks < KT1 / 16; ++ks) {
             const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
+            const uint32_t ac = (uint32_t)(ks * 8);  // 16 K elements = 8 TMEM columns
             const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
-            tc::mma_f16(tmem, dahi + o, dbhi + o, idesc, acc0);
-            tc::mma_f16(tmem, dahi + o, dblo + o, idesc, 1u);
-            tc::mma_f16(tmem, dalo + o, dbhi + o, idesc, 1u);
+            tc::mma_f16_ts(tmem, ahi + ac, dbhi + o, idesc, acc0);
+            tc::mma_f16_ts(tmem, ahi + ac, dblo + o, idesc, 1u);
+            tc::mma_f16_ts(tmem, alo + ac, dbhi + o, idesc, 1u);
           }
         }
         tc::umma_commit(&empty_a[s]);
@@ -514,9 +514,11 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     }
   } else {
     // ------------------------------------------------ ktilde generators (4 threads per row, 8 n each)
+    // warp w writes TMEM lane quarter w % 4, so row r = 32 (w % 4) + lane; qd = which 8 of the 32
     const int gt = tid - 32 * CTRL_WARPS;  // 0..511
-    const int r = gt % 128, qd = gt / 128;
+    const int r = (warp % 4) * 32 + lane, qd = (warp - CTRL_WARPS) / 4;
     const int row = row0 + r;
+    const uint32_t tlane = (uint32_t)((warp % 4) * 32) << 16;
     // exponent as (x*_c - X_nc) * kappa / l_c: difference first, then scale (4x smaller fp32
     // error in ktilde than scaling first, scripts/fp32_floor.py)
     float xq[D], sc[D];
@@ -533,8 +535,6 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
       const int s = i % ST1, x = i % STA;
       tc::mbar_wait(&full_x[x], (uint32_t)(i / STA) & 1u);             // aux rows of tile i landed
       tc::mbar_wait(&empty_a[s], ((uint32_t)(i / ST1) & 1u) ^ 1u);     // MMA done reading A[s]
-      __half* ahi = reinterpret_cast<__half*>(asm_ + (size_t)s * 2 * a_bytes);
-      __half* alo = ahi + 128 * KT1;
       const float* aux = reinterpret_cast<const float*>(xsm + (size_t)x * x_bytes);
       uint32_t hw[4], lw[4];
       if (!(a.diag & 1))
@@ -559,12 +559,16 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
       }
-      const int ci = tc::canon_idx(r, qd * 8, KT1);
-      *reinterpret_cast<uint4*>(ahi + ci) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      *reinterpret_cast<uint4*>(alo + ci) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-      // MEMBAR.CTA + proxy fence: the A stores are visible to the MMA, and every aux load above
-      // has returned before the aux stage is released (SYNCS.ARRIVE does not wait for pending LDS)
-      if (!(a.diag & 4)) tc::fence_proxy_async();
+      // A tile (row r, K pairs 4 qd .. 4 qd + 3) -> TMEM stage s, hi then lo
+      tc::tc_fence_after();
+      const uint32_t ta = tmem + tlane + acol0 + (uint32_t)(s * A1C + qd * 4);
+      tc::tmem_st4(ta, hw);
+      tc::tmem_st4(ta + (uint32_t)(KT1 / 2), lw);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      // MEMBAR.CTA: every aux load above has returned before the aux stage is released
+      // (SYNCS.ARRIVE does not wait for pending LDS)
+      if (!(a.diag & 4)) __threadfence_block();
       tc::mbar_arrive(&full_a[s]);
       tc::mbar_arrive(&empty_x[x]);
     }
@@ -774,7 +778,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   __shared__ P1Shared<D> sh;
   __shared__ uint32_t tmem_base;
   uint32_t ncols = 32;
-  while ((int)ncols < a.g.NZ) ncols <<= 1;
+  while ((int)ncols < (a.g.NZ + 31) / 32 * 32 + ST1 * A1C) ncols <<= 1;
   if (threadIdx.x / 32 == 1) tc::tmem_alloc(&tmem_base, ncols);
   tc::tc_fence_before();
   __syncthreads();
@@ -1314,7 +1318,9 @@ namespace {
 Geo geo_of(const bagel_ctx* c) { return make_geo(c->N, c->d, c->p, c->k); }
 
 size_t p1_smem(const Geo& g) {
-  return (size_t)ST1 * (2 * (size_t)128 * KT1 * 2 + (size_t)4 * g.NZ * KT1) + (size_t)STA * KT1 * AUXW * 4;
+  // B ring + aux ring; the FUSED tail parks a [128][NZ + 4] fp32 partial tile in the same memory
+  const size_t ring = (size_t)ST1 * ((size_t)4 * g.NZ * KT1) + (size_t)STA * KT1 * AUXW * 4;
+  return std::max(ring, (size_t)128 * (g.NZ + 4) * 4);
 }
 size_t p2_smem(const Geo& g) {
   (void)g;
