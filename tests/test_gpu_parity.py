@@ -422,3 +422,19 @@ def test_c3_wide_policy_subset(bagel):
     seed = W.rollout_seed(2)
     cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), "C3 subset")
+
+
+def test_c4_shape_four_outputs_rank_512(bagel):
+    """C4's shape at reduced N / B / T: hydraulic plant (p = 4 outputs, d = 5), rank 512 (two
+    z-column tiles in pass 1 -> the separate reduce kernels; two j tiles in pass 2), ragged B."""
+    wl = W.config("C4", N=2000, B=200, T=6)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    assert ctx.gp_kernel() == 1
+    xs = np.random.default_rng(21).uniform(-2, 2, (200, 5)).astype(np.float32)
+    out = ctx.gp_predict(torch.from_numpy(xs).cuda())
+    print("C4-shape worst error / tolerance:", _check_predict(wl, mdl, *out, xs.astype(np.float64)))
+    seed = W.rollout_seed(4)
+    cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), "C4 shape")
