@@ -129,9 +129,11 @@ __global__ void __launch_bounds__(32 * WARP_ROWS_BLOCK) k_epilogue(EpiArgs e, un
 //   delta_L  = xs-bar[p:] (1 - u^2);  delta_{l-1} = (W_l^T delta_l) (1 - h_l^2)
 //   xbar_t   = xbar_{t+1} + xs-bar[:p] + dphi/dx^T (W_0^T delta_0) + d(r_t / B)/dx_t
 // W (row-major, as theta) is staged in shared memory once per block; each step's tape row
-// (activations, A, x) is prefetched one step ahead with cp.async into a per-warp double buffer, so
-// the recursion itself only touches shared memory.
+// (activations, A, x) is prefetched three steps ahead with cp.async into a per-warp ring, so the
+// recursion itself only touches shared memory (one step of the chain is shorter than the tape's
+// HBM latency).
 constexpr int REV2_WARPS = 8;
+constexpr int REV2_RING = 4;  // tape-row buffers per warp: steps t .. t-3 in flight (prefetch distance 3)
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
@@ -150,11 +152,18 @@ __host__ __device__ inline int rev2_row_floats(const PolicyDesc& P, int p, int d
   return (P.act_ld + p * d + p + 3) & ~3;
 }
 __host__ __device__ inline int rev2_warp_floats(const PolicyDesc& P, int p, int d) {
-  return 2 * ((P.max_width + 3) & ~3) + 2 * rev2_row_floats(P, p, d);
+  return 2 * ((P.max_width + 3) & ~3) + REV2_RING * rev2_row_floats(P, p, d);
+}
+// Staged weights: every W_l transposed, Wt[i][o], rows padded to round4(out) + 4 floats (float4
+// reads of a row by consecutive lanes are bank-conflict free).
+__host__ __device__ inline int rev2_wt_ld(int out) { return ((out + 3) & ~3) + 4; }
+__host__ __device__ inline int rev2_wt_floats(const PolicyDesc& P) {
+  int n = 0;
+  for (int l = 0; l < P.n_layers; ++l) n += P.sizes[l] * rev2_wt_ld(P.sizes[l + 1]);
+  return n;
 }
 __host__ __device__ inline bool rev2_theta_staged(const PolicyDesc& P, int p, int d) {
-  return sizeof(float) * ((((size_t)P.n_params + 3) & ~(size_t)3) + (size_t)REV2_WARPS * rev2_warp_floats(P, p, d)) <=
-         200 * 1024;
+  return sizeof(float) * ((size_t)rev2_wt_floats(P) + (size_t)REV2_WARPS * rev2_warp_floats(P, p, d)) <= 200 * 1024;
 }
 
 template <int D, bool STAGED>
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     float* __restrict__ tape_delta, float invB) {
   extern __shared__ __align__(16) float sm[];
   constexpr bool staged = STAGED;  // (a compile-time choice: shared-memory W reads stay LDS)
-  const int np4 = staged ? (P.n_params + 3) & ~3 : 0;
+  const int np4 = staged ? rev2_wt_floats(P) : 0;
   const int RF = rev2_row_floats(P, p, D);
   const int mw4 = (P.max_width + 3) & ~3;
   const float* th_s = staged ? sm : theta;  // W row-major, as theta (global when too large)
@@ -172,8 +181,17 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
   float* d0 = sm + np4 + (size_t)w * rev2_warp_floats(P, p, D);  // this warp's region
   float* d1 = d0 + mw4;
   float* rows = d1 + mw4;  // 2 x RF: [act | A | x] of one step
-  if (staged)
-    for (int i = threadIdx.x; i < P.n_params; i += blockDim.x) sm[i] = __ldg(theta + i);
+  if (staged) {
+    int wo = 0;
+    for (int l = 0; l < P.n_layers; ++l) {
+      const int in = P.sizes[l], out = P.sizes[l + 1], ld = rev2_wt_ld(out);
+      for (int idx = threadIdx.x; idx < in * out; idx += blockDim.x) {
+        const int o = idx / in, i = idx % in;
+        sm[wo + i * ld + o] = __ldg(theta + P.w_off[l] + idx);
+      }
+      wo += in * ld;
+    }
+  }
   __syncthreads();
   const int b = blockIdx.x * REV2_WARPS + w;
   if (b >= B || T <= 0) return;  // warp-uniform
@@ -190,7 +208,10 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     if (lane < p) cp_async4(dst + AL + pd + lane, x + lane);
     cp_async_commit();
   };
-  prefetch(T - 1, rows);
+  for (int k = 0; k < REV2_RING - 1; ++k) {  // steps T-1, T-2, T-3 (empty groups past t = 0)
+    if (T - 1 - k >= 0) prefetch(T - 1 - k, rows + k * RF);
+    else cp_async_commit();
+  }
   const float gl = lane < p ? goals[(size_t)b * p + lane] : 0.0f;
   float xb = 0.0f;
   {
@@ -202,13 +223,10 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     if (lane < p) xb = invB * rr * rw.Q[lane] * (xT - gl) * inv_sr2;
   }
   for (int t = T - 1; t >= 0; --t) {
-    float* cur = rows + ((T - 1 - t) & 1) * RF;
-    if (t > 0) {
-      prefetch(t - 1, rows + ((T - t) & 1) * RF);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    float* cur = rows + ((T - 1 - t) % REV2_RING) * RF;
+    if (t - (REV2_RING - 1) >= 0) prefetch(t - (REV2_RING - 1), rows + ((T - 1 - t + REV2_RING - 1) % REV2_RING) * RF);
+    else cp_async_commit();
+    cp_async_wait<REV2_RING - 1>();  // step t's group (issued REV2_RING - 1 groups ago) has landed
     __syncwarp();
     const float* act = cur;
     const float* At = cur + AL;
@@ -231,12 +249,69 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     __syncwarp();
     float* dc = d0;
     float* dn = d1;
+    int wt_end = np4;  // staged layers are consumed last to first
     for (int l = L - 1; l >= 0; --l) {
       const int in = P.sizes[l], out = P.sizes[l + 1];
       const float* W = th_s + P.w_off[l];
       for (int o = lane; o < out; o += 32) dl[P.doff[l] + o] = dc[o];
       const float* hin = act + P.aoff[l];  // layer l's input activations
-      if (in >= 32) {
+      const int ld = rev2_wt_ld(out);
+      wt_end -= in * ld;
+      if (STAGED && in >= 32) {
+        // lanes over inputs, two inputs per pass; W^T rows and delta read as float4
+        const float* Wt = sm + wt_end;
+        const float4* dv = reinterpret_cast<const float4*>(dc);
+        for (int i = lane; i < in; i += 64) {
+          const bool two = i + 32 < in;
+          const int i2 = two ? i + 32 : i;
+          const float4* w1 = reinterpret_cast<const float4*>(Wt + (size_t)i * ld);
+          const float4* w2 = reinterpret_cast<const float4*>(Wt + (size_t)i2 * ld);
+          float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f;
+          const int n4 = out / 4;
+#pragma unroll 4
+          for (int o4 = 0; o4 < n4; ++o4) {
+            const float4 e = dv[o4], x = w1[o4], y = w2[o4];
+            a0 = fmaf(x.x, e.x, a0);
+            a1 = fmaf(x.y, e.y, a1);
+            a2 = fmaf(x.z, e.z, a2);
+            a3 = fmaf(x.w, e.w, a3);
+            c0 = fmaf(y.x, e.x, c0);
+            c1 = fmaf(y.y, e.y, c1);
+            c2 = fmaf(y.z, e.z, c2);
+            c3 = fmaf(y.w, e.w, c3);
+          }
+          for (int o = 4 * n4; o < out; ++o) {
+            a0 = fmaf(Wt[(size_t)i * ld + o], dc[o], a0);
+            c0 = fmaf(Wt[(size_t)i2 * ld + o], dc[o], c0);
+          }
+          const float hb = (a0 + a1) + (a2 + a3), hb2 = (c0 + c1) + (c2 + c3);
+          if (l > 0) {
+            const float h = hin[i];
+            dn[i] = hb * (1.0f - h * h);
+            if (two) {
+              const float h2 = hin[i2];
+              dn[i2] = hb2 * (1.0f - h2 * h2);
+            }
+          } else {
+            dn[i] = hb;
+            if (two) dn[i2] = hb2;
+          }
+        }
+      } else if (STAGED) {
+        // narrow input from the staged W^T: lane = (o group, i), xor-reduced (fixed tree)
+        const float* Wt = sm + wt_end;
+        int ip = 1;
+        while (ip < in) ip <<= 1;
+        const int ng = 32 / ip, i = lane % ip, grp = lane / ip;
+        float a = 0.0f;
+        if (i < in)
+          for (int o = grp; o < out; o += ng) a = fmaf(Wt[i * ld + o], dc[o], a);
+        for (int sh = 16; sh >= ip; sh >>= 1) a += __shfl_xor_sync(0xffffffffu, a, sh);
+        if (lane < in) {
+          const float h = l > 0 ? hin[lane] : 0.0f;
+          dn[lane] = l > 0 ? a * (1.0f - h * h) : a;
+        }
+      } else if (in >= 32) {
         // lanes over inputs, two inputs per pass, 4 o's per iteration (8 independent chains)
         for (int i = lane; i < in; i += 64) {
           const bool two = i + 32 < in;
@@ -492,7 +567,7 @@ size_t epi_smem(const PolicyDesc& P) { return sizeof(float) * EPI_ROWS * P.act_t
 }  // namespace
 
 size_t ro_reverse_smem(const PolicyDesc& P, int p, int d) {
-  return sizeof(float) * ((rev2_theta_staged(P, p, d) ? ((P.n_params + 3) & ~3) : 0) +
+  return sizeof(float) * ((rev2_theta_staged(P, p, d) ? (size_t)rev2_wt_floats(P) : 0) +
                           (size_t)REV2_WARPS * rev2_warp_floats(P, p, d));
 }
 // rows per staged chunk of the theta-gradient contraction: TG_KC, fewer for wide policies so the
