@@ -170,7 +170,7 @@ template <int D, bool STAGED>
 __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     PolicyDesc P, RewardDesc rw, int p, const float* __restrict__ theta, const float* __restrict__ goals, int B,
     int T, const float* __restrict__ tape_x, const float* __restrict__ tape_A, const float* __restrict__ tape_act,
-    float* __restrict__ tape_delta, float invB) {
+    float* __restrict__ tape_delta, float invB, unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(16) float sm[];
   constexpr bool staged = STAGED;  // (a compile-time choice: shared-memory W reads stay LDS)
   const int np4 = staged ? rev2_wt_floats(P) : 0;
@@ -223,11 +223,14 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     if (lane < p) xb = invB * rr * rw.Q[lane] * (xT - gl) * inv_sr2;
   }
   for (int t = T - 1; t >= 0; --t) {
+    const bool stampit = dbg && blockIdx.x == 0 && threadIdx.x == 0 && t == T / 2;
+    if (stampit) dbg[0] = gtimer_ro();
     float* cur = rows + ((T - 1 - t) % REV2_RING) * RF;
     if (t - (REV2_RING - 1) >= 0) prefetch(t - (REV2_RING - 1), rows + ((T - 1 - t + REV2_RING - 1) % REV2_RING) * RF);
     else cp_async_commit();
     cp_async_wait<REV2_RING - 1>();  // step t's group (issued REV2_RING - 1 groups ago) has landed
     __syncwarp();
+    if (stampit) dbg[1] = gtimer_ro();
     const float* act = cur;
     const float* At = cur + AL;
     const float xt = lane < p ? cur[AL + pd + lane] : 0.0f;
@@ -247,6 +250,7 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
       }
     }
     __syncwarp();
+    if (stampit) dbg[2] = gtimer_ro();
     float* dc = d0;
     float* dn = d1;
     int wt_end = np4;  // staged layers are consumed last to first
@@ -362,6 +366,7 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
         }
       }
       __syncwarp();
+      if (stampit) dbg[3 + (L - 1 - l)] = gtimer_ro();
       float* tmp = dc;
       dc = dn;
       dn = tmp;
@@ -377,6 +382,7 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     const float rr = expf(-qd * rw.inv_two_sr2);
     if (lane < p) xb += xs + hb_phi + invB * rr * rw.Q[lane] * (xt - gl) * inv_sr2;
     __syncwarp();
+    if (stampit) dbg[8] = gtimer_ro();
   }
 }
 
@@ -665,11 +671,11 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
   if (rev2_theta_staged(c->pol, c->gp.p, c->gp.d)) {
     DISPATCH_D(c->gp.d, (k_reverse2<D, true><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, smem, st>>>(
                             c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
-                            invB)));
+                            invB, c->tcs.dbg3)));
   } else {
     DISPATCH_D(c->gp.d, (k_reverse2<D, false><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, smem, st>>>(
                             c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
-                            invB)));
+                            invB, c->tcs.dbg3)));
   }
   *nblk_out = ro_theta_blocks(c, B, T);
   return 1;
