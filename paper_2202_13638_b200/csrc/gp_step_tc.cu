@@ -1000,7 +1000,7 @@ struct P2Args {
 // c * R + w, ... (R = ceil(B / CTAs)) -- the separate epilogue launch disappears.
 template <int D>
 struct P2Shared {
-  uint64_t zready, full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2], tempty[2], mma_done;
+  uint64_t zready[4], full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2], tempty[2], mma_done;
   float asum[3][128][1 + D];
 };
 
@@ -1016,7 +1016,7 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
   constexpr int NAUX = D + 1;
   constexpr size_t slab_bytes = (size_t)4 * NT2 * KS2;  // hi + lo of one slab
   constexpr size_t x_bytes = (size_t)NT2 * AUXW * 4;    // aux rows of one tile
-  uint64_t& zready = sh.zready;
+  uint64_t* zready = sh.zready;  // per K slab: that slab's Z columns are in TMEM
   uint64_t* full_s = sh.full_s;
   uint64_t* empty_s = sh.empty_s;
   uint64_t* full_x = sh.full_x;
@@ -1041,7 +1041,7 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
 
   if (tid == 0) stamp(a.dbg, 0);
   if (tid == 0) {
-    tc::mbar_init(&zready, 32 * GEN_WARPS);
+    for (int z = 0; z < 4; ++z) tc::mbar_init(&zready[z], 32 * GEN_WARPS);
     for (int s = 0; s < ST2; ++s) {
       tc::mbar_init(&full_s[s], 1);
       tc::mbar_init(&empty_s[s], 1);
@@ -1092,8 +1092,6 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
       const uint32_t idesc = tc::idesc_f16(128, NT2);
       constexpr uint32_t SBO = (KS2 / 8) * 128u;
       const uint32_t zhi = tmem + ZC, zlo = tmem + ZC + (uint32_t)(KJ / 2);
-      tc::mbar_wait(&zready, 0);
-      tc::tc_fence_after();
       stamp(a.dbg, 1);
       int q = 0;
       for (int i = 0; i < ntile; ++i) {
@@ -1103,6 +1101,7 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
         const uint32_t d = tmem + (uint32_t)(b * NT2);
         for (int sl = 0; sl < nsl; ++sl, ++q) {
           const int s = q % ST2;
+          if (i == 0) tc::mbar_wait(&zready[sl], 0);  // the first tile starts as Z arrives slab by slab
           tc::mbar_wait(&full_s[s], (uint32_t)(q / ST2) & 1u);
           tc::tc_fence_after();
           const uint32_t sb = tc::smem_u32(ssm + (size_t)s * slab_bytes);
@@ -1134,32 +1133,37 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
       // [group of 4 words][row][4 words] (see k_r1b_tc); this row's group gi is at zrow + gi * 128
       const uint4* zrow = reinterpret_cast<const uint4*>(
           a.Zp + (((size_t)m * cdiv_dev(a.B, 128) + rt) * g.njt + jt) * (size_t)128 * KJ * 2 * 2) + r;
-      // batches of 8 chunks: all loads of a batch are in flight before the first TMEM store
-      for (int base = cg * 8; base < KJ; base += 8 * 32) {
-        uint4 q[8][2];
+      // every load in flight first; then slab by slab (hi chunk sl, lo chunk nsl + sl of the
+      // 8-word chunks w0 = cg * 8 + 32 * chunk) into TMEM, releasing the MMA slab by slab
+      uint4 q[4][2][2];
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int w0 = base + it * 32;
-          if (w0 < KJ) {
-            // L2 loads (not the read-only path): in the persistent rollout kernel Z changes every step
-            q[it][0] = __ldcg(zrow + (size_t)(w0 / 4) * 128);
-            q[it][1] = __ldcg(zrow + (size_t)(w0 / 4 + 1) * 128);
-          }
-        }
-        if (tid == 32 * CTRL_WARPS && base == cg * 8) stamp(a.dbg, 8 + (q[0][0].x == 0x12345678u));
+      for (int sl = 0; sl < 4; ++sl) {
+        if (sl < nsl) {
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int w0 = base + it * 32;
-          if (w0 < KJ) {
-            const uint32_t v[8] = {q[it][0].x, q[it][0].y, q[it][0].z, q[it][0].w,
-                                   q[it][1].x, q[it][1].y, q[it][1].z, q[it][1].w};
-            tc::tmem_st8(tmem + ((uint32_t)(quarter * 32) << 16) + ZC + (uint32_t)w0, v);
+          for (int h = 0; h < 2; ++h) {
+            const int w0 = cg * 8 + (h ? nsl + sl : sl) * 32;
+            // L2 loads (not the read-only path): Z is rewritten every step
+            q[sl][h][0] = __ldcg(zrow + (size_t)(w0 / 4) * 128);
+            q[sl][h][1] = __ldcg(zrow + (size_t)(w0 / 4 + 1) * 128);
           }
         }
       }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&zready);
+      if (tid == 32 * CTRL_WARPS) stamp(a.dbg, 8 + (q[0][0][0].x == 0x12345678u));
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        if (sl < nsl) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int w0 = cg * 8 + (h ? nsl + sl : sl) * 32;
+            const uint32_t v[8] = {q[sl][h][0].x, q[sl][h][0].y, q[sl][h][0].z, q[sl][h][0].w,
+                                   q[sl][h][1].x, q[sl][h][1].y, q[sl][h][1].z, q[sl][h][1].w};
+            tc::tmem_st8(tmem + ((uint32_t)(quarter * 32) << 16) + ZC + (uint32_t)w0, v);
+          }
+          tc::tmem_st_wait();
+          tc::tc_fence_before();
+          tc::mbar_arrive(&zready[sl]);
+        }
+      }
       if (tid == 32 * CTRL_WARPS) stamp(a.dbg, 6);
     }
     // ------------------------------------------------ epilogue: sum_n (s w_n) ktilde_n [1 | X_n]
@@ -1235,7 +1239,7 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
   __syncthreads();
   if (tid == 0) {
     stamp(a.dbg, 5);
-    tc::mbar_inval(&zready);
+    for (int z = 0; z < 4; ++z) tc::mbar_inval(&zready[z]);
     for (int s = 0; s < ST2; ++s) {
       tc::mbar_inval(&full_s[s]);
       tc::mbar_inval(&empty_s[s]);
