@@ -147,7 +147,7 @@ void free_workspace(bagel_ctx* c) {
   Workspace& w = c->ws;
   dev_free(w.xstar); dev_free(w.P1); dev_free(w.Z); dev_free(w.P2); dev_free(w.mu); dev_free(w.var);
   dev_free(w.tape_x); dev_free(w.tape_sig); dev_free(w.tape_jmu); dev_free(w.tape_jv); dev_free(w.G);
-  dev_free(w.tape_A); dev_free(w.tape_act); dev_free(w.tape_delta);
+  dev_free(w.tape_A); dev_free(w.tape_act); dev_free(w.tape_delta); dev_free(w.xbar);
   w.tape_pol_cap = 0;
   dev_free(w.theta_part); dev_free(w.grad_tmp); dev_free(w.thetaT); dev_free(w.cost_dev); dev_free(w.err_flag);
   dev_free(c->tcs.P1z); dev_free(c->tcs.P1h); dev_free(c->tcs.Zp); dev_free(c->tcs.zrow_inv);
@@ -217,6 +217,7 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
     dev_alloc(c, w.tape_jmu, Ts * Bs * p * d);
     dev_alloc(c, w.tape_jv, Ts * Bs * p * d);
     dev_alloc(c, w.tape_A, Ts * Bs * p * d);
+    dev_alloc(c, w.xbar, Bs * p);
     dev_alloc(c, w.G, Bs);
     dev_alloc(c, w.cost_dev, 1);
     dev_alloc(c, w.err_flag, 1);

@@ -76,6 +76,7 @@ struct EpiArgs {
   int* err_flag;
   float* trace_mu;       // nullable, T x B x p
   float* trace_var;      // nullable, T x B x p
+  int policy_external;   // 1: the next action is computed by mlp_forward_step (wide policies)
 };
 
 // Tensor-core (tcgen05) path state: packed operand tiles (cache-build time) and
@@ -122,6 +123,7 @@ struct Workspace {
   float* tape_act = nullptr;
   float* tape_delta = nullptr;
   size_t tape_pol_cap = 0;      // rows (T x B) the activation / delta tapes hold
+  float* xbar = nullptr;        // B x p adjoint state (tiled reverse of wide policies)
   double* G = nullptr;      // B returns
   float* theta_part = nullptr;  // nblk x n_params reverse partials
   int theta_part_cap = 0;
@@ -241,6 +243,10 @@ int ro_philox_raw(const uint32_t* ctr, uint32_t k0, uint32_t k1, int n, uint32_t
 int ro_philox_normals(uint64_t seed, long long traj_offset, int B, int T, int p, float* out,
                       cudaStream_t st);
 int ro_theta_blocks(const bagel_ctx* c, int B, int T);
+bool ro_wide_policy(const PolicyDesc& P);
+int mlp_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st);
+int mlp_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B, int T, long long B_global,
+                cudaStream_t st);
 int ro_theta_grad(const bagel_ctx* c, int B, int T, int nblk, cudaStream_t st);
 size_t ro_theta_grad_smem(const PolicyDesc& P);
 

@@ -227,7 +227,7 @@ __device__ void epi_post(const EpiArgs& e, const int t, int b0, int nr, const fl
   __syncwarp();
   const float* gb = e.goals + (size_t)b0 * p;
   if (lane < nr) e.G[b0 + lane] += (double)reward_fn(e.rw, &sc.xn_s[lane * p], gb + lane * p, p);
-  if (!policy_next) return;
+  if (!policy_next || e.policy_external) return;
   warp_policy<R>(e.P, p, th_s, sc.xn_s, gb, nr, buf, sc.us, e.tape_act + ((size_t)(t + 1) * B + b0) * e.P.act_ld);
   for (int i = lane; i < nr * D; i += 32) {
     const int r = i / D, c = i % D;

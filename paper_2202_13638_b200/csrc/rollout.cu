@@ -653,12 +653,16 @@ EpiArgs ro_epi_args(const bagel_ctx* c, const float* goals, int B, int t, int T,
 
 int ro_step_epilogue(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, int T,
                      uint64_t seed, long long traj_offset, float* trace_mu, float* trace_var, cudaStream_t st) {
-  (void)theta;
-  const EpiArgs e = ro_epi_args(c, goals, B, t, T, seed, traj_offset, trace_mu, trace_var);
+  EpiArgs e = ro_epi_args(c, goals, B, t, T, seed, traj_offset, trace_mu, trace_var);
+  const bool wide = ro_wide_policy(c->pol);
+  e.policy_external = wide ? 1 : 0;
   DISPATCH_D(c->gp.d, (k_epilogue<D><<<cdiv(B, ROWS_BLOCK), 32 * WARP_ROWS_BLOCK, policy_smem(c->pol), st>>>(
                           e, t == T - 2 ? c->tcs.dbg3 : nullptr)));
+  if (wide && t + 1 < T) return 1 + mlp_forward_step(c, theta, goals, B, t + 1, st);  // tiled a1 of step t + 1
   return 1;
 }
+
+bool ro_wide_policy(const PolicyDesc& P) { return !policy_theta_staged(P); }
 
 int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B, int T, uint64_t seed,
                long long traj_offset, long long B_global, int* nblk_out, cudaStream_t st) {
@@ -666,6 +670,10 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
   (void)traj_offset;
   ro_set_attributes();
   const Workspace& w = c->ws;
+  if (ro_wide_policy(c->pol)) {  // register-tiled GEMM steps (mlp_tiled.cu)
+    *nblk_out = ro_theta_blocks(c, B, T);
+    return T > 0 ? mlp_reverse(c, theta, goals, B, T, B_global, st) : 0;
+  }
   const size_t smem = ro_reverse_smem(c->pol, c->gp.p, c->gp.d);
   const float invB = (float)(1.0 / (double)B_global);
   if (rev2_theta_staged(c->pol, c->gp.p, c->gp.d)) {
