@@ -135,6 +135,36 @@ int rollout_cost_and_grad(bagel_ctx* ctx, const float* policy_params, const floa
                           const float* goals, int B, int T, uint64_t seed, long long traj_offset,
                           long long B_global, double* mean_cost, float* grad);
 
+/* ------------------------------------- Algorithm 1 around the hot path (NEXT-2) */
+
+/* bagel_sample_states -- "Sample batch of initial states S_0" (Alg.1) and
+ * goal-conditioned goals "sampled according to a distribution", uniform
+ * within the data bounds:
+ *   out[b][m] = lo[m] + (hi[m] - lo[m]) u,  u = ((o >> 9) + 0.5) 2^-23 (R29),
+ *   o = Philox4x32-10(key = (seed lo, seed hi),
+ *                     ctr = (traj_offset + b, 0, m >> 2, 2 + which))[m & 3].
+ *   which = 0 draws S_0, 1 draws G (disjoint streams; the rollout noise uses ctr
+ *   word 3 = 0).  lo, hi [host] p floats; out [dev] B x p.  Asynchronous.
+ * Errors: E_ARG (B < 1, p not in [1, 4], which not in {0, 1}, lo > hi or
+ * non-finite bounds, out not device memory, traj_offset + B >= 2^32). */
+int bagel_sample_states(bagel_ctx* ctx, uint64_t seed, long long traj_offset, int B, int p, int which,
+                        const float* lo, const float* hi, float* out);
+
+/* policy_adam_step -- "Update theta via gradient descent" (Alg.1) with
+ * Adam ("for which we will use Adam"; lr 1e-2), bias-corrected
+ * (Kingma & Ba Alg.1), elementwise on n floats:
+ *   m1 = b1 m1 + (1 - b1) g;  m2 = b2 m2 + (1 - b2) g^2;
+ *   params -= lr (m1 / (1 - b1^step)) / (sqrt(m2 / (1 - b2^step)) + eps).
+ * params, m1, m2 [dev] n floats updated in place (m1 = m2 = 0 before step 1);
+ * grad [dev] n floats; step >= 1 counts updates (the caller increments it).
+ * If any grad entry is non-finite, nothing is updated and *skipped = 1.
+ * skipped [host, nullable]: when non-NULL the call synchronises the stream and
+ * reports; when NULL the update is only enqueued.
+ * Errors: E_ARG (n < 1, step < 1, lr < 0, beta outside [0, 1), eps <= 0,
+ * non-device arrays). */
+int policy_adam_step(bagel_ctx* ctx, float* params, const float* grad, float* m1, float* m2, int n,
+                     long long step, float lr, float beta1, float beta2, float eps, int* skipped);
+
 /* Number of kernel launches the last rollout_cost_and_grad enqueued (host int). */
 int bagel_last_launch_count(const bagel_ctx* ctx, int* launches);
 

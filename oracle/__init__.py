@@ -81,6 +81,10 @@ def lib():
                                       C.c_int, C.c_int, C.c_uint64, C.c_longlong, C.c_longlong,
                                       C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_uint64]
             L.orc_rollout.restype = C.c_int
+            L.orc_sample_states.argtypes = [C.c_uint64, C.c_longlong, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
+            L.orc_adam_step.argtypes = [_dp, _dp, _dp, _dp, C.c_int, C.c_longlong, C.c_double, C.c_double,
+                                        C.c_double, C.c_double]
+            L.orc_adam_step.restype = C.c_int
             L.orc_num_threads.restype = C.c_int
             L.orc_set_num_threads.argtypes = [C.c_int]
             _lib = L
@@ -244,6 +248,43 @@ def rollout(model: Model, sizes, phi_mode, theta, Q, sigma_r, x0, goals, T, seed
     if trace:
         out.update(x=tx, mu=tm, var=tv)
     return out
+
+
+# ---------------------------------------------------------------- Algorithm 1 around the path
+def sample_states(seed: int, traj_offset: int, B: int, lo, hi, which: int = 0) -> np.ndarray:
+    """S_0 (which = 0) / goals (which = 1): uniform within [lo, hi] per column."""
+    lo, hi = _d(lo).reshape(-1), _d(hi).reshape(-1)
+    p = lo.shape[0]
+    out = np.zeros((B, p))
+    lib().orc_sample_states(int(seed) & 0xFFFFFFFFFFFFFFFF, int(traj_offset), int(B), p, int(which), _ptr(lo),
+                            _ptr(hi), _ptr(out))
+    return out
+
+
+def adam_step(theta, g, m1, m2, t: int, lr=1e-2, b1=0.9, b2=0.999, eps=1e-8) -> bool:
+    """In-place bias-corrected Adam on float64 arrays.  True if skipped (non-finite g)."""
+    for a in (theta, g, m1, m2):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    return bool(lib().orc_adam_step(_ptr(theta), _ptr(g), _ptr(m1), _ptr(m2), theta.shape[0], int(t), float(lr),
+                                    float(b1), float(b2), float(eps)))
+
+
+def train(model: Model, sizes, phi_mode, theta0, Q, sigma_r, T, iters, B, lo, hi, seed0, lr=1e-2,
+          x0=None, goals=None):
+    """Algorithm 1's inner loop: per iteration i (seed0 + i) sample S_0 and G (unless fixed,
+    P:144), rollout cost and gradient, Adam.  Returns (theta, [cost_i])."""
+    theta = _d(theta0).copy()
+    m1, m2 = np.zeros_like(theta), np.zeros_like(theta)
+    costs, t = [], 0
+    for i in range(iters):
+        seed = seed0 + i
+        xs = _d(x0) if x0 is not None else sample_states(seed, 0, B, lo, hi, 0)
+        gs = _d(goals) if goals is not None else sample_states(seed, 0, B, lo, hi, 1)
+        out = rollout(model, sizes, phi_mode, theta, Q, sigma_r, xs, gs, T, seed)
+        costs.append(out["cost"])
+        if not adam_step(theta, out["grad"], m1, m2, t + 1, lr):
+            t += 1
+    return theta, costs
 
 
 def num_threads() -> int:

@@ -724,3 +724,50 @@ void orc_set_num_threads(int n)
     (void)n;
 #endif
 }
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 1 around the hot path            */
+/* ------------------------------------------------------------------ */
+
+/* "Sample batch of initial states S_0" (Alg.1) and goals "sampled
+ * according to a distribution", uniform within the data bounds
+ * (P:180): out[b][m] = lo[m] + (hi[m] - lo[m]) u with u the 23-bit uniform of
+ * Philox4x32-10(key = seed, ctr = (traj_offset + b, 0, m >> 2, 2 + which))[m & 3]
+ * (which = 0: S_0, 1: G).  Counter convention: DESIGN.md "Philox". */
+void orc_sample_states(uint64_t seed, long long traj_offset, int B, int p, int which,
+                       const double* lo, const double* hi, double* out)
+{
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    for (int b = 0; b < B; ++b) {
+        for (int m = 0; m < p; ++m) {
+            uint32_t ctr[4] = {(uint32_t)(traj_offset + b), 0u, (uint32_t)(m >> 2), 2u + (uint32_t)which};
+            uint32_t o[4];
+            orc_philox4x32_10(ctr, key, o);
+            double u = orc_uniform(o[m & 3]);
+            out[(size_t)b * p + m] = lo[m] + (hi[m] - lo[m]) * u;
+        }
+    }
+}
+
+/* Adam (Kingma & Ba 2015, Algorithm 1; "for which we will use Adam", P:144;
+ * SPEC S:399-403), bias-corrected, step t >= 1:
+ *   m1 <- b1 m1 + (1 - b1) g;  m2 <- b2 m2 + (1 - b2) g^2
+ *   m1hat = m1 / (1 - b1^t);   m2hat = m2 / (1 - b2^t)
+ *   theta <- theta - lr m1hat / (sqrt(m2hat) + eps)
+ * Returns 1 (and changes nothing) if any gradient entry is non-finite. */
+int orc_adam_step(double* theta, const double* g, double* m1, double* m2, int n, long long t,
+                  double lr, double b1, double b2, double eps)
+{
+    for (int i = 0; i < n; ++i)
+        if (!isfinite(g[i])) return 1;
+    double bc1 = 1.0 - pow(b1, (double)t);
+    double bc2 = 1.0 - pow(b2, (double)t);
+    for (int i = 0; i < n; ++i) {
+        m1[i] = b1 * m1[i] + (1.0 - b1) * g[i];
+        m2[i] = b2 * m2[i] + (1.0 - b2) * g[i] * g[i];
+        double m1hat = m1[i] / bc1;
+        double m2hat = m2[i] / bc2;
+        theta[i] -= lr * m1hat / (sqrt(m2hat) + eps);
+    }
+    return 0;
+}

@@ -65,6 +65,10 @@ def lib() -> C.CDLL:
             L.bagel_debug_buffer.argtypes = [_vp, C.c_int, _vp, C.c_size_t]
             L.bagel_debug_trace.argtypes = [_vp, C.c_int]
             L.bagel_get_gp_kernel.argtypes = [_vp, C.POINTER(C.c_int)]
+            L.bagel_sample_states.argtypes = [_vp, C.c_uint64, C.c_longlong, C.c_int, C.c_int, C.c_int,
+                                              C.POINTER(C.c_float), C.POINTER(C.c_float), _vp]
+            L.policy_adam_step.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_longlong, C.c_float, C.c_float,
+                                           C.c_float, C.c_float, C.POINTER(C.c_int)]
             _lib = L
     return _lib
 
@@ -74,7 +78,7 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
            "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench",
-           "bagel_debug_buffer", "bagel_debug_trace"]
+           "bagel_debug_buffer", "bagel_debug_trace", "bagel_sample_states", "policy_adam_step"]
 
 PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce", "theta_grad"]
 
@@ -171,6 +175,29 @@ class Context:
                                                  int(seed) & 0xFFFFFFFFFFFFFFFF, int(traj_offset), int(B_global),
                                                  C.byref(cost), _ptr(grad)))
         return cost.value, grad
+
+    # ------------------------------------------------------------ Algorithm 1 around the path
+    def sample_states(self, seed: int, traj_offset: int, B: int, lo, hi, which: int = 0, out=None):
+        """S_0 (which = 0) or goals (which = 1) uniform in [lo, hi] per state column."""
+        lo = np.ascontiguousarray(lo, dtype=np.float32).reshape(-1)
+        hi = np.ascontiguousarray(hi, dtype=np.float32).reshape(-1)
+        p = lo.shape[0]
+        if out is None:
+            out = torch.empty(B, p, dtype=torch.float32, device=self.dev)
+        fp = C.POINTER(C.c_float)
+        self._check(self.L.bagel_sample_states(self.h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(traj_offset), int(B), p,
+                                               int(which), lo.ctypes.data_as(fp), hi.ctypes.data_as(fp), _ptr(out)))
+        return out
+
+    def adam_step(self, params, grad, m1, m2, step: int, lr: float = 1e-2, beta1: float = 0.9,
+                  beta2: float = 0.999, eps: float = 1e-8, report_skip: bool = False):
+        """In-place Adam update of device tensors.  Returns True if the update was skipped
+        because of a non-finite gradient (only when report_skip, which synchronises)."""
+        sk = C.c_int(0)
+        self._check(self.L.policy_adam_step(self.h, _ptr(params), _ptr(grad), _ptr(m1), _ptr(m2), int(params.numel()),
+                                            int(step), float(lr), float(beta1), float(beta2), float(eps),
+                                            C.byref(sk) if report_skip else None))
+        return bool(sk.value)
 
     def last_launch_count(self) -> int:
         n = C.c_int(0)

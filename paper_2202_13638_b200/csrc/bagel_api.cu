@@ -405,6 +405,8 @@ extern "C" int bagel_destroy(bagel_ctx* c) {
   dev_free(c->X);
   dev_free(c->Y);
   dev_free(c->ws.stage);
+  dev_free(c->op_flag);
+  dev_free(c->op_bounds);
   delete c;
   return BAGEL_OK;
 }
@@ -903,6 +905,57 @@ extern "C" int bagel_debug_trace(bagel_ctx* c, int enable) {
       dev_alloc(c, c->tcs.dbg2, (size_t)16 * 4096);
       CK(cudaMemsetAsync(c->tcs.dbg1, 0, 16 * 4096 * sizeof(unsigned long long), c->stream));
       CK(cudaMemsetAsync(c->tcs.dbg2, 0, 16 * 4096 * sizeof(unsigned long long), c->stream));
+    }
+  });
+}
+
+// ------------------------------------------------------------ Algorithm 1 around the hot path
+extern "C" int bagel_sample_states(bagel_ctx* c, uint64_t seed, long long traj_offset, int B, int p, int which,
+                                   const float* lo, const float* hi, float* out) {
+  return guarded(c, [&] {
+    REQUIRE(lo && hi && out, BAGEL_E_ARG, "bagel_sample_states: NULL argument");
+    REQUIRE(B >= 1 && p >= 1 && p <= BAGEL_MAX_P && (which == 0 || which == 1), BAGEL_E_ARG,
+            "bagel_sample_states: need B >= 1, 1 <= p <= %d, which in {0, 1} (B=%d, p=%d, which=%d)", BAGEL_MAX_P, B,
+            p, which);
+    REQUIRE(traj_offset >= 0 && traj_offset + B <= 0xffffffffLL, BAGEL_E_ARG,
+            "bagel_sample_states: need 0 <= traj_offset, traj_offset + B < 2^32");
+    REQUIRE(is_device_ptr(out), BAGEL_E_ARG, "bagel_sample_states: out must be device memory");
+    float hb[2 * BAGEL_MAX_P];
+    for (int m = 0; m < p; ++m) {
+      REQUIRE(isfinite(lo[m]) && isfinite(hi[m]) && lo[m] <= hi[m], BAGEL_E_ARG,
+              "bagel_sample_states: bounds[%d] = [%g, %g] must be finite with lo <= hi", m, (double)lo[m], (double)hi[m]);
+      hb[m] = lo[m];
+      hb[BAGEL_MAX_P + m] = hi[m];
+    }
+    if (!c->op_bounds) dev_alloc(c, c->op_bounds, 2 * BAGEL_MAX_P);
+    CK(cudaMemcpyAsync(c->op_bounds, hb, sizeof hb, cudaMemcpyHostToDevice, c->stream));
+    op_sample_uniform(seed, traj_offset, B, p, which, c->op_bounds, c->op_bounds + BAGEL_MAX_P, out, c->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+extern "C" int policy_adam_step(bagel_ctx* c, float* params, const float* grad, float* m1, float* m2, int n,
+                                long long step, float lr, float beta1, float beta2, float eps, int* skipped) {
+  return guarded(c, [&] {
+    REQUIRE(params && grad && m1 && m2, BAGEL_E_ARG, "policy_adam_step: NULL array argument");
+    REQUIRE(n >= 1 && step >= 1, BAGEL_E_ARG, "policy_adam_step: need n >= 1 and step >= 1 (n=%d, step=%lld)", n, step);
+    REQUIRE(isfinite(lr) && lr >= 0.0f && beta1 >= 0.0f && beta1 < 1.0f && beta2 >= 0.0f && beta2 < 1.0f &&
+                isfinite(eps) && eps > 0.0f,
+            BAGEL_E_ARG, "policy_adam_step: need lr >= 0, 0 <= beta1, beta2 < 1, eps > 0 (lr=%g b1=%g b2=%g eps=%g)",
+            (double)lr, (double)beta1, (double)beta2, (double)eps);
+    REQUIRE(is_device_ptr(params) && is_device_ptr(grad) && is_device_ptr(m1) && is_device_ptr(m2), BAGEL_E_ARG,
+            "policy_adam_step: params, grad, m1 and m2 must be device memory");
+    if (!c->op_flag) dev_alloc(c, c->op_flag, 1);
+    // bias corrections in float64 on the host, rounded once
+    const float bc1 = (float)(1.0 - pow((double)beta1, (double)step));
+    const float bc2 = (float)(1.0 - pow((double)beta2, (double)step));
+    op_adam(params, grad, m1, m2, n, lr, beta1, beta2, eps, bc1, bc2, c->op_flag, c->stream);
+    CK(cudaGetLastError());
+    if (skipped) {
+      int f = 0;
+      CK(cudaMemcpyAsync(&f, c->op_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      *skipped = f;
     }
   });
 }

@@ -159,6 +159,8 @@ struct bagel_ctx {
   RewardDesc rw{};
   Workspace ws;
   TcState tcs;
+  int* op_flag = nullptr;     // Adam skip flag (device int, optim.cu)
+  float* op_bounds = nullptr; // 2 x MAX_P sampling bounds (lo | hi)
   int gp_kernel = 1;  // 1: tcgen05 path (default), 0: v0 FFMA path (reference / A-B tests)
   int last_launches = 0;
   int num_sms = 148;
@@ -256,6 +258,10 @@ size_t tc_tiles1_bytes(const bagel_ctx* c);
 size_t tc_tiles2_bytes(const bagel_ctx* c);
 int tc_pack(bagel_ctx* c, int m, cudaStream_t st);
 void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2, int* p1_fused);
+int op_sample_uniform(uint64_t seed, long long traj_offset, int B, int p, int which, const float* lo,
+                      const float* hi, float* out, cudaStream_t st);
+int op_adam(float* theta, const float* g, float* m1, float* m2, int n, float lr, float b1, float b2, float eps,
+            float bc1, float bc2, int* flag, cudaStream_t st);
 size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1);
 size_t tc_zp_bytes(const bagel_ctx* c, int B);
 int tc_njt(const bagel_ctx* c);

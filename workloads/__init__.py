@@ -205,7 +205,7 @@ def make_dataset(plant: str, N: int, seed: int = 0):
 
 def make_workload(name: str = "custom", plant: str = "boom", N: int = 5000, rank: int = 256,
                   hidden=(64, 64), B: int = 1024, T: int = 100, phi_mode: str = "xg",
-                  data_seed: int = 0) -> Workload:
+                  data_seed: int = 0, fixed_start: bool = False) -> Workload:
     """Build a workload.  phi_mode 'xg' -> policy input [x, g] (in = 2p);
     'xgd' -> [x, g, g - x] (in = 3p, C1)."""
     X, Y, ell, s, noise, norm = make_dataset(plant, N, data_seed)
@@ -216,9 +216,10 @@ def make_workload(name: str = "custom", plant: str = "boom", N: int = 5000, rank
     wl = Workload(name=name, plant=plant, N=N, p=p, q=q, rank=rank, sizes=sizes, B=B, T=T,
                   X=X, Y=Y, ell=ell, s=s, noise=noise,
                   Q=np.asarray(Q_DIAG[plant], dtype=np.float32))
-    if name == "C1":
-        # Exp. 1: all rows start at the same state, single fixed goal.
-        x0 = ((-0.8 - norm["mu"][:p]) / norm["sd"][:p]).astype(np.float32)
+    if fixed_start or name == "C1":
+        # Exp. 1: all rows start at the same state ("a low angle": -0.8 rad, at rest), single
+        # fixed goal r(., -mu_X / sigma_X), i.e. 0 rad (and 0 rad/s) in normalised units.
+        x0 = ((np.array([-0.8, 0.0, 0.0, 0.0])[:p] - norm["mu"][:p]) / norm["sd"][:p]).astype(np.float32)
         g = ((0.0 - norm["mu"][:p]) / norm["sd"][:p]).astype(np.float32)
         wl.x0 = np.tile(x0, (B, 1)).astype(np.float32)
         wl.goals = np.tile(g, (B, 1)).astype(np.float32)
@@ -244,6 +245,9 @@ CONFIGS = {
     "C3": dict(plant="boom", N=5000, rank=256, hidden=(256, 256, 256), B=4096, T=500, phi_mode="xg"),
     "C4": dict(plant="hydraulic4", N=20000, rank=512, hidden=(64, 64), B=8192, T=200, phi_mode="xg"),
     "C5": dict(plant="boom", N=50000, rank=512, hidden=(64, 64), B=65536, T=200, phi_mode="xg"),
+    # the paper's Exp. 1 shape: n = 2200, b = 100, H = 300, policy [8, 8], fixed start and
+    # goal; LOVE rank unstated -> 100 (GPyTorch's default root-decomposition size, reading R32)
+    "E1": dict(plant="boom", N=2200, rank=100, hidden=(8, 8), B=100, T=300, phi_mode="xg", fixed_start=True),
 }
 
 
