@@ -165,6 +165,25 @@ int bagel_sample_states(bagel_ctx* ctx, uint64_t seed, long long traj_offset, in
 int policy_adam_step(bagel_ctx* ctx, float* params, const float* grad, float* m1, float* m2, int n,
                      long long step, float lr, float beta1, float beta2, float eps, int* skipped);
 
+/* gp_log_marginal_likelihood -- "Learn GP transition dynamics using D" (Alg.1
+ * P:98): the exact log marginal likelihood of output GP m and its gradient in
+ * the log-hyperparameters (Eq.5-6, reading R33 -- Eq.5 is written up
+ * to a factor 2 and a constant, Eq.6 is garbled):
+ *   log p(y_m | X, phi) = -1/2 y^T Khat^-1 y - 1/2 log|Khat| - N/2 log(2 pi),
+ *   d/dphi_j = 1/2 tr((alpha alpha^T - Khat^-1) dKhat/dphi_j),  alpha = Khat^-1 y,
+ * phi = [log l_1 .. log l_d, log s, log sigma_n^2] ("Adam on
+ * log-parameters"), computed in float64 on the GPU (Cholesky, triangular
+ * inverse, Khat^-1 formed tile by tile inside the gradient reduction).
+ *   m        output index in [0, p); uses the X and column m of y of gp_load.
+ *   log_hyp  [host, nullable] d + 2 doubles; NULL = the hyperparameters of gp_load.
+ *   mll      [host] receives the log marginal likelihood.
+ *   grad     [host, nullable] d + 2 doubles; NULL skips the gradient (O(N^3) less).
+ * Synchronous.  Workspace 2 N^2 float64 (kept for the next call at the same N).
+ * Does not change the loaded model or its LOVE cache.
+ * Errors: E_STATE without gp_load; E_ARG (m out of range, non-finite log_hyp,
+ * noise < 1e-8, workspace > 120 GB); E_NUMERIC if a Cholesky pivot <= 0; E_CUDA. */
+int gp_log_marginal_likelihood(bagel_ctx* ctx, int m, const double* log_hyp, double* mll, double* grad);
+
 /* Number of kernel launches the last rollout_cost_and_grad enqueued (host int). */
 int bagel_last_launch_count(const bagel_ctx* ctx, int* launches);
 

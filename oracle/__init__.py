@@ -85,6 +85,8 @@ def lib():
             L.orc_adam_step.argtypes = [_dp, _dp, _dp, _dp, C.c_int, C.c_longlong, C.c_double, C.c_double,
                                         C.c_double, C.c_double]
             L.orc_adam_step.restype = C.c_int
+            L.orc_mll.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, _dp, _dp]
+            L.orc_mll.restype = C.c_int
             L.orc_num_threads.restype = C.c_int
             L.orc_set_num_threads.argtypes = [C.c_int]
             _lib = L
@@ -248,6 +250,19 @@ def rollout(model: Model, sizes, phi_mode, theta, Q, sigma_r, x0, goals, T, seed
     if trace:
         out.update(x=tx, mu=tm, var=tv)
     return out
+
+
+def log_marginal_likelihood(X, y, log_hyp, want_grad=True):
+    """(log p(y | X, phi), d/dphi) with phi = [log l (d) | log s | log sn2] (Eq.5-6, reading R33)."""
+    X, y, h = _d(X), _d(y).reshape(-1), _d(log_hyp).reshape(-1)
+    N, d = X.shape
+    assert h.shape == (d + 2,) and y.shape == (N,)
+    val = C.c_double(0.0)
+    g = np.zeros(d + 2) if want_grad else None
+    rc = lib().orc_mll(_ptr(X), N, d, _ptr(y), _ptr(h), C.byref(val), _ptr(g))
+    if rc != 0:
+        raise ArithmeticError(f"oracle Cholesky failed at pivot {rc - 1}")
+    return val.value, g
 
 
 # ---------------------------------------------------------------- Algorithm 1 around the path

@@ -771,3 +771,93 @@ int orc_adam_step(double* theta, const double* g, double* m1, double* m2, int n,
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* GP hyperparameter learning                 */
+/* ------------------------------------------------------------------ */
+
+/* Exact log marginal likelihood of one output GP and its gradient in the
+ * log-hyperparameters phi = [log l_1..log l_d, log s, log sigma_n^2]
+ * ("learned by maximizing the log marginal likelihood", Eq.5-6, P:77-80;
+ * Eq.5 is stated up to a factor 2 and a constant and Eq.6 is garbled, so the
+ * oracle writes out the standard definitions, reading R33):
+ *   log p(y|X,phi) = -1/2 y^T Khat^-1 y - 1/2 log|Khat| - N/2 log(2 pi)
+ *   d/dphi_j       =  1/2 y^T Khat^-1 (dKhat/dphi_j) Khat^-1 y
+ *                   - 1/2 tr(Khat^-1 dKhat/dphi_j)
+ *   dKhat_ij/dlog l_c = K_ij (x_ic - x_jc)^2 / l_c^2,  dKhat/dlog s = K,
+ *   dKhat/dlog sigma_n^2 = sigma_n^2 I.
+ * Plain steps: dense Khat, Cholesky, alpha by two triangular solves, log|Khat|
+ * = 2 sum log L_ii, Khat^-1 column by column (solves against unit vectors),
+ * then each derivative matrix built and contracted in full.  grad may be NULL.
+ * Returns 0, or pivot + 1 if Khat is not SPD. */
+int orc_mll(const double* X, int N, int d, const double* y, const double* log_hyp, double* mll,
+            double* grad)
+{
+    double ell[16];
+    for (int c = 0; c < d; ++c) ell[c] = exp(log_hyp[c]);
+    double s = exp(log_hyp[d]), sn2 = exp(log_hyp[d + 1]);
+    double* L = orc_khat(X, N, d, ell, s, sn2);
+    if (!L) return -1;
+    int rc = orc_cholesky(L, N);
+    if (rc != 0) {
+        free(L);
+        return rc;
+    }
+    double* tmp = (double*)malloc(sizeof(double) * N);
+    double* alpha = (double*)malloc(sizeof(double) * N);
+    orc_forward_solve(L, N, y, tmp);
+    orc_backward_solve_T(L, N, tmp, alpha);
+    double yKy = 0.0, logdet = 0.0;
+    for (int i = 0; i < N; ++i) yKy += y[i] * alpha[i];
+    for (int i = 0; i < N; ++i) logdet += 2.0 * log(L[(size_t)i * N + i]);
+    *mll = -0.5 * yKy - 0.5 * logdet - 0.5 * N * log(2.0 * 3.14159265358979323846);
+    if (grad) {
+        /* Khat^-1, column j = Khat^-1 e_j */
+        double* Kinv = (double*)malloc(sizeof(double) * (size_t)N * N);
+        double* e = (double*)calloc((size_t)N, sizeof(double));
+        double* col = (double*)malloc(sizeof(double) * N);
+        for (int j = 0; j < N; ++j) {
+            e[j] = 1.0;
+            orc_forward_solve(L, N, e, tmp);
+            orc_backward_solve_T(L, N, tmp, col);
+            e[j] = 0.0;
+            for (int i = 0; i < N; ++i) Kinv[(size_t)i * N + j] = col[i];
+        }
+        double* D = (double*)malloc(sizeof(double) * (size_t)N * N);
+        for (int jp = 0; jp < d + 2; ++jp) {
+            /* D = dKhat / dphi_jp */
+            for (int i = 0; i < N; ++i)
+                for (int j = 0; j < N; ++j) {
+                    double v;
+                    if (jp < d) {
+                        double diff = X[(size_t)i * d + jp] - X[(size_t)j * d + jp];
+                        v = orc_kernel(X + (size_t)i * d, X + (size_t)j * d, d, ell, s) * diff * diff /
+                            (ell[jp] * ell[jp]);
+                    } else if (jp == d) {
+                        v = orc_kernel(X + (size_t)i * d, X + (size_t)j * d, d, ell, s);
+                    } else {
+                        v = (i == j) ? sn2 : 0.0;
+                    }
+                    D[(size_t)i * N + j] = v;
+                }
+            /* 1/2 alpha^T D alpha - 1/2 tr(Kinv D) */
+            double quad = 0.0, tr = 0.0;
+            for (int i = 0; i < N; ++i) {
+                double Da = 0.0;
+                for (int j = 0; j < N; ++j) Da += D[(size_t)i * N + j] * alpha[j];
+                quad += alpha[i] * Da;
+            }
+            for (int i = 0; i < N; ++i)
+                for (int j = 0; j < N; ++j) tr += Kinv[(size_t)i * N + j] * D[(size_t)j * N + i];
+            grad[jp] = 0.5 * quad - 0.5 * tr;
+        }
+        free(D);
+        free(col);
+        free(e);
+        free(Kinv);
+    }
+    free(alpha);
+    free(tmp);
+    free(L);
+    return 0;
+}

@@ -67,6 +67,8 @@ def lib() -> C.CDLL:
             L.bagel_get_gp_kernel.argtypes = [_vp, C.POINTER(C.c_int)]
             L.bagel_sample_states.argtypes = [_vp, C.c_uint64, C.c_longlong, C.c_int, C.c_int, C.c_int,
                                               C.POINTER(C.c_float), C.POINTER(C.c_float), _vp]
+            L.gp_log_marginal_likelihood.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                     C.POINTER(C.c_double)]
             L.policy_adam_step.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_longlong, C.c_float, C.c_float,
                                            C.c_float, C.c_float, C.POINTER(C.c_int)]
             _lib = L
@@ -78,7 +80,8 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
            "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench",
-           "bagel_debug_buffer", "bagel_debug_trace", "bagel_sample_states", "policy_adam_step"]
+           "bagel_debug_buffer", "bagel_debug_trace", "bagel_sample_states", "policy_adam_step",
+           "gp_log_marginal_likelihood"]
 
 PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce", "theta_grad"]
 
@@ -145,6 +148,9 @@ class Context:
         p = Y.shape[1]
         self._check(self.L.gp_load(self.h, _ptr(X), _ptr(Y), N, d, p, _ptr(ell), _ptr(s), _ptr(sn)))
         self.N, self.d, self.p = N, d, p
+        self._ell = ell.double().cpu().numpy().reshape(p, d)
+        self._s = s.double().cpu().numpy().reshape(p)
+        self._noise = sn.double().cpu().numpy().reshape(p)
 
     def love_cache_build(self, rank: int) -> float:
         sec = C.c_double(0.0)
@@ -175,6 +181,23 @@ class Context:
                                                  int(seed) & 0xFFFFFFFFFFFFFFFF, int(traj_offset), int(B_global),
                                                  C.byref(cost), _ptr(grad)))
         return cost.value, grad
+
+    def loaded_log_hyp(self, m: int) -> np.ndarray:
+        """phi of output m as loaded by gp_load: [log l (d) | log s | log sn2]."""
+        return np.log(np.r_[self._ell[m], self._s[m], self._noise[m]]).astype(np.float64)
+
+    def log_marginal_likelihood(self, m: int, log_hyp=None, want_grad: bool = True):
+        """(log p(y_m | X, phi), d/dphi) with phi = [log l (d) | log s | log sn2] (Eq.5-6, P:77-80);
+        log_hyp None = the loaded hyperparameters.  The gradient is None unless want_grad."""
+        dp = C.POINTER(C.c_double)
+        h = None if log_hyp is None else np.ascontiguousarray(log_hyp, dtype=np.float64)
+        if h is not None and h.shape != (self.d + 2,):
+            raise ValueError(f"log_hyp must have d + 2 = {self.d + 2} entries")
+        val = C.c_double(0.0)
+        g = np.zeros(self.d + 2) if want_grad else None
+        self._check(self.L.gp_log_marginal_likelihood(self.h, int(m), None if h is None else h.ctypes.data_as(dp),
+                                                      C.byref(val), None if g is None else g.ctypes.data_as(dp)))
+        return val.value, g
 
     # ------------------------------------------------------------ Algorithm 1 around the path
     def sample_states(self, seed: int, traj_offset: int, B: int, lo, hi, which: int = 0, out=None):

@@ -407,6 +407,9 @@ extern "C" int bagel_destroy(bagel_ctx* c) {
   dev_free(c->ws.stage);
   dev_free(c->op_flag);
   dev_free(c->op_bounds);
+  dev_free(c->mll_K);
+  dev_free(c->mll_Li);
+  dev_free(c->mll_vec);
   delete c;
   return BAGEL_OK;
 }
@@ -957,5 +960,57 @@ extern "C" int policy_adam_step(bagel_ctx* c, float* params, const float* grad, 
       CK(cudaStreamSynchronize(c->stream));
       *skipped = f;
     }
+  });
+}
+
+// ------------------------------------------------------------ GP hyperparameter learning (NEXT-1)
+extern "C" int gp_log_marginal_likelihood(bagel_ctx* c, int m, const double* log_hyp, double* mll, double* grad) {
+  return guarded(c, [&] {
+    REQUIRE(c->N > 0, BAGEL_E_STATE, "gp_log_marginal_likelihood: no GP loaded (call gp_load first)");
+    REQUIRE(m >= 0 && m < c->p, BAGEL_E_ARG, "gp_log_marginal_likelihood: output m=%d out of range [0, %d)", m, c->p);
+    REQUIRE(mll, BAGEL_E_ARG, "gp_log_marginal_likelihood: mll must be non-NULL");
+    const int N = c->N, d = c->d;
+    REQUIRE((double)N * N * 8.0 * 2.0 < 120e9, BAGEL_E_ARG,
+            "gp_log_marginal_likelihood: N=%d needs 2 N^2 float64 (%.1f GB) of workspace, above the 120 GB limit", N,
+            (double)N * N * 16.0 / 1e9);
+    double h[BAGEL_MAX_D + 2];
+    for (int i = 0; i < d; ++i) h[i] = log_hyp ? log_hyp[i] : log((double)c->ell[(size_t)m * d + i]);
+    h[d] = log_hyp ? log_hyp[d] : log((double)c->s[m]);
+    h[d + 1] = log_hyp ? log_hyp[d + 1] : log((double)c->noise[m]);
+    for (int i = 0; i < d + 2; ++i)
+      REQUIRE(isfinite(h[i]) && fabs(h[i]) < 700.0, BAGEL_E_ARG, "gp_log_marginal_likelihood: log_hyp[%d] = %g out of range",
+              i, h[i]);
+    REQUIRE(exp(h[d + 1]) >= 1e-8, BAGEL_E_ARG, "gp_log_marginal_likelihood: noise exp(log_hyp[%d]) = %g must be >= 1e-8",
+            d + 1, exp(h[d + 1]));
+    const size_t nvec = (size_t)N + 2 + (BAGEL_MAX_D + 2) + (size_t)mll_part_count(N);
+    if (c->mll_N != N) {
+      dev_free(c->mll_K);
+      dev_free(c->mll_Li);
+      dev_free(c->mll_vec);
+      c->mll_N = 0;
+      dev_alloc(c, c->mll_K, (size_t)N * N);
+      dev_alloc(c, c->mll_Li, (size_t)N * N);
+      dev_alloc(c, c->mll_vec, nvec);
+      c->mll_N = N;
+    }
+    if (!c->op_flag) dev_alloc(c, c->op_flag, 1);
+    double* alpha = c->mll_vec;
+    double* sc = alpha + N;
+    double* g = sc + 2;
+    double* part = g + BAGEL_MAX_D + 2;
+    cudaStream_t st = c->stream;
+    CK(cudaMemsetAsync(c->op_flag, 0, sizeof(int), st));
+    mll_launch(c->X, c->Y + m, c->p, N, d, h, c->mll_K, c->mll_Li, alpha, sc, part, g, c->op_flag, grad != nullptr, st);
+    CK(cudaGetLastError());
+    int pv = 0;
+    double hs[2 + BAGEL_MAX_D + 2];
+    CK(cudaMemcpyAsync(&pv, c->op_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs, sc, (2 + (size_t)(grad ? d + 2 : 0)) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    REQUIRE(pv == 0, BAGEL_E_NUMERIC, "gp_log_marginal_likelihood: Cholesky pivot %d of output %d is <= 0 (Khat not SPD)",
+            pv - 1, m);
+    *mll = -0.5 * hs[1] - hs[0] - 0.5 * N * log(2.0 * M_PI);
+    if (grad)
+      for (int i = 0; i < d + 2; ++i) grad[i] = hs[2 + i];
   });
 }

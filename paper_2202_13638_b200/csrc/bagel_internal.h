@@ -161,6 +161,10 @@ struct bagel_ctx {
   TcState tcs;
   int* op_flag = nullptr;     // Adam skip flag (device int, optim.cu)
   float* op_bounds = nullptr; // 2 x MAX_P sampling bounds (lo | hi)
+  double* mll_K = nullptr;    // N x N: Khat, then its Cholesky factor (mll.cu)
+  double* mll_Li = nullptr;   // N x N: L^-1
+  double* mll_vec = nullptr;  // alpha (N) | scalars (2) | grad (MAX_D + 2) | tile partials
+  int mll_N = 0;
   int gp_kernel = 1;  // 1: tcgen05 path (default), 0: v0 FFMA path (reference / A-B tests)
   int last_launches = 0;
   int num_sms = 148;
@@ -262,6 +266,10 @@ int op_sample_uniform(uint64_t seed, long long traj_offset, int B, int p, int wh
                       const float* hi, float* out, cudaStream_t st);
 int op_adam(float* theta, const float* g, float* m1, float* m2, int n, float lr, float b1, float b2, float eps,
             float bc1, float bc2, int* flag, cudaStream_t st);
+int mll_part_count(int N);
+int mll_launch(const float* X, const float* Y, int ystride, int N, int d, const double* log_hyp, double* K,
+               double* Li, double* alpha, double* sc, double* part, double* grad, int* pivot_flag, bool want_grad,
+               cudaStream_t st);
 size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1);
 size_t tc_zp_bytes(const bagel_ctx* c, int B);
 int tc_njt(const bagel_ctx* c);

@@ -63,24 +63,22 @@ __global__ void __launch_bounds__(256) k_mll_scalars(const double* __restrict__ 
   }
 }
 
-// Diagonal blocks of Linv: Linv_II = L_II^-1 (thread c solves L_II x = e_c by forward substitution).
+// Diagonal blocks of Linv: Linv_II = L_II^-1 (thread c solves L_II x = e_c by forward substitution;
+// its column lives in Li itself: every element is written and re-read by the same thread).
 __global__ void __launch_bounds__(TB) k_trtri_diag(const double* __restrict__ L, int N, double* __restrict__ Li) {
   __shared__ double Ls[TB][TB + 1];
-  __shared__ double Xs[TB][TB + 1];
   const int i0 = blockIdx.x * TB, nb = min(TB, N - i0), c = threadIdx.x;
   for (int r = 0; r < nb; ++r)
     if (c < nb) Ls[r][c] = L[(size_t)(i0 + r) * N + i0 + c];
   __syncthreads();
   if (c < nb) {
+    double* col = Li + (size_t)i0 * N + i0 + c;
     for (int r = 0; r < nb; ++r) {
       double acc = (r == c) ? 1.0 : 0.0;
-      for (int k = c; k < r; ++k) acc -= Ls[r][k] * Xs[k][c];
-      Xs[r][c] = r < c ? 0.0 : acc / Ls[r][r];
+      for (int k = c; k < r; ++k) acc -= Ls[r][k] * col[(size_t)k * N];
+      col[(size_t)r * N] = r < c ? 0.0 : acc / Ls[r][r];
     }
   }
-  __syncthreads();
-  for (int r = 0; r < nb; ++r)
-    if (c < nb) Li[(size_t)(i0 + r) * N + i0 + c] = Xs[r][c];
 }
 
 // acc[u][v] += sum_l A(l, ty + 16u) B(l, tx + 16v) over one 16-deep chunk staged in shared memory
@@ -110,7 +108,7 @@ __global__ void __launch_bounds__(256) k_trtri_row(const double* __restrict__ L,
   const int ni = min(TB, N - i0);
   __shared__ double As[16][TB];
   __shared__ double Bs[16][TB];
-  __shared__ double Ts[TB][TB + 1];
+  __shared__ double Ts[TB][TB];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double acc[4][4] = {};
   for (int K = J; K < I; ++K) {

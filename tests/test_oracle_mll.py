@@ -1,0 +1,87 @@
+"""Pins of the oracle's log marginal likelihood and its gradient (Eq.5-6; reading R33) --
+no GPU: closed forms at N = 1 and N = 2, brute force at N = 8 against numpy's slogdet / inverse,
+central finite differences, and the SPEC S:229 sign property."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import small_gp_data
+
+LOG2PI = math.log(2.0 * math.pi)
+
+
+def test_n1_closed_form():
+    """N = 1: Khat = s + sn2; log p = -y^2/(2 Khat) - log(Khat)/2 - log(2 pi)/2;
+    d/dlog s = s/2 (y^2/Khat^2 - 1/Khat), d/dlog sn2 likewise with sn2, d/dlog l = 0 (r = 0)."""
+    X, y = np.array([[0.3, -0.2, 1.1]]), np.array([0.7])
+    ell, s, sn2 = np.array([0.8, 1.3, 0.4]), 0.2, 0.05
+    val, g = O.log_marginal_likelihood(X, y, np.log(np.r_[ell, s, sn2]))
+    Kh = s + sn2
+    assert val == pytest.approx(-0.49 / (2 * Kh) - 0.5 * math.log(Kh) - 0.5 * LOG2PI, rel=1e-14)
+    assert g[:3] == pytest.approx([0.0, 0.0, 0.0], abs=1e-300)
+    assert g[3] == pytest.approx(0.5 * s * (0.49 / Kh ** 2 - 1 / Kh), rel=1e-13)
+    assert g[4] == pytest.approx(0.5 * sn2 * (0.49 / Kh ** 2 - 1 / Kh), rel=1e-13)
+
+
+def test_n2_closed_form():
+    """N = 2: Khat = [[a, k], [k, a]], a = s + sn2, k = s exp(-r^2/2), r^2 = sum_c dx_c^2 / l_c^2.
+    log|Khat| = log(a^2 - k^2); y^T Khat^-1 y = (a y1^2 - 2 k y1 y2 + a y2^2) / (a^2 - k^2);
+    d/dlog l_c (only k moves, dk = k dx_c^2 / l_c^2): d log p = dk (y^T Khat^-1 E Khat^-1 y - tr(Khat^-1 E)) / 2
+    with E = [[0, 1], [1, 0]]."""
+    X = np.array([[0.1, 0.5], [-0.4, 0.9]])
+    y = np.array([0.3, -0.8])
+    ell, s, sn2 = np.array([0.7, 1.5]), 0.9, 0.1
+    val, g = O.log_marginal_likelihood(X, y, np.log(np.r_[ell, s, sn2]))
+    dx = X[0] - X[1]
+    r2c = dx ** 2 / ell ** 2
+    k = s * math.exp(-0.5 * r2c.sum())
+    a = s + sn2
+    det = a * a - k * k
+    Kinv = np.array([[a, -k], [-k, a]]) / det
+    quad = (a * y[0] ** 2 - 2 * k * y[0] * y[1] + a * y[1] ** 2) / det
+    assert val == pytest.approx(-0.5 * quad - 0.5 * math.log(det) - LOG2PI, rel=1e-14)
+    al = Kinv @ y
+    E = np.array([[0.0, 1.0], [1.0, 0.0]])
+    dE = al @ E @ al - np.trace(Kinv @ E)
+    for c in range(2):
+        assert g[c] == pytest.approx(0.5 * k * r2c[c] * dE, rel=1e-12)
+    # d/dlog s: dKhat = K (off-diagonal k, diagonal s); d/dlog sn2: sn2 I
+    Ks = np.array([[s, k], [k, s]])
+    assert g[2] == pytest.approx(0.5 * (al @ Ks @ al - np.trace(Kinv @ Ks)), rel=1e-12)
+    assert g[3] == pytest.approx(0.5 * sn2 * (al @ al - np.trace(Kinv)), rel=1e-12)
+
+
+def test_brute_force_n8_against_numpy():
+    X, Y, ell, s, noise = small_gp_data(N=8, d=3, p=1, seed=4)
+    y = Y[:, 0]
+    h = np.log(np.r_[ell[0], s[0], noise[0]])
+    val, _ = O.log_marginal_likelihood(X, y, h)
+    D = ((X[:, None, :] - X[None, :, :]) / ell[0]) ** 2
+    Kh = s[0] * np.exp(-0.5 * D.sum(-1)) + noise[0] * np.eye(8)
+    sign, ld = np.linalg.slogdet(Kh)
+    assert sign > 0
+    ref = -0.5 * y @ np.linalg.solve(Kh, y) - 0.5 * ld - 4 * LOG2PI
+    assert val == pytest.approx(ref, rel=1e-12)
+
+
+def test_gradient_matches_central_differences():
+    X, Y, ell, s, noise = small_gp_data(N=40, d=3, p=2, seed=1)
+    for m in range(2):
+        h = np.log(np.r_[ell[m], s[m], noise[m]])
+        _, g = O.log_marginal_likelihood(X, Y[:, m], h)
+        for j in range(5):
+            e = np.zeros(5)
+            e[j] = 1e-5
+            fp, _ = O.log_marginal_likelihood(X, Y[:, m], h + e, want_grad=False)
+            fm, _ = O.log_marginal_likelihood(X, Y[:, m], h - e, want_grad=False)
+            fd = (fp - fm) / 2e-5
+            assert g[j] == pytest.approx(fd, rel=1e-6, abs=1e-7 * np.abs(g).max())
+
+
+def test_zero_targets_push_signal_variance_down():
+    """y = 0 -> d/dlog s = -tr(Khat^-1 K)/2 < 0."""
+    X, _, ell, s, noise = small_gp_data(N=30, d=2, p=1, seed=2)
+    _, g = O.log_marginal_likelihood(X, np.zeros(30), np.log(np.r_[ell[0], s[0], noise[0]]))
+    assert g[2] < 0 and g[3] < 0
