@@ -87,6 +87,17 @@ int gp_load(bagel_ctx* ctx, const float* X, const float* y, int N, int d, int p,
  * or T is not positive definite; E_CUDA (incl. out of memory). */
 int love_cache_build(bagel_ctx* ctx, int rank, double* seconds_out);
 
+/* exact_cache_build -- the exact-GP variant of the cache (SURVEY.md §8(f)
+ * NEXT-3; the paper's "AutoDiff on exact GPs" baseline): per
+ * output, in float64 on the GPU, L = chol(Khat), alpha = Khat^-1 y and
+ * R = L^-1 (N x N, blocked triangular inverse), installed as a rank-N cache,
+ * so every rollout / predict call afterwards uses the exact Eq.3 variance
+ * k** - ||L^-1 k||^2 instead of the LOVE estimate (K^-1 = R^T R exactly).
+ * Synchronous; seconds_out [host, nullable].  Replaces any LOVE cache.
+ * Errors: E_STATE without gp_load; E_ARG if N > 768 (the largest rank the
+ * hot-path kernels hold); E_NUMERIC if a Cholesky pivot <= 0; E_CUDA. */
+int exact_cache_build(bagel_ctx* ctx, double* seconds_out);
+
 /* ------------------------------------------------------- policy / reward */
 
 /* policy_configure -- tanh MLP policy u = pi_theta(x, g) (P:104, P:129,

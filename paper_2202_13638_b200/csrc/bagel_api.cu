@@ -609,6 +609,47 @@ extern "C" int love_cache_build(bagel_ctx* c, int rank, double* seconds_out) {
   });
 }
 
+extern "C" int exact_cache_build(bagel_ctx* c, double* seconds_out) {
+  return guarded(c, [&] {
+    REQUIRE(c->N > 0, BAGEL_E_STATE, "exact_cache_build: no GP loaded (call gp_load first)");
+    REQUIRE(c->N <= BAGEL_MAX_RANK, BAGEL_E_ARG,
+            "exact_cache_build: the exact variance is the LOVE query at rank N, supported for N <= %d (N=%d)",
+            BAGEL_MAX_RANK, c->N);
+    const auto t0 = std::chrono::steady_clock::now();
+    const int N = c->N;
+    cudaStream_t st = c->stream;
+    alloc_cache(c, N);
+    double* K = nullptr;
+    int* piv = nullptr;
+    struct Guard {
+      bagel_ctx* c;
+      double** K;
+      int** piv;
+      ~Guard() {
+        dev_free(*K);
+        dev_free(*piv);
+      }
+    } guard{c, &K, &piv};
+    dev_alloc(c, K, (size_t)N * N);
+    dev_alloc(c, piv, 1);
+    for (int m = 0; m < c->p; ++m) {
+      CK(cudaMemsetAsync(piv, 0, sizeof(int), st));
+      exact_launch(c->X, c->Y + m, c->p, N, c->d, c->ell.data() + (size_t)m * c->d, c->s[m], c->noise[m], K,
+                   c->R64 + (size_t)m * N * N, c->alpha64 + (size_t)m * N, piv, st);
+      int pv = 0;
+      CK(cudaMemcpyAsync(&pv, piv, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      REQUIRE(pv == 0, BAGEL_E_NUMERIC, "exact_cache_build: Cholesky pivot %d of output %d is <= 0 (Khat not SPD)", pv - 1,
+              m);
+      pack_output(c, m);
+      c->cache_ok[m] = 1;
+    }
+    CK(cudaStreamSynchronize(st));
+    if (seconds_out)
+      *seconds_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
 extern "C" int policy_configure(bagel_ctx* c, const int* sizes, int n_sizes) {
   return guarded(c, [&] {
     REQUIRE(c->N > 0, BAGEL_E_STATE, "policy_configure: no GP loaded (call gp_load first)");

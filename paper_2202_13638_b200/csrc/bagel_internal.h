@@ -267,6 +267,8 @@ int op_sample_uniform(uint64_t seed, long long traj_offset, int B, int p, int wh
 int op_adam(float* theta, const float* g, float* m1, float* m2, int n, float lr, float b1, float b2, float eps,
             float bc1, float bc2, int* flag, cudaStream_t st);
 int mll_part_count(int N);
+int exact_launch(const float* X, const float* Y, int ystride, int N, int d, const float* ell, float s, float noise,
+                 double* K, double* Li, double* alpha, int* pivot_flag, cudaStream_t st);
 int mll_launch(const float* X, const float* Y, int ystride, int N, int d, const double* log_hyp, double* K,
                double* Li, double* alpha, double* sc, double* part, double* grad, int* pivot_flag, bool want_grad,
                cudaStream_t st);

@@ -250,6 +250,31 @@ inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace
 
+// Exact-GP variance cache ("AutoDiff on exact GPs"): L = chol(Khat),
+// alpha = Khat^-1 y, Li = L^-1, so that var = s - ||L^-1 k||^2 (Eq.3 exactly) is the LOVE query with
+// R = L^-1 at rank N.  Hyperparameters as gp_load holds them (float, widened).
+int exact_launch(const float* X, const float* Y, int ystride, int N, int d, const float* ell, float s, float noise,
+                 double* K, double* Li, double* alpha, int* pivot_flag, cudaStream_t st) {
+  Hyp64 h{};
+  for (int c = 0; c < d; ++c) h.inv_l2[c] = 1.0 / ((double)ell[c] * (double)ell[c]);
+  h.s = (double)s;
+  h.noise = (double)noise;
+  int launches = 0;
+  k_khat64<<<dim3(cdiv(N, 256), N), 256, 0, st>>>(X, N, d, h, K);
+  ++launches;
+  launches += cb_cholesky(K, N, pivot_flag, st);
+  launches += cb_cholesky_solve(K, N, Y, ystride, alpha, nullptr, st);
+  const int nb = cdiv(N, TB);
+  cudaMemsetAsync(Li, 0, (size_t)N * N * sizeof(double), st);
+  k_trtri_diag<<<nb, TB, 0, st>>>(K, N, Li);
+  ++launches;
+  for (int I = 1; I < nb; ++I) {
+    k_trtri_row<<<I, 256, 0, st>>>(K, N, I, Li);
+    ++launches;
+  }
+  return launches;
+}
+
 int mll_part_count(int N) {
   const int nb = cdiv(N, TB);
   return nb * (nb + 1) / 2 * NPART;
