@@ -75,6 +75,16 @@ const char* bagel_last_error(const bagel_ctx* ctx);
 int gp_load(bagel_ctx* ctx, const float* X, const float* y, int N, int d, int p,
             const float* lengthscales, const float* outputscale, const float* noise);
 
+/* gp_target_mode -- what the GPs' targets y were ("each m-th GP can model
+ * the one-step forward dynamics of one output y = x_{k+1} or the discrete
+ * difference y = Delta x = x_{k+1} - x_k"):
+ *   absolute = 0 (default, reading R6): Delta targets, x' = x + mu + sigma eps;
+ *   absolute = 1 (NEXT-4): absolute targets, x' = mu + sigma eps, and the
+ *   reverse pass drops the identity path dx'/dx = I.
+ * Applies to every later rollout / trace call; kept across gp_load.
+ * Errors: E_ARG if absolute is not 0 or 1. */
+int gp_target_mode(bagel_ctx* ctx, int absolute);
+
 /* love_cache_build -- the one-time LOVE cache ("one-time caching
  * operation ... ~0.6s"), for every output m, in float64 on the GPU:
  *   alpha_m = Khat_m^-1 y_m by blocked Cholesky (Khat = K + sigma_n^2 I; R21),

@@ -43,7 +43,7 @@ def build(force: bool = False) -> str:
 
 class GP(C.Structure):
     _fields_ = [("N", C.c_int), ("d", C.c_int), ("p", C.c_int), ("k", C.c_int),
-                ("X", _dp), ("ell", _dp), ("s", _dp), ("alpha", _dp), ("R", _dp)]
+                ("X", _dp), ("ell", _dp), ("s", _dp), ("alpha", _dp), ("R", _dp), ("abs_target", C.c_int)]
 
 
 class Policy(C.Structure):
@@ -173,7 +173,7 @@ def love_build(X, y, ell, s, noise, k, m_index=0):
 class Model:
     """The oracle's GP dynamics model: fp64 copies of X, hyperparameters, alpha and R."""
 
-    def __init__(self, X, ell, s, alpha, R):
+    def __init__(self, X, ell, s, alpha, R, abs_target=False):
         self.X = _d(X)
         self.ell = _d(ell)
         self.s = _d(s).reshape(-1)
@@ -184,11 +184,12 @@ class Model:
         self.k = self.R.shape[1]
         assert self.alpha.shape == (self.p, self.N)
         assert self.R.shape == (self.p, self.k, self.N)
+        self.abs_target = bool(abs_target)  # targets y = x_{k+1} instead of Delta x
         self.struct = GP(self.N, self.d, self.p, self.k, _ptr(self.X), _ptr(self.ell), _ptr(self.s),
-                         _ptr(self.alpha), _ptr(self.R))
+                         _ptr(self.alpha), _ptr(self.R), int(self.abs_target))
 
     @classmethod
-    def build(cls, X, Y, ell, s, noise, k):
+    def build(cls, X, Y, ell, s, noise, k, abs_target=False):
         """Exact alpha (Cholesky) and naive LOVE R for every output (one-time cache)."""
         X, Y, ell, s, noise = _d(X), _d(Y), _d(ell), _d(s), _d(noise)
         p = Y.shape[1]
@@ -199,7 +200,7 @@ class Model:
             alphas.append(a)
             Rs.append(R)
             restarts.append(nr)
-        mdl = cls(X, ell, s, np.stack(alphas), np.stack(Rs))
+        mdl = cls(X, ell, s, np.stack(alphas), np.stack(Rs), abs_target)
         mdl.restarts = restarts
         return mdl
 

@@ -358,6 +358,7 @@ typedef struct {
     const double* s;     /* p */
     const double* alpha; /* p x N   (Khat^-1 y, not scaled by s) */
     const double* R;     /* p x k x N */
+    int abs_target;      /* 0: Delta targets x' = x + f (R6); 1: absolute x' = f (NEXT-4) */
 } orc_gp;
 
 /* fp32-sensitivity mode (variant (a)): every kernel value entering the
@@ -607,7 +608,8 @@ int orc_rollout(const orc_gp* gp, const orc_policy* pol, const orc_reward* rw, c
                     tsig[(size_t)t * p + m] = sig;
                     tvpos[(size_t)t * p + m] = v > ORC_VAR_FLOOR ? 1.0 : 0.0;
                     teps[(size_t)t * p + m] = e;
-                    xn[m] = x[m] + mu + sig * e; /* Eq.10: x_{k-1} + f_D, f_D ~ N(mu, var) */
+                    /* Eq.10: x_{k-1} + f_D, f_D ~ N(mu, var); absolute targets: f_D alone */
+                    xn[m] = (gp->abs_target ? 0.0 : x[m]) + mu + sig * e;
                     if (trace_mu) trace_mu[((size_t)t * B + b) * p + m] = mu;
                     if (trace_var) trace_var[((size_t)t * B + b) * p + m] = v;
                 }
@@ -681,7 +683,8 @@ int orc_rollout(const orc_gp* gp, const orc_policy* pol, const orc_reward* rw, c
                 for (int c = 0; c < p; ++c) {
                     double hb = dcur[c];
                     if (pol->phi_mode == 1) hb -= dcur[2 * p + c];
-                    xbar[c] = xbar[c] + xsbar[c] + hb +
+                    /* dx_{t+1}/dx_t = I + ... for Delta targets, no identity path for absolute */
+                    xbar[c] = (gp->abs_target ? 0.0 : xbar[c]) + xsbar[c] + hb +
                               invB * r * rw->Q[c] * (x[c] - g[c]) / (rw->sigma_r * rw->sigma_r);
                 }
             }

@@ -45,6 +45,7 @@ def lib() -> C.CDLL:
             L.gp_load.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp]
             L.love_cache_build.argtypes = [_vp, C.c_int, C.POINTER(C.c_double)]
             L.exact_cache_build.argtypes = [_vp, C.POINTER(C.c_double)]
+            L.gp_target_mode.argtypes = [_vp, C.c_int]
             L.policy_configure.argtypes = [_vp, C.POINTER(C.c_int), C.c_int]
             L.reward_configure.argtypes = [_vp, C.POINTER(C.c_float), C.c_float]
             L.rollout_cost_and_grad.argtypes = [_vp, _vp, _vp, _vp, C.c_int, C.c_int, C.c_uint64, C.c_longlong,
@@ -82,7 +83,8 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
            "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench",
            "bagel_debug_buffer", "bagel_debug_trace", "bagel_sample_states", "policy_adam_step",
-           "gp_log_marginal_likelihood", "exact_cache_build"]
+           "gp_log_marginal_likelihood", "exact_cache_build",
+           "gp_target_mode"]
 
 PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce", "theta_grad"]
 
@@ -157,6 +159,10 @@ class Context:
         sec = C.c_double(0.0)
         self._check(self.L.love_cache_build(self.h, int(rank), C.byref(sec)))
         return sec.value
+
+    def gp_target_mode(self, absolute: bool):
+        """False (default): Delta targets, x' = x + f; True: absolute targets, x' = f."""
+        self._check(self.L.gp_target_mode(self.h, int(bool(absolute))))
 
     def exact_cache_build(self) -> float:
         """Exact-GP cache (R = L^-1 at rank N, N <= 768): exact Eq.3 variances from here on."""

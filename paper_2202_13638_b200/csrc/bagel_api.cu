@@ -168,6 +168,7 @@ void setup_gpdesc(bagel_ctx* c, int k) {
   g.k = k;
   g.C = 1 + c->d + k;
   g.Cld = round_up(g.C, 64);
+  g.abs_target = c->abs_target;
   for (int m = 0; m < c->p; ++m) {
     g.s[m] = c->s[m];
     for (int j = 0; j < c->d; ++j) {
@@ -1053,5 +1054,13 @@ extern "C" int gp_log_marginal_likelihood(bagel_ctx* c, int m, const double* log
     *mll = -0.5 * hs[1] - hs[0] - 0.5 * N * log(2.0 * M_PI);
     if (grad)
       for (int i = 0; i < d + 2; ++i) grad[i] = hs[2 + i];
+  });
+}
+
+extern "C" int gp_target_mode(bagel_ctx* c, int absolute) {
+  return guarded(c, [&] {
+    REQUIRE(absolute == 0 || absolute == 1, BAGEL_E_ARG, "gp_target_mode: absolute must be 0 or 1 (got %d)", absolute);
+    c->abs_target = absolute;
+    c->gp.abs_target = absolute;
   });
 }

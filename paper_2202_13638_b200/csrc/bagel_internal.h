@@ -48,6 +48,7 @@ struct GpDesc {
   float ell2inv[BAGEL_MAX_P][BAGEL_MAX_D];  // 1 / l_mc^2
   float qscale[BAGEL_MAX_P][BAGEL_MAX_D];   // KAPPA / l_mc
   float s[BAGEL_MAX_P];
+  int abs_target;  // 0: Delta targets x' = x + f (R6, default); 1: absolute targets x' = f (NEXT-4)
 };
 
 // Arguments of the step epilogue (policy_rows.cuh epi_warp_rows) for step t of T: pass-2
@@ -165,6 +166,7 @@ struct bagel_ctx {
   double* mll_Li = nullptr;   // N x N: L^-1
   double* mll_vec = nullptr;  // alpha (N) | scalars (2) | grad (MAX_D + 2) | tile partials
   int mll_N = 0;
+  int abs_target = 0;         // gp_target_mode
   int gp_kernel = 1;  // 1: tcgen05 path (default), 0: v0 FFMA path (reference / A-B tests)
   int last_launches = 0;
   int num_sms = 148;

@@ -7,7 +7,7 @@
 //            generated on the fly from exp2(-||x_hat - X_hat||^2), never stored.
 //   reduce 1 v = s - ||z||^2 (LOVE Eq.3), sigma, J^mu_c = (sum k a X_c - x*_c mu) / l_c^2
 //   pass 2   w = R^T z on the fly, sum_n w_n k_n [1 | X_n]            (autodiff of Eq.3)
-//            -> J^v_c = (2 / l_c^2) (x*_c sum w k - sum w k X_c)     (finished by the caller)
+//            -> J^v_c = (2 / l_c^2) sum_n w k (x*_c - X_nc)  (difference form; finished by the caller)
 //
 // The contraction over N is split S ways for parallelism; partial sums are
 // reduced in a fixed order (deterministic).  Dominant work: 2 p N (1+d+k) +
@@ -226,16 +226,18 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2(GpDesc g, const float* __r
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = ty * 8 + i;
-        float q = 0.0f;
+        float q = 0.0f, dx[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const float df = (xq[c * P2_BM + r] - Xr[nn * D + c]) * g.qscale[m][c];
+          dx[c] = xq[c * P2_BM + r] - Xr[nn * D + c];
+          const float df = dx[c] * g.qscale[m][c];
           q = fmaf(df, df, q);
         }
         const float t = w[i][e] * exp2f(-q);
         acc[i][0] += t;
+        // difference form: sum_n (s w_n k_n) (x*_c - X_nc)
 #pragma unroll
-        for (int c = 0; c < D; ++c) acc[i][1 + c] = fmaf(t, Xr[nn * D + c], acc[i][1 + c]);
+        for (int c = 0; c < D; ++c) acc[i][1 + c] = fmaf(t, dx[c], acc[i][1 + c]);
       }
     }
   }
@@ -284,7 +286,7 @@ __global__ void k_finish_predict(GpDesc g, const float* __restrict__ xstar, int 
 #pragma unroll
     for (int c = 0; c < D; ++c)
       dvar[(size_t)idx * D + c] =
-          2.0f * g.ell2inv[m][c] * (xstar[(size_t)b * D + c] * sums[0] - sums[1 + c]);
+          2.0f * g.ell2inv[m][c] * sums[1 + c];  // sums[1 + c] = sum_n w_n k_n (x*_c - X_nc)
   }
 }
 

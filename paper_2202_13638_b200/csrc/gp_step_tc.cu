@@ -5,7 +5,7 @@
 //
 // Per output m and a batch of query rows x* (Eq.2-3 with LOVE):
 //   pass 1 (k_p1_tc)  z = R k(x*, X) on tcgen05 (3-pass fp16 hi/lo split, fp32 TMEM
-//                     accumulation); the 1 + d mean columns [mu | sum k a X_c] are
+//                     accumulation); the 1 + d mean columns [mu | sum k a (x*_c - X_c)] are
 //                     accumulated in fp32 on the CUDA cores by the same warps that
 //                     generate ktilde = exp2(-||x_hat - X_hat||^2) (never stored in HBM).
 //   reduce 1          sums the N-split partials; v = s - ||z||^2, sigma, J^mu; packs
@@ -98,7 +98,7 @@ __device__ __forceinline__ float pow2_scale_for(float amax, float* inv) {
 
 // ====================================================================== packing
 // Pass-1 tiles of output m: [ct][t] -> [B hi: NZ x KT1 | B lo | aux: KT1 x AUXW]
-// B(j, n) = s R_jn * colscale_j^-1 (j = ct*NZ + row), aux(n) = [X(d) | s alpha | s alpha X(d)].
+// B(j, n) = s R_jn * colscale_j^-1 (j = ct*NZ + row), aux(n) = [X(d) | s alpha] (rest of the row 0).
 __global__ void k_pack1(Geo g, const float* __restrict__ X, const double* __restrict__ alpha,
                         const double* __restrict__ R, double s, const float* __restrict__ qscale,
                         const float* __restrict__ colscale_inv, uint8_t* __restrict__ out) {
@@ -125,7 +125,6 @@ __global__ void k_pack1(Geo g, const float* __restrict__ X, const double* __rest
     if (n < g.N) {
       if (f < g.d) v = X[(size_t)n * g.d + f];  // raw X: the exponent differences before scaling
       else if (f == g.d) v = (float)(s * alpha[n]);
-      else if (f < 2 * g.d + 1) v = (float)(s * alpha[n] * (double)X[(size_t)n * g.d + f - g.d - 1]);
     } else if (f < g.d) {
       v = 1e18f;  // padded training point: infinitely far, ktilde = 0
     }
@@ -399,7 +398,7 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
                                         uint8_t* sm, P1Shared<D>& sh, const uint32_t tmem) {
   const Geo& g = a.g;
   const int NZ = g.NZ;
-  constexpr int NAUX = 2 * D + 1;
+  constexpr int NAUX = D + 1;  // X_n (d) | s alpha_n
   const size_t b_bytes = (size_t)4 * NZ * KT1;   // B hi + lo of one tile
   const size_t x_bytes = (size_t)KT1 * AUXW * 4; // aux rows of one tile
   uint8_t* bsm = sm;                             // ST1 x (B hi | B lo)
@@ -543,16 +542,22 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         // training points e and e + 1 of this thread's 8 as the two lanes of fp32x2 operations
         float2 an[NAUX];
         load_aux2<NAUX>(aux + ((qd * 8 + e) >> 1) * (2 * AUXW), an);
-        float2 q = make_float2(0.0f, 0.0f);
+        float2 q = make_float2(0.0f, 0.0f), dx[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const float2 df = mul2(sub2(make_float2(xq[c], xq[c]), an[c]), make_float2(sc[c], sc[c]));
+          dx[c] = sub2(make_float2(xq[c], xq[c]), an[c]);  // x*_c - X_nc
+          const float2 df = mul2(dx[c], make_float2(sc[c], sc[c]));
           q = fma2(df, df, q);
         }
         const float2 kt = make_float2(ex2_approx(-q.x), ex2_approx(-q.y));
+        // mean column and the mean Jacobian in difference form: sum_n s k_n alpha_n (x*_c - X_nc)
+        // (no x* mu - sum k alpha X_c cancellation between two large sums)
+        // mu keeps the fused k * (s alpha) + acc (one rounding per term: the mean is the most
+        // cancellation-sensitive output); the Jacobian columns take the rounded product
         hacc2[0] = fma2(kt, an[D], hacc2[0]);
+        const float2 ka = mul2(kt, an[D]);
 #pragma unroll
-        for (int c = 0; c < D; ++c) hacc2[1 + c] = fma2(kt, an[D + 1 + c], hacc2[1 + c]);
+        for (int c = 0; c < D; ++c) hacc2[1 + c] = fma2(ka, dx[c], hacc2[1 + c]);
         const __half2 h2 = __floats2half2_rn(kt.x, kt.y);
         const float2 res = sub2(kt, __half22float2(h2));
         const __half2 l2 = __floats2half2_rn(res.x, res.y);
@@ -744,7 +749,7 @@ __device__ __forceinline__ void p1_reduce(const P1Args& a, const int bx, const i
       }
       if (jmu && lane >= 1 && lane <= D)
         jmu[((size_t)row * g.p + mm) * D + lane - 1] =
-            (hv - a.xstar[(size_t)row * D + lane - 1] * h0) * a.ell2inv[mm][lane - 1];
+            -hv * a.ell2inv[mm][lane - 1];  // J^mu_c = -(1/l_c^2) sum_n s k alpha (x*_c - X_nc)
       // packed pass-2 A operand (see k_r1b_tc): columns 4l.. of group l/2 (half l%2) and
       // 128+4l.. of group 16 + l/2; lo groups follow the KJ/8 hi groups
       const int rrow = row % 128;
@@ -941,7 +946,7 @@ __global__ void __launch_bounds__(256) k_r1b_tc(R1Args a, const double* __restri
       if (a.jmu)
 #pragma unroll
         for (int c = 0; c < D; ++c)
-          a.jmu[((size_t)row * g.p + m) * D + c] = (h[1 + c] - a.xstar[(size_t)row * D + c] * h[0]) * a.ell2inv[m][c];
+          a.jmu[((size_t)row * g.p + m) * D + c] = -h[1 + c] * a.ell2inv[m][c];
     }
     scale_s[lane] = sc;
   }
@@ -1198,16 +1203,18 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
         // columns u, u + 1 as the two lanes of fp32x2 operations
         float2 an[NAUX];
         load_aux2<NAUX>(aux + ((cg * 32 + u) >> 1) * (2 * AUXW), an);
-        float2 q = make_float2(0.0f, 0.0f);
+        float2 q = make_float2(0.0f, 0.0f), dx[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          const float2 df = mul2(sub2(make_float2(xq[c], xq[c]), an[c]), make_float2(sc[c], sc[c]));
+          dx[c] = sub2(make_float2(xq[c], xq[c]), an[c]);  // x*_c - X_nc
+          const float2 df = mul2(dx[c], make_float2(sc[c], sc[c]));
           q = fma2(df, df, q);
         }
         const float2 t = mul2(mul2(make_float2(w[u], w[u + 1]), an[D]), make_float2(ex2_approx(-q.x), ex2_approx(-q.y)));
         acc2[0] = add2(acc2[0], t);
+        // difference form: sum_n (s w_n k_n) (x*_c - X_nc)
 #pragma unroll
-        for (int c = 0; c < D; ++c) acc2[1 + c] = fma2(t, an[c], acc2[1 + c]);
+        for (int c = 0; c < D; ++c) acc2[1 + c] = fma2(t, dx[c], acc2[1 + c]);
       }
       __threadfence_block();  // every aux load above has returned before the stage is released
       tc::mbar_arrive(&empty_x[x]);

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp_bwd(PolicyDesc P, RewardDes
                                                          const float* __restrict__ goals, int B,
                                                          const float* __restrict__ x_t, const float* __restrict__ A_t,
                                                          const float* __restrict__ act_t,
-                                                         float* __restrict__ delta_t, float invB,
+                                                         float* __restrict__ delta_t, float invB, float carry,
                                                          float* __restrict__ xbar) {
   extern __shared__ __align__(16) float sm[];
   float* Da = sm;                    // MLP_RB x MLP_LD: the current delta
@@ -268,7 +268,8 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp_bwd(PolicyDesc P, RewardDes
       float hb = dc[r * MLP_LD + c];
       if (P.phi_mode == 1) hb -= dc[r * MLP_LD + 2 * p + c];
       const float df = x_t[(size_t)b * p + c] - goals[(size_t)b * p + c];
-      xbar[(size_t)b * p + c] += xs_s[r][c] + hb + invB * rr * rw.Q[c] * df * inv_sr2;
+      // carry = 1 for Delta targets, 0 for absolute targets (NEXT-4)
+      xbar[(size_t)b * p + c] = carry * xbar[(size_t)b * p + c] + xs_s[r][c] + hb + invB * rr * rw.Q[c] * df * inv_sr2;
     }
   }
 }
@@ -324,7 +325,7 @@ int mlp_reverse(const bagel_ctx* c, const float* theta, const float* goals, int 
     DISPATCH_D(d, (k_mlp_bwd<D><<<cdiv(B, MLP_RB), MLP_THREADS, mlp_smem(), st>>>(
                       c->pol, c->rw, p, theta, goals, B, w.tape_x + (size_t)t * B * p,
                       w.tape_A + (size_t)t * B * p * d, w.tape_act + (size_t)t * B * c->pol.act_ld,
-                      w.tape_delta + (size_t)t * B * c->pol.d_ld, invB, w.xbar)));
+                      w.tape_delta + (size_t)t * B * c->pol.d_ld, invB, c->gp.abs_target ? 0.0f : 1.0f, w.xbar)));
   }
   return 1 + T;
 }

@@ -161,7 +161,7 @@ __device__ void epi_pre(const EpiArgs& e, const int t, int b0, int nr, float* sc
     const float sg = fabsf(sgr);
     const float ep = bagel_f4get(e4, m & 3);
     const float mum = e.mu[(size_t)m * B + b];
-    const float xn = tape_x_t[(size_t)b * p + m] + mum + sg * ep;
+    const float xn = (e.g.abs_target ? 0.0f : tape_x_t[(size_t)b * p + m]) + mum + sg * ep;
     if (!isfinite(xn)) atomicMin(e.err_flag, t * B + b);
     tape_x_next[(size_t)b * p + m] = xn;
     sc.xn_s[r * p + m] = xn;
@@ -213,13 +213,14 @@ __device__ void epi_post(const EpiArgs& e, const int t, int b0, int nr, const fl
     }
   }
   __syncwarp();
-  // J^v from the (r, m) row of sums [sum w k | sum w k X_c]; tape A = J^mu + f J^v (reverse input)
+  // J^v from the (r, m) row of sums [sum w k | sum w k (x*_c - X_c)]; tape A = J^mu + f J^v (reverse input)
   for (int li = lane; li < nl; li += 32) {
     const int r = li / per_row, m = (li % per_row) / (D + 1), c = li % (D + 1);
     if (c == 0) continue;
     const int b = b0 + r;
-    const float s0 = sc.psum[li - c], part = sc.psum[li];
-    const float jv = 2.0f * e.g.ell2inv[m][c - 1] * (sc.xq[r * BAGEL_MAX_D + c - 1] * s0 - part);
+    // part = sum_n w_n k_n (x*_c - X_nc) (difference form)
+    const float part = sc.psum[li];
+    const float jv = 2.0f * e.g.ell2inv[m][c - 1] * part;
     const size_t o = ((size_t)b * p + m) * D + c - 1;
     jv_t[o] = jv;
     A_t[o] = fmaf(sc.f_s[r * p + m], jv, sc.jmu[r * BAGEL_MAX_P * BAGEL_MAX_D + m * D + c - 1]);

@@ -170,7 +170,7 @@ template <int D, bool STAGED>
 __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     PolicyDesc P, RewardDesc rw, int p, const float* __restrict__ theta, const float* __restrict__ goals, int B,
     int T, const float* __restrict__ tape_x, const float* __restrict__ tape_A, const float* __restrict__ tape_act,
-    float* __restrict__ tape_delta, float invB, unsigned long long* __restrict__ dbg) {
+    float* __restrict__ tape_delta, float invB, float carry, unsigned long long* __restrict__ dbg) {
   extern __shared__ __align__(16) float sm[];
   constexpr bool staged = STAGED;  // (a compile-time choice: shared-memory W reads stay LDS)
   const int np4 = staged ? rev2_wt_floats(P) : 0;
@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
     float qd = lane < p ? rw.Q[lane] * (xt - gl) * (xt - gl) : 0.0f;
     for (int o = 16; o > 0; o >>= 1) qd += __shfl_xor_sync(0xffffffffu, qd, o);
     const float rr = expf(-qd * rw.inv_two_sr2);
-    if (lane < p) xb += xs + hb_phi + invB * rr * rw.Q[lane] * (xt - gl) * inv_sr2;
+    // carry = 1 for Delta targets (dx'/dx = I + ...), 0 for absolute targets (NEXT-4)
+    if (lane < p) xb = carry * xb + xs + hb_phi + invB * rr * rw.Q[lane] * (xt - gl) * inv_sr2;
     __syncwarp();
     if (stampit) dbg[8] = gtimer_ro();
   }
@@ -679,11 +680,11 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
   if (rev2_theta_staged(c->pol, c->gp.p, c->gp.d)) {
     DISPATCH_D(c->gp.d, (k_reverse2<D, true><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, smem, st>>>(
                             c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
-                            invB, c->tcs.dbg3)));
+                            invB, c->gp.abs_target ? 0.0f : 1.0f, c->tcs.dbg3)));
   } else {
     DISPATCH_D(c->gp.d, (k_reverse2<D, false><<<cdiv(B, REV2_WARPS), 32 * REV2_WARPS, smem, st>>>(
                             c->pol, c->rw, c->gp.p, theta, goals, B, T, w.tape_x, w.tape_A, w.tape_act, w.tape_delta,
-                            invB, c->tcs.dbg3)));
+                            invB, c->gp.abs_target ? 0.0f : 1.0f, c->tcs.dbg3)));
   }
   *nblk_out = ro_theta_blocks(c, B, T);
   return 1;

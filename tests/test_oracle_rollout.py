@@ -188,3 +188,49 @@ def test_thread_count_independence(boom_small):
     finally:
         O.set_num_threads(n0)
     assert a["cost"] == b["cost"] and np.array_equal(a["grad"], b["grad"])
+
+
+def test_scalar_rollout_closed_form_absolute_targets():
+    """Absolute targets (y = x_{k+1}; NEXT-4): N=1, p=q=1, zero policy:
+    x_{t+1} = k(x_t) y1/(s+sn2) + sqrt(s - k(x_t)^2/(s+sn2)) eps_t (no x_t carried)."""
+    X = np.array([[0.3, -0.2]])
+    y = np.array([[0.05]])
+    ell = np.array([[0.8, 0.6]])
+    s, sn2 = 0.04, 0.004
+    mdl = O.Model.build(X, y, ell, [s], [sn2], 1, abs_target=True)
+    sizes = (2, 3, 1)
+    out = O.rollout(mdl, sizes, "xg", np.zeros(W.n_params(sizes)), np.array([10.0]), 1.0, np.array([[-0.5]]),
+                    np.array([[0.4]]), 9, 0x5EED0043, traj_offset=3, B_global=1, trace=True)
+    key = [0x5EED0043, 0]
+    x = -0.5
+    G = math.exp(-5.0 * (x - 0.4) ** 2)
+    for t in range(9):
+        o = O.philox4x32_10([3, t, 0, 0], key)
+        u0, u1 = [((int(v) >> 9) + 0.5) * 2.0 ** -23 for v in o[:2]]
+        eps = math.sqrt(-2.0 * math.log(u0)) * math.cos(2.0 * math.pi * u1)
+        k = s * math.exp(-0.5 * (((x - 0.3) / 0.8) ** 2 + ((0.0 + 0.2) / 0.6) ** 2))
+        x = k * 0.05 / (s + sn2) + math.sqrt(s - k * k / (s + sn2)) * eps
+        assert out["x"][t + 1, 0, 0] == pytest.approx(x, rel=1e-11, abs=1e-14)
+        G += math.exp(-5.0 * (x - 0.4) ** 2)
+    assert out["cost"] == pytest.approx(-G, rel=1e-11)
+
+
+def test_gradient_directional_fd_absolute_targets():
+    wl = W.make_workload(plant="boom", N=150, rank=48, hidden=(16, 16), B=8, T=15, data_seed=2, target="abs")
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank, abs_target=True)
+    goals = (wl.x0 + np.array([0.4, -0.2], dtype=np.float32)).astype(np.float32)
+    base = _run(wl, mdl, goals=goals)
+    th = wl.theta.astype(np.float64)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        dirv = rng.normal(size=th.size)
+        dirv /= np.linalg.norm(dirv)
+        h = 1e-5
+        fp = _run(wl, mdl, theta=th + h * dirv, goals=goals, want_grad=False)["cost"]
+        fm = _run(wl, mdl, theta=th - h * dirv, goals=goals, want_grad=False)["cost"]
+        fd = (fp - fm) / (2 * h)
+        an = float(base["grad"] @ dirv)
+        assert abs(an - fd) <= 1e-6 * max(abs(fd), 1e-3 * np.linalg.norm(base["grad"]))
+    # and it is a different dynamics from the Delta form on the same data
+    mdl_d = O.Model(mdl.X, mdl.ell, mdl.s, mdl.alpha, mdl.R, abs_target=False)
+    assert abs(_run(wl, mdl_d, goals=goals)["cost"] - base["cost"]) > 1e-3

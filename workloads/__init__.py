@@ -179,8 +179,9 @@ def he_init(sizes, seed: int = 3) -> np.ndarray:
     return np.concatenate(parts).astype(np.float32)
 
 
-def make_dataset(plant: str, N: int, seed: int = 0):
-    """Simulate, standardise and build (X, Y, hyperparameters).  Returns float32 arrays."""
+def make_dataset(plant: str, N: int, seed: int = 0, target: str = "delta"):
+    """Simulate, standardise and build (X, Y, hyperparameters).  Returns float32 arrays.
+    target "delta": y = Delta x (reading R6); "abs": y = x_{k+1}, both in normalised units."""
     rng = np.random.default_rng(seed)
     obs, act = PLANTS[plant](N, rng)
     states, nxt = obs[:-1], obs[1:]
@@ -190,7 +191,7 @@ def make_dataset(plant: str, N: int, seed: int = 0):
     sd[sd < 1e-8] = 1.0
     X = (raw - mu) / sd
     p = states.shape[1]
-    Y = (nxt - states) / sd[:p]
+    Y = (nxt - states) / sd[:p] if target == "delta" else (nxt - mu[:p]) / sd[:p]
     q = act.shape[1]
     s = Y.var(axis=0)
     noise = 1e-2 * s
@@ -205,10 +206,10 @@ def make_dataset(plant: str, N: int, seed: int = 0):
 
 def make_workload(name: str = "custom", plant: str = "boom", N: int = 5000, rank: int = 256,
                   hidden=(64, 64), B: int = 1024, T: int = 100, phi_mode: str = "xg",
-                  data_seed: int = 0, fixed_start: bool = False) -> Workload:
+                  data_seed: int = 0, fixed_start: bool = False, target: str = "delta") -> Workload:
     """Build a workload.  phi_mode 'xg' -> policy input [x, g] (in = 2p);
     'xgd' -> [x, g, g - x] (in = 3p, C1)."""
-    X, Y, ell, s, noise, norm = make_dataset(plant, N, data_seed)
+    X, Y, ell, s, noise, norm = make_dataset(plant, N, data_seed, target)
     p = Y.shape[1]
     q = X.shape[1] - p
     n_in = 2 * p if phi_mode == "xg" else 3 * p
