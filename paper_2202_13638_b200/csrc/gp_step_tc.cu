@@ -40,6 +40,7 @@ constexpr int KS2 = 64;      // j per pass-2 K slab (one pipeline stage)
 constexpr int ST2 = 6;       // pass-2 slab ring stages (Z lives in TMEM)
 constexpr int STX2 = 2;      // pass-2 aux ring stages (one per tile)
 constexpr int STA = 8;       // pass-1 aux (per-n side data) ring stages
+constexpr int P1_MAX_TILES = 64;  // longest pass-1 accumulation chain (N-tiles of KT1 points per split)
 constexpr int CTRL_WARPS = 3; // B producer, MMA issuer, aux producer
 constexpr int GEN_WARPS = 16; // generator / epilogue warps (4 per TMEM lane quarter)
 constexpr int THREADS = 32 * CTRL_WARPS + 32 * GEN_WARPS;
@@ -1377,6 +1378,11 @@ void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, in
   const int rt = cdiv(B, 128);
   const int target = c->num_sms;  // one CTA per SM (smem-bound), one wave
   int s1 = target / (rt * g.p * g.nct);  // floor: never more CTAs than SMs (one wave)
+  // ... but never a longer tcgen05 accumulation chain than P1_MAX_TILES N-tiles per TMEM
+  // accumulator: the tensor core's fp32 accumulation error grows with the chain length (measured:
+  // the whole N = 50,000 in one chain put ||z||^2 off by 4e-4 s, 1.5x the fp32 tolerance; DESIGN.md
+  // §7), so long ranges are split and the partials summed on the CUDA cores (multi-wave grids)
+  s1 = s1 < cdiv(g.nt1, P1_MAX_TILES) ? cdiv(g.nt1, P1_MAX_TILES) : s1;
   s1 = s1 < 1 ? 1 : (s1 > g.nt1 ? g.nt1 : s1);
   *tps1 = cdiv(g.nt1, s1);
   *S1 = cdiv(g.nt1, *tps1);
