@@ -97,3 +97,80 @@ def test_allreduce_is_identity_without_process_group():
     g = torch.arange(5, dtype=torch.float32)
     c, g2 = allreduce_cost_grad(1.5, g)
     assert c == 1.5 and g2 is g
+
+
+class _OracleCtx:
+    """Stand-in for bagel.Context on CPU (test-only): the oracle's sampler, rollout and Adam behind the
+    methods train.train_policy calls, so the loop's sharding and all_reduce are exercised without a GPU."""
+
+    def __init__(self, mdl, wl):
+        self.mdl, self.wl = mdl, wl
+        self.dev = torch.device("cpu")
+
+    def sample_states(self, seed, off, B, lo, hi, which=0, out=None):
+        import oracle as O
+
+        out.copy_(torch.from_numpy(O.sample_states(seed, off, B, lo, hi, which).astype(np.float32)))
+        return out
+
+    def rollout_cost_and_grad(self, theta, x0, goals, T, seed, traj_offset=0, B_global=None, grad=None):
+        import oracle as O
+
+        r = O.rollout(self.mdl, self.wl.sizes, "xg", theta.double().numpy(), self.wl.Q, self.wl.sigma_r,
+                      x0.double().numpy(), goals.double().numpy(), T, seed, traj_offset=traj_offset,
+                      B_global=B_global)
+        grad.copy_(torch.from_numpy(r["grad"]))
+        return r["cost"], grad
+
+    def adam_step(self, params, grad, m1, m2, step, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, report_skip=False):
+        import oracle as O
+
+        th, g = params.double().numpy().copy(), grad.double().numpy().copy()
+        a, b = m1.double().numpy().copy(), m2.double().numpy().copy()
+        skipped = O.adam_step(th, g, a, b, step, lr, beta1, beta2, eps)
+        params.copy_(torch.from_numpy(th))
+        m1.copy_(torch.from_numpy(a))
+        m2.copy_(torch.from_numpy(b))
+        return skipped
+
+
+def _train_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_13638_b200.train import train_policy
+
+        wl, _, mdl = _problem()
+        lo, hi = wl.X[:, :wl.p].min(0), wl.X[:, :wl.p].max(0)
+        th, log = train_policy(_OracleCtx(mdl, wl), wl.theta, wl.T, 4, wl.B, lo, hi, lr=1e-2, seed0=0x5EED2000)
+        q.put((rank, log.cost, th.double().numpy()))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_two_rank_training_loop_equals_single_process():
+    """Algorithm 1's loop (train.train_policy) at world size 2: each rank samples and rolls out its own
+    trajectory block, one all_reduce per iteration, identical replicated Adam updates -- equal to the
+    single-process oracle loop (O.train) on the whole batch."""
+    import oracle as O
+
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_train_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    wl, _, mdl = _problem()
+    lo, hi = wl.X[:, :wl.p].min(0), wl.X[:, :wl.p].max(0)
+    th_ref, costs_ref = O.train(mdl, wl.sizes, "xg", wl.theta, wl.Q, wl.sigma_r, wl.T, 4, wl.B, lo, hi, 0x5EED2000,
+                                lr=1e-2)
+    (_, c0, t0), (_, c1, t1) = sorted(res, key=lambda r: r[0])
+    assert np.array_equal(t0, t1)  # replicated parameters stay identical on every rank
+    np.testing.assert_allclose(c0, costs_ref, rtol=1e-5)
+    np.testing.assert_allclose(t0, th_ref, rtol=1e-5, atol=1e-6)
