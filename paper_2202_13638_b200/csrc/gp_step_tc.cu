@@ -40,7 +40,7 @@ constexpr int KS2 = 64;      // j per pass-2 K slab (one pipeline stage)
 constexpr int ST2 = 6;       // pass-2 slab ring stages (Z lives in TMEM)
 constexpr int STX2 = 2;      // pass-2 aux ring stages (one per tile)
 constexpr int STA = 8;       // pass-1 aux (per-n side data) ring stages
-constexpr int P1_MAX_TILES = 64;  // longest pass-1 accumulation chain (N-tiles of KT1 points per split)
+constexpr int P1_MAX_TILES = 80;  // longest pass-1 accumulation chain (N-tiles of KT1 points per split; C3 keeps S1 = 2)
 constexpr int CTRL_WARPS = 3; // B producer, MMA issuer, aux producer
 constexpr int GEN_WARPS = 16; // generator / epilogue warps (4 per TMEM lane quarter)
 constexpr int THREADS = 32 * CTRL_WARPS + 32 * GEN_WARPS;

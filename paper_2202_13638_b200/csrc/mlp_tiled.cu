@@ -79,6 +79,31 @@ __device__ __forceinline__ void tile_gemm(const float* __restrict__ W, int K, in
     const int k0 = c * MLP_KC, kc = min(MLP_KC, K - k0);
     const float* buf = Ws + (c & 1) * (BAGEL_MAX_WIDTH * MLP_WK);
     int kk = 0;
+    if (kc == MLP_KC) {
+      // full chunk: compile-time trip count, fully unrolled so the next k-group's shared-memory
+      // loads are issued ahead of the current FMAs (the kernel is shared-memory-latency bound at
+      // 8 warps per SM); same FMA order as the general loop below
+#pragma unroll
+      for (int k4 = 0; k4 < MLP_KC; k4 += 4) {
+        float4 h[4], w[8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) h[r] = *reinterpret_cast<const float4*>(Hin + (4 * ty + r) * MLP_LD + k0 + k4);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          w[j] = tx + 32 * j < NO ? *reinterpret_cast<const float4*>(buf + (tx + 32 * j) * MLP_WK + k4)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc[r][j] = fmaf(h[r].x, w[j].x, acc[r][j]);
+            acc[r][j] = fmaf(h[r].y, w[j].y, acc[r][j]);
+            acc[r][j] = fmaf(h[r].z, w[j].z, acc[r][j]);
+            acc[r][j] = fmaf(h[r].w, w[j].w, acc[r][j]);
+          }
+      }
+      kk = kc;
+    }
     for (; kk + 4 <= kc; kk += 4) {
       float4 h[4], w[8];
 #pragma unroll
