@@ -438,3 +438,31 @@ def test_c4_shape_four_outputs_rank_512(bagel):
     seed = W.rollout_seed(4)
     cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), "C4 shape")
+
+
+def test_maximum_sizes(bagel):
+    """The ABI's limits at once: p = 4 outputs, d = 8 inputs (q = 4 actions), LOVE rank 768
+    (BAGEL_MAX_RANK: three 256-column z tiles, three j tiles), 256-wide policy layers, ragged B."""
+    from conftest import small_gp_data
+
+    rng = np.random.default_rng(11)
+    N, d, p = 1000, 8, 4
+    X, Y, ell, s, noise = small_gp_data(N=N, d=d, p=p, seed=11)
+    sizes = (2 * p, 256, 256, d - p)
+    wl = W.Workload(name="max", plant="synthetic", N=N, p=p, q=d - p, rank=768, sizes=sizes, B=130, T=3,
+                    X=X.astype(np.float32), Y=Y.astype(np.float32), ell=ell.astype(np.float32),
+                    s=s.astype(np.float32), noise=noise.astype(np.float32),
+                    Q=np.array([10.0, 0.1, 1.0, 1.0], dtype=np.float32))
+    wl.x0 = rng.uniform(-1, 1, (130, p)).astype(np.float32)
+    wl.goals = (wl.x0 + 0.3).astype(np.float32)
+    wl.theta = W.he_init(sizes, 4)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    assert ctx.gp_kernel() == 1
+    xs = rng.uniform(-2, 2, (130, d)).astype(np.float32)
+    print("max sizes worst error / tolerance:",
+          _check_predict(wl, mdl, *ctx.gp_predict(torch.from_numpy(xs).cuda()), xs.astype(np.float64)))
+    seed = W.rollout_seed(6)
+    cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), "max sizes")
