@@ -36,6 +36,10 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
@@ -52,10 +56,17 @@ __device__ __forceinline__ void tile_gemm(const float* __restrict__ W, int K, in
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[r][j] = 0.0f;
   const int nch = (K + MLP_KC - 1) / MLP_KC;
+  // 16-byte copies need every row start 16-byte aligned
+  const bool vec16 = (in % 4 == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
   auto stage = [&](int c) {
     const int k0 = c * MLP_KC, kc = min(MLP_KC, K - k0);
     float* buf = Ws + (c & 1) * (BAGEL_MAX_WIDTH * MLP_WK);
-    if (FWD) {
+    if (FWD && kc == MLP_KC && vec16) {
+      // W[o][k] rows of 32 k as 8 x 16-byte copies: a warp covers 4 rows per instruction
+      const int r4 = tx / 8, c4 = (tx % 8) * 4;
+      for (int o = 4 * ty + r4; o < NO; o += 4 * (MLP_THREADS / 32))
+        cp_async16(buf + o * MLP_WK + c4, W + (size_t)o * in + k0 + c4);
+    } else if (FWD) {
       // W[o][k]: lane = k (coalesced 128-byte rows), warps step over o
       if (tx < kc)
         for (int o = ty; o < NO; o += MLP_THREADS / 32) cp_async4(buf + o * MLP_WK + tx, W + (size_t)o * in + k0 + tx);
@@ -213,7 +224,7 @@ __global__ void k_xbar_init(RewardDesc rw, int p, const float* __restrict__ xT, 
 // One reverse step t for rows b0 .. b0 + MLP_RB - 1 (xbar: B x p, updated in place).
 template <int D>
 __global__ void __launch_bounds__(MLP_THREADS) k_mlp_bwd(PolicyDesc P, RewardDesc rw, int p,
-                                                         const float* __restrict__ theta,
+                                                         const float* __restrict__ thetaT,  // per-layer W_l^T (k_transpose_theta)
                                                          const float* __restrict__ goals, int B,
                                                          const float* __restrict__ x_t, const float* __restrict__ A_t,
                                                          const float* __restrict__ act_t,
@@ -257,7 +268,10 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp_bwd(PolicyDesc P, RewardDes
     }
     // hbar[r][i] = sum_o delta[r][o] W_l[o][i]
     float acc[4][8];
-    tile_gemm<false>(theta + P.w_off[l], out, in, in, dc, Ws, acc);
+    // hbar = delta W_l = delta (W_l^T)^T: the forward-form GEMM on thetaT's W_l^T rows (in x out,
+    // contiguous over o) -- coalesced, bank-conflict-free weight staging (the transposed staging
+    // of theta was an 8-way shared-memory bank conflict per cp.async)
+    tile_gemm<true>(thetaT + P.w_off[l], out, in, out, dc, Ws, acc);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int i = tx + 32 * j;
@@ -348,7 +362,7 @@ int mlp_reverse(const bagel_ctx* c, const float* theta, const float* goals, int 
   k_xbar_init<<<cdiv(B, 128), 128, 0, st>>>(c->rw, p, w.tape_x + (size_t)T * B * p, goals, B, invB, w.xbar);
   for (int t = T - 1; t >= 0; --t) {
     DISPATCH_D(d, (k_mlp_bwd<D><<<cdiv(B, MLP_RB), MLP_THREADS, mlp_smem(), st>>>(
-                      c->pol, c->rw, p, theta, goals, B, w.tape_x + (size_t)t * B * p,
+                      c->pol, c->rw, p, w.thetaT, goals, B, w.tape_x + (size_t)t * B * p,
                       w.tape_A + (size_t)t * B * p * d, w.tape_act + (size_t)t * B * c->pol.act_ld,
                       w.tape_delta + (size_t)t * B * c->pol.d_ld, invB, c->gp.abs_target ? 0.0f : 1.0f, w.xbar)));
   }
