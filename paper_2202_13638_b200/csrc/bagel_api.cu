@@ -152,6 +152,8 @@ void free_workspace(bagel_ctx* c) {
   dev_free(w.theta_part); dev_free(w.grad_tmp); dev_free(w.thetaT); dev_free(w.cost_dev); dev_free(w.err_flag);
   dev_free(c->tcs.P1z); dev_free(c->tcs.P1h); dev_free(c->tcs.Zp); dev_free(c->tcs.zrow_inv);
   dev_free(c->tcs.zz_part); dev_free(c->tcs.zmax_part);
+  dev_free(w.mlp_wpk);
+  w.mlp_wpk_cap = 0;
   w.B = w.T = 0;
   w.S1 = w.S2 = 0;
   w.theta_part_cap = 0;
@@ -325,6 +327,12 @@ int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goal
   int launches = 0;
   CK(cudaMemsetAsync(w.err_flag, 0x7f, sizeof(int), st));
   launches += timed(c, PC_INIT, [&] { return ro_init(c, theta, x0, goals, B, st); });
+  if (ro_wide_policy(c->pol) && mlp_tc_enabled(c)) {
+    // wide policies: this iteration's weights as the tensor-core MLP's hi/lo operand (mlp_tc.cu)
+    const int r = mlp_tc_pack(c, theta, st);
+    REQUIRE(r > 0, BAGEL_E_CUDA, "rollout: out of device memory for the packed policy weights");
+    launches += r;
+  }
   const bool tc = use_tc(c);
   w.S2eff = tc ? w.S2tc * tc_njt(c) : w.S2;
   const bool fuse_epi = tc && tc_pass2_epi_ok(c, B);

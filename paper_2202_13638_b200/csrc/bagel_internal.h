@@ -135,6 +135,8 @@ struct Workspace {
   // host staging of [dev|host] inputs
   float* stage = nullptr;
   size_t stage_cap = 0;
+  uint8_t* mlp_wpk = nullptr;   // wide policies: packed hi/lo weight chunks of the tensor-core MLP (mlp_tc.cu)
+  size_t mlp_wpk_cap = 0;
 };
 
 struct bagel_ctx {
@@ -252,6 +254,9 @@ int ro_philox_normals(uint64_t seed, long long traj_offset, int B, int T, int p,
                       cudaStream_t st);
 int ro_theta_blocks(const bagel_ctx* c, int B, int T);
 bool ro_wide_policy(const PolicyDesc& P);
+bool mlp_tc_enabled(const bagel_ctx* c);
+int mlp_tc_pack(bagel_ctx* c, const float* theta, cudaStream_t st);
+int mlp_tc_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st);
 int mlp_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st);
 int mlp_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B, int T, long long B_global,
                 cudaStream_t st);

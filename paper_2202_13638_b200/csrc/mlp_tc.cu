@@ -1,0 +1,323 @@
+// mlp_tc.cu -- the per-step policy forward (a1; tanh hidden and output, R13/R14)
+// of WIDE policies (C3: 4-256-256-256-1) on the 5th-generation tensor cores.
+//
+// One CTA owns 128 trajectories and runs every layer for them:
+//   D[128 x out] = H[128 x in] . W_l^T  on tcgen05 (kind::f16, fp32 TMEM accumulator), with the same
+//   3-pass fp16 split as the GP contraction (h = h_hi + h_lo, W = W_hi + W_lo;
+//   h.W ~ h_hi W_hi + h_hi W_lo + h_lo W_hi, fp32-class accuracy, tests/test_gpu_tc.py),
+//   then bias + tanh in the epilogue, which also writes the activation tape and places the next
+//   layer's input H (hi | lo, fp16 pairs) straight into TMEM as the A operand of the next layer's
+//   TS-form MMAs.  The weights are packed once per rollout (k_pack_mlp) into K-chunks of the
+//   canonical no-swizzle K-major layout (tc.cuh), streamed by 1-D bulk copies through a 3-stage
+//   ring.  TMEM: accumulator columns [0, 256), H hi [256, 384), H lo [384, 512).
+// Warps 0-15: epilogue (warp w: TMEM lane quarter w % 4, column group w / 4); warp 16: weight
+// producer; warp 17: MMA issuer.  Replaces the register-tiled fp32 GEMM k_mlp_fwd (mlp_tiled.cu),
+// which is shared-memory-latency bound at 8 warps per SM.
+#include <cuda_fp16.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "bagel_internal.h"
+#include "tc.cuh"
+
+namespace mtc {
+
+constexpr int ROWS = 128;
+constexpr int KCH = 64;          // K elements per pipeline stage
+constexpr int NST = 3;           // ring stages
+constexpr int EPI_WARPS = 16;    // 4 per TMEM lane quarter, each a quarter of the columns
+constexpr int THREADS = 32 * (EPI_WARPS + 2);
+constexpr int MAXCH = 32;        // chunks over all layers (8 layers x 4 chunks of 64)
+constexpr uint32_t ACC = 0, AHI = 256, ALO = 384;
+constexpr size_t STAGE_BYTES = (size_t)BAGEL_MAX_WIDTH * KCH * 2 * 2;  // hi + lo of 256 x 64 fp16
+
+struct Args {
+  PolicyDesc P;
+  int p, D, B;
+  const uint8_t* wpk;            // packed weight chunks
+  int nch;
+  int ch_layer[MAXCH], ch_k0[MAXCH], ch_kc[MAXCH];
+  long long ch_off[MAXCH];
+  int Np[BAGEL_MAX_LAYERS];      // out rounded up to 16 (>= 16)
+  const float* theta;            // biases
+  const float* x;                // B x p (this step's state)
+  const float* goals;            // B x p
+  float* act;                    // B x act_ld (this step's activation tape rows)
+  float* xstar;                  // B x D
+};
+
+inline int rup(int a, int b) { return (a + b - 1) / b * b; }
+
+// Chunk table of a policy (host): chunk q of layer l covers K elements [k0, k0 + kc) (kc a multiple
+// of 16), packed as [hi: Np x kc | lo: Np x kc] fp16 canonical K-major (KT = kc).
+void chunk_table(const PolicyDesc& P, Args& a, size_t* total) {
+  size_t off = 0;
+  a.nch = 0;
+  for (int l = 0; l < P.n_layers; ++l) {
+    const int Kp = rup(P.sizes[l], 16), Np = std::max(16, rup(P.sizes[l + 1], 16));
+    a.Np[l] = Np;
+    for (int k0 = 0; k0 < Kp; k0 += KCH) {
+      const int kc = std::min(KCH, Kp - k0);
+      a.ch_layer[a.nch] = l;
+      a.ch_k0[a.nch] = k0;
+      a.ch_kc[a.nch] = kc;
+      a.ch_off[a.nch] = (long long)off;
+      off += (size_t)Np * kc * 2 * 2;
+      ++a.nch;
+    }
+  }
+  *total = off;
+}
+
+__global__ void k_pack_mlp(Args a, const float* __restrict__ theta, uint8_t* __restrict__ wpk) {
+  const int q = blockIdx.y;
+  const int l = a.ch_layer[q], k0 = a.ch_k0[q], kc = a.ch_kc[q], Np = a.Np[l];
+  const int in = a.P.sizes[l], out = a.P.sizes[l + 1];
+  __half* hi = reinterpret_cast<__half*>(wpk + a.ch_off[q]);
+  __half* lo = hi + (size_t)Np * kc;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < Np * kc; idx += gridDim.x * blockDim.x) {
+    const int r = idx / kc, k = idx % kc, kg = k0 + k;
+    const float v = (r < out && kg < in) ? theta[a.P.w_off[l] + (size_t)r * in + kg] : 0.0f;
+    const __half h = __float2half_rn(v);
+    const __half e = __float2half_rn(v - __half2float(h));
+    const int ci = tc::canon_idx(r, k, kc);
+    hi[ci] = h;
+    lo[ci] = e;
+  }
+}
+
+// tanh with ~1e-7 absolute / few-ulp relative error at a third of tanhf's instructions: odd
+// Taylor polynomial for |v| < 1/8 (truncation < 1e-9 relative), else 1 - 2 / (e^{2v} + 1).
+__device__ __forceinline__ float tanh_fast(float v) {
+  const float a = fabsf(v);
+  if (a < 0.125f) {
+    const float v2 = v * v;
+    return v * fmaf(v2, fmaf(v2, fmaf(v2, -17.0f / 315.0f, 2.0f / 15.0f), -1.0f / 3.0f), 1.0f);
+  }
+  const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * a) + 1.0f);
+  return copysignf(t, v);
+}
+
+// hi/lo fp16 split of 2 consecutive K elements packed as one 32-bit TMEM word each
+__device__ __forceinline__ void split_pair(float v0, float v1, uint32_t& hw, uint32_t& lw) {
+  const __half2 h2 = __floats2half2_rn(v0, v1);
+  const float2 hf = __half22float2(h2);
+  const __half2 l2 = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+  hw = *reinterpret_cast<const uint32_t*>(&h2);
+  lw = *reinterpret_cast<const uint32_t*>(&l2);
+}
+
+__global__ void __launch_bounds__(THREADS, 1) k_mlp_fwd_tc(const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t full[NST], empty[NST], mma_done, a_ready;
+  __shared__ uint32_t tmem_base;
+  __shared__ float bias_s[BAGEL_MAX_LAYERS][BAGEL_MAX_WIDTH];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const PolicyDesc& P = a.P;
+  const int L = P.n_layers;
+  const int b0 = blockIdx.x * ROWS;
+  if (warp == EPI_WARPS + 1) tc::tmem_alloc(&tmem_base, 512);
+  for (int l = 0; l < P.n_layers; ++l)
+    for (int o = tid; o < P.sizes[l + 1]; o += THREADS) bias_s[l][o] = __ldg(a.theta + P.b_off[l] + o);
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&mma_done, 1);
+    tc::mbar_init(&a_ready, 32 * EPI_WARPS);
+    tc::fence_mbar_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == EPI_WARPS) {
+    // ------------------------------------------------ weight producer (static operand: starts now)
+    if (lane == 0) {
+      for (int q = 0; q < a.nch; ++q) {
+        const int s = q % NST;
+        tc::mbar_wait(&empty[s], ((uint32_t)(q / NST) & 1u) ^ 1u);
+        const uint32_t bytes = (uint32_t)a.Np[a.ch_layer[q]] * a.ch_kc[q] * 4u;
+        tc::mbar_arrive_expect_tx(&full[s], bytes);
+        tc::bulk_g2s(sm + (size_t)s * STAGE_BYTES, a.wpk + a.ch_off[q], bytes, &full[s]);
+      }
+    }
+  } else if (warp == EPI_WARPS + 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int q = 0;
+      for (int l = 0; l < L; ++l) {
+        tc::mbar_wait(&a_ready, (uint32_t)l & 1u);  // this layer's input H is in TMEM
+        tc::tc_fence_after();
+        const uint32_t idesc = tc::idesc_f16(ROWS, a.Np[l]);
+        bool first = true;
+        for (; q < a.nch && a.ch_layer[q] == l; ++q) {
+          const int s = q % NST, kc = a.ch_kc[q], k0 = a.ch_k0[q];
+          tc::mbar_wait(&full[s], (uint32_t)(q / NST) & 1u);
+          tc::tc_fence_after();
+          const uint32_t base = tc::smem_u32(sm + (size_t)s * STAGE_BYTES);
+          const uint32_t sbo = (uint32_t)(kc / 8) * 128u;
+          const uint64_t bhi = tc::umma_desc(base, 128, sbo);
+          const uint64_t blo = tc::umma_desc(base + (uint32_t)a.Np[l] * kc * 2u, 128, sbo);
+          for (int ks = 0; ks < kc / 16; ++ks) {
+            const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4
+            const uint32_t ac = (uint32_t)((k0 + 16 * ks) / 2);
+            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, bhi + o, idesc, first ? 0u : 1u);
+            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, blo + o, idesc, 1u);
+            tc::mma_f16_ts(tmem + ACC, tmem + ALO + ac, bhi + o, idesc, 1u);
+            first = false;
+          }
+          tc::umma_commit(&empty[s]);
+        }
+        tc::umma_commit(&mma_done);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps
+    const int quarter = warp % 4, half = warp / 4;  // half: column group 0..3
+    const int r = quarter * 32 + lane, b = b0 + r;
+    const bool ok = b < a.B;
+    const uint32_t tl = (uint32_t)(quarter * 32) << 16;
+    float* act = ok ? a.act + (size_t)b * P.act_ld : nullptr;
+    // layer-0 input phi = [x, g] or [x, g, g - x], zero-padded to 16 K elements
+    if (half == 0) {
+      const int n0 = P.sizes[0];
+      float ph[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float v = 0.0f;
+        if (ok && i < n0) {
+          if (i < a.p) v = a.x[(size_t)b * a.p + i];
+          else if (i < 2 * a.p) v = a.goals[(size_t)b * a.p + i - a.p];
+          else v = a.goals[(size_t)b * a.p + i - 2 * a.p] - a.x[(size_t)b * a.p + i - 2 * a.p];
+          act[P.aoff[0] + i] = v;
+        }
+        ph[i] = v;
+      }
+      uint32_t hw[8], lw[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) split_pair(ph[2 * e], ph[2 * e + 1], hw[e], lw[e]);
+      tc::tmem_st8(tmem + tl + AHI, hw);
+      tc::tmem_st8(tmem + tl + ALO, lw);
+      tc::tmem_st_wait();
+      if (ok)
+        for (int c = 0; c < a.p; ++c) a.xstar[(size_t)b * a.D + c] = a.x[(size_t)b * a.p + c];
+    }
+    tc::tc_fence_before();
+    tc::mbar_arrive(&a_ready);
+    for (int l = 0; l < L; ++l) {
+      const int out = P.sizes[l + 1], Np = a.Np[l];
+      const bool last = l == L - 1;
+      const float* bias = bias_s[l];
+      tc::mbar_wait(&mma_done, (uint32_t)l & 1u);
+      __syncwarp();
+      tc::tc_fence_after();
+      // this warp's columns: group `half` of 16-column chunks, chunk i going to group i % 4
+      const int c_begin = 16 * half, c_step = 64, c_end = Np;
+      for (int c0 = c_begin; c0 < c_end; c0 += c_step) {
+        float v[16];
+        tc::tmem_ld16(tmem + tl + ACC + (uint32_t)c0, v);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int o = c0 + i;
+          v[i] = o < out ? tanh_fast(v[i] + bias[o]) : 0.0f;
+        }
+        if (ok) {
+          if (c0 + 16 <= out && ((P.act_ld | P.aoff[l + 1]) & 3) == 0) {
+            float4* dst = reinterpret_cast<float4*>(act + P.aoff[l + 1] + c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < out) act[P.aoff[l + 1] + c0 + i] = v[i];
+          }
+          if (last)
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < out) a.xstar[(size_t)b * a.D + a.p + c0 + i] = v[i];
+        }
+        if (!last) {
+          uint32_t hw[8], lw[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) split_pair(v[2 * e], v[2 * e + 1], hw[e], lw[e]);
+          tc::tmem_st8(tmem + tl + AHI + (uint32_t)(c0 / 2), hw);
+          tc::tmem_st8(tmem + tl + ALO + (uint32_t)(c0 / 2), lw);
+        }
+      }
+      if (!last) {
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&a_ready);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == EPI_WARPS + 1) tc::tmem_dealloc(tmem, 512);
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      tc::mbar_inval(&full[s]);
+      tc::mbar_inval(&empty[s]);
+    }
+    tc::mbar_inval(&mma_done);
+    tc::mbar_inval(&a_ready);
+  }
+}
+
+size_t smem_bytes() { return NST * STAGE_BYTES; }
+
+}  // namespace mtc
+
+bool mlp_tc_enabled(const bagel_ctx* c) {
+  const char* env = getenv("BAGEL_MLP_TC");
+  if (env && env[0] == '0') return false;
+  int nch = 0;
+  for (int l = 0; l < c->pol.n_layers; ++l) nch += (c->pol.sizes[l] + 15) / 16 * 16 / mtc::KCH + 1;
+  return c->pol.sizes[0] <= 16 && nch <= mtc::MAXCH;
+}
+
+// Pack theta's weights into the chunked hi/lo operand (once per rollout; theta changes per iteration).
+int mlp_tc_pack(bagel_ctx* c, const float* theta, cudaStream_t st) {
+  mtc::Args a{};
+  a.P = c->pol;
+  size_t total = 0;
+  mtc::chunk_table(c->pol, a, &total);
+  if (c->ws.mlp_wpk_cap < total) {
+    if (c->ws.mlp_wpk) cudaFree(c->ws.mlp_wpk);
+    c->ws.mlp_wpk = nullptr;
+    c->ws.mlp_wpk_cap = 0;
+    if (cudaMalloc((void**)&c->ws.mlp_wpk, total) != cudaSuccess) return -1;
+    c->ws.mlp_wpk_cap = total;
+  }
+  mtc::k_pack_mlp<<<dim3(16, a.nch), 256, 0, st>>>(a, theta, c->ws.mlp_wpk);
+  return 1;
+}
+
+int mlp_tc_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mtc::k_mlp_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mtc::smem_bytes());
+    attr = true;
+  }
+  const Workspace& w = c->ws;
+  mtc::Args a{};
+  a.P = c->pol;
+  size_t total = 0;
+  mtc::chunk_table(c->pol, a, &total);
+  a.p = c->gp.p;
+  a.D = c->gp.d;
+  a.B = B;
+  a.wpk = w.mlp_wpk;
+  a.theta = theta;
+  a.x = w.tape_x + (size_t)t * B * a.p;
+  a.goals = goals;
+  a.act = w.tape_act + (size_t)t * B * c->pol.act_ld;
+  a.xstar = w.xstar;
+  mtc::k_mlp_fwd_tc<<<(B + mtc::ROWS - 1) / mtc::ROWS, mtc::THREADS, mtc::smem_bytes(), st>>>(a);
+  return 1;
+}

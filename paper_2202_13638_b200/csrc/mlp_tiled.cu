@@ -343,6 +343,7 @@ void mlp_set_attrs() {
 
 // Policy of step t for every row: x = tape_x[t]; writes tape_act[t] and x*.
 int mlp_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st) {
+  if (mlp_tc_enabled(c) && c->ws.mlp_wpk) return mlp_tc_forward_step(c, theta, goals, B, t, st);
   mlp_set_attrs();
   const Workspace& w = c->ws;
   const int p = c->gp.p;
