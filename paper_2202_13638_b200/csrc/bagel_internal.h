@@ -256,6 +256,7 @@ int ro_theta_blocks(const bagel_ctx* c, int B, int T);
 bool ro_wide_policy(const PolicyDesc& P);
 bool mlp_tc_enabled(const bagel_ctx* c);
 int mlp_tc_pack(bagel_ctx* c, const float* theta, cudaStream_t st);
+int mlp_tc_backward_step(const bagel_ctx* c, const float* goals, int B, int t, long long B_global, cudaStream_t st);
 int mlp_tc_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st);
 int mlp_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st);
 int mlp_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B, int T, long long B_global,

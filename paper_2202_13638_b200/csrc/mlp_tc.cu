@@ -269,6 +269,258 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_fwd_tc(const __grid_constant
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// The adjoint step of wide policies (a9) on the same machinery, per 128 rows:
+//   xs-bar = sum_m xbar_m A_t[m];  dl_{L-1} = xs-bar[p:] (1 - u^2);
+//   for l = L-1 .. 0:  hbar_l = dl_l W_l  (tcgen05: A = dl_l in TMEM, K = out_l; B = W_l^T rows,
+//                      N = in_l);  l > 0: dl_{l-1} = hbar_l (1 - h_l^2) (tape + next A), else
+//   xbar_t = carry xbar_{t+1} + xs-bar[:p] + dphi/dx^T hbar_0 + d(r_t / B)/dx_t.
+// Backward chunks follow the forward ones in the packed buffer, layers in reverse order:
+// B(r = i, k = o) = W_l[o][i], N = in_l rounded to 16 (>= 16), K = out_l rounded to 16.
+struct BArgs {
+  PolicyDesc P;
+  RewardDesc rw;
+  int p, D, B;
+  const uint8_t* wpk;
+  int nch;
+  int ch_layer[MAXCH], ch_k0[MAXCH], ch_kc[MAXCH];
+  long long ch_off[MAXCH];
+  int Np[BAGEL_MAX_LAYERS];
+  const float* goals;
+  const float* x_t;     // B x p
+  const float* A_t;     // B x p x D
+  const float* act_t;   // B x act_ld
+  float* delta_t;       // B x d_ld
+  float* xbar;          // B x p (in: t + 1, out: t)
+  float invB, carry;
+};
+
+void chunk_table_bwd(const PolicyDesc& P, BArgs& a, size_t base, size_t* total) {
+  size_t off = base;
+  a.nch = 0;
+  for (int l = P.n_layers - 1; l >= 0; --l) {
+    const int Kp = rup(P.sizes[l + 1], 16), Np = std::max(16, rup(P.sizes[l], 16));
+    a.Np[l] = Np;
+    for (int k0 = 0; k0 < Kp; k0 += KCH) {
+      const int kc = std::min(KCH, Kp - k0);
+      a.ch_layer[a.nch] = l;
+      a.ch_k0[a.nch] = k0;
+      a.ch_kc[a.nch] = kc;
+      a.ch_off[a.nch] = (long long)off;
+      off += (size_t)Np * kc * 2 * 2;
+      ++a.nch;
+    }
+  }
+  *total = off;
+}
+
+__global__ void k_pack_mlp_bwd(BArgs a, const float* __restrict__ theta, uint8_t* __restrict__ wpk) {
+  const int q = blockIdx.y;
+  const int l = a.ch_layer[q], k0 = a.ch_k0[q], kc = a.ch_kc[q], Np = a.Np[l];
+  const int in = a.P.sizes[l], out = a.P.sizes[l + 1];
+  __half* hi = reinterpret_cast<__half*>(wpk + a.ch_off[q]);
+  __half* lo = hi + (size_t)Np * kc;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < Np * kc; idx += gridDim.x * blockDim.x) {
+    const int r = idx / kc, k = idx % kc, kg = k0 + k;  // r = input unit i, kg = output unit o
+    const float v = (r < in && kg < out) ? theta[a.P.w_off[l] + (size_t)kg * in + r] : 0.0f;
+    const __half h = __float2half_rn(v);
+    const __half e = __float2half_rn(v - __half2float(h));
+    const int ci = tc::canon_idx(r, k, kc);
+    hi[ci] = h;
+    lo[ci] = e;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) k_mlp_bwd_tc(const __grid_constant__ BArgs a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t full[NST], empty[NST], mma_done, a_ready;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const PolicyDesc& P = a.P;
+  const int L = P.n_layers, p = a.p, D = a.D, q = P.sizes[L];
+  const int b0 = blockIdx.x * ROWS;
+  if (warp == EPI_WARPS + 1) tc::tmem_alloc(&tmem_base, 512);
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&mma_done, 1);
+    tc::mbar_init(&a_ready, 32 * EPI_WARPS);
+    tc::fence_mbar_init();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == EPI_WARPS) {
+    if (lane == 0) {
+      for (int c = 0; c < a.nch; ++c) {
+        const int s = c % NST;
+        tc::mbar_wait(&empty[s], ((uint32_t)(c / NST) & 1u) ^ 1u);
+        const uint32_t bytes = (uint32_t)a.Np[a.ch_layer[c]] * a.ch_kc[c] * 4u;
+        tc::mbar_arrive_expect_tx(&full[s], bytes);
+        tc::bulk_g2s(sm + (size_t)s * STAGE_BYTES, a.wpk + a.ch_off[c], bytes, &full[s]);
+      }
+    }
+  } else if (warp == EPI_WARPS + 1) {
+    if (lane == 0) {
+      int c = 0;
+      for (int j = 0; j < L; ++j) {
+        const int l = L - 1 - j;
+        tc::mbar_wait(&a_ready, (uint32_t)j & 1u);
+        tc::tc_fence_after();
+        const uint32_t idesc = tc::idesc_f16(ROWS, a.Np[l]);
+        bool first = true;
+        for (; c < a.nch && a.ch_layer[c] == l; ++c) {
+          const int s = c % NST, kc = a.ch_kc[c], k0 = a.ch_k0[c];
+          tc::mbar_wait(&full[s], (uint32_t)(c / NST) & 1u);
+          tc::tc_fence_after();
+          const uint32_t base = tc::smem_u32(sm + (size_t)s * STAGE_BYTES);
+          const uint32_t sbo = (uint32_t)(kc / 8) * 128u;
+          const uint64_t bhi = tc::umma_desc(base, 128, sbo);
+          const uint64_t blo = tc::umma_desc(base + (uint32_t)a.Np[l] * kc * 2u, 128, sbo);
+          for (int ks = 0; ks < kc / 16; ++ks) {
+            const uint64_t o = (uint64_t)(ks * 16);
+            const uint32_t ac = (uint32_t)((k0 + 16 * ks) / 2);
+            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, bhi + o, idesc, first ? 0u : 1u);
+            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, blo + o, idesc, 1u);
+            tc::mma_f16_ts(tmem + ACC, tmem + ALO + ac, bhi + o, idesc, 1u);
+            first = false;
+          }
+          tc::umma_commit(&empty[s]);
+        }
+        tc::umma_commit(&mma_done);
+      }
+    }
+  } else {
+    const int quarter = warp % 4, group = warp / 4;
+    const int r = quarter * 32 + lane, b = b0 + r;
+    const bool ok = b < a.B;
+    const uint32_t tl = (uint32_t)(quarter * 32) << 16;
+    // xs-bar_c = sum_m xbar_m A_t[m][c]
+    float xs[BAGEL_MAX_D];
+#pragma unroll
+    for (int c = 0; c < BAGEL_MAX_D; ++c) {
+      xs[c] = 0.0f;
+      if (ok && c < D)
+        for (int m = 0; m < p; ++m) xs[c] = fmaf(a.xbar[(size_t)b * p + m], a.A_t[((size_t)b * p + m) * D + c], xs[c]);
+    }
+    if (group == 0) {
+      // dl_{L-1} = ubar (1 - u^2) (q <= 7 values, K padded to 16)
+      float dv[16];
+#pragma unroll
+      for (int o = 0; o < 16; ++o) {
+        float v = 0.0f;
+#pragma unroll
+        for (int c = 0; c < BAGEL_MAX_D; ++c)
+          if (ok && o < q && c == p + o) {
+            const float u = a.act_t[(size_t)b * P.act_ld + P.aoff[L] + o];
+            v = xs[c] * (1.0f - u * u);
+          }
+        if (ok && o < q) a.delta_t[(size_t)b * P.d_ld + P.doff[L - 1] + o] = v;
+        dv[o] = v;
+      }
+      uint32_t hw[8], lw[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) split_pair(dv[2 * e], dv[2 * e + 1], hw[e], lw[e]);
+      tc::tmem_st8(tmem + tl + AHI, hw);
+      tc::tmem_st8(tmem + tl + ALO, lw);
+      tc::tmem_st_wait();
+    }
+    tc::tc_fence_before();
+    tc::mbar_arrive(&a_ready);
+    for (int j = 0; j < L; ++j) {
+      const int l = L - 1 - j, in = P.sizes[l], Np = a.Np[l];
+      tc::mbar_wait(&mma_done, (uint32_t)j & 1u);
+      __syncwarp();
+      tc::tc_fence_after();
+      for (int c0 = 16 * group; c0 < Np; c0 += 64) {
+        float v[16];
+        tc::tmem_ld16(tmem + tl + ACC + (uint32_t)c0, v);
+        tc::tmem_ld_wait();
+        if (l > 0) {
+          // dl_{l-1} = hbar (1 - h^2), h = layer l's input activations (tape)
+          const float* h = a.act_t + (size_t)b * P.act_ld + P.aoff[l] + c0;
+          float* dst = a.delta_t + (size_t)b * P.d_ld + P.doff[l - 1] + c0;
+          const bool vec = c0 + 16 <= in && ((P.act_ld | P.aoff[l] | P.d_ld | P.doff[l - 1]) & 3) == 0;
+          if (vec) {
+            float4 hv4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              hv4[i] = ok ? __ldg(reinterpret_cast<const float4*>(h) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              v[4 * i] *= 1.0f - hv4[i].x * hv4[i].x;
+              v[4 * i + 1] *= 1.0f - hv4[i].y * hv4[i].y;
+              v[4 * i + 2] *= 1.0f - hv4[i].z * hv4[i].z;
+              v[4 * i + 3] *= 1.0f - hv4[i].w * hv4[i].w;
+            }
+            if (ok)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float hv = (ok && c0 + i < in) ? h[i] : 0.0f;
+              v[i] = (c0 + i < in) ? v[i] * (1.0f - hv * hv) : 0.0f;
+              if (ok && c0 + i < in) dst[i] = v[i];
+            }
+          }
+          uint32_t hw[8], lw[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) split_pair(v[2 * e], v[2 * e + 1], hw[e], lw[e]);
+          tc::tmem_st8(tmem + tl + AHI + (uint32_t)(c0 / 2), hw);
+          tc::tmem_st8(tmem + tl + ALO + (uint32_t)(c0 / 2), lw);
+        } else if (ok && c0 == 0) {
+          // xbar_t = carry xbar_{t+1} + xs-bar[:p] + dphi/dx^T hbar_0 + d(r_t / B)/dx_t
+          float qd = 0.0f;
+          for (int c = 0; c < p; ++c) {
+            const float df = a.x_t[(size_t)b * p + c] - a.goals[(size_t)b * p + c];
+            qd = fmaf(a.rw.Q[c] * df, df, qd);
+          }
+          const float rr = expf(-qd * a.rw.inv_two_sr2);
+          const float inv_sr2 = 2.0f * a.rw.inv_two_sr2;
+#pragma unroll
+          for (int c = 0; c < BAGEL_MAX_P; ++c) {
+            if (c >= p) continue;
+            float hb = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (i == c) hb += v[i];
+              if (P.phi_mode == 1 && i == 2 * p + c) hb -= v[i];
+            }
+            float xsc = 0.0f;
+#pragma unroll
+            for (int cc = 0; cc < BAGEL_MAX_D; ++cc)
+              if (cc == c) xsc = xs[cc];
+            const float df = a.x_t[(size_t)b * p + c] - a.goals[(size_t)b * p + c];
+            a.xbar[(size_t)b * p + c] = a.carry * a.xbar[(size_t)b * p + c] + xsc + hb + a.invB * rr * a.rw.Q[c] * df * inv_sr2;
+          }
+        }
+      }
+      if (l > 0) {
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&a_ready);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == EPI_WARPS + 1) tc::tmem_dealloc(tmem, 512);
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      tc::mbar_inval(&full[s]);
+      tc::mbar_inval(&empty[s]);
+    }
+    tc::mbar_inval(&mma_done);
+    tc::mbar_inval(&a_ready);
+  }
+}
+
 size_t smem_bytes() { return NST * STAGE_BYTES; }
 
 }  // namespace mtc
@@ -285,8 +537,11 @@ bool mlp_tc_enabled(const bagel_ctx* c) {
 int mlp_tc_pack(bagel_ctx* c, const float* theta, cudaStream_t st) {
   mtc::Args a{};
   a.P = c->pol;
-  size_t total = 0;
-  mtc::chunk_table(c->pol, a, &total);
+  size_t fwd = 0, total = 0;
+  mtc::chunk_table(c->pol, a, &fwd);
+  mtc::BArgs ab{};
+  ab.P = c->pol;
+  mtc::chunk_table_bwd(c->pol, ab, fwd, &total);
   if (c->ws.mlp_wpk_cap < total) {
     if (c->ws.mlp_wpk) cudaFree(c->ws.mlp_wpk);
     c->ws.mlp_wpk = nullptr;
@@ -295,6 +550,40 @@ int mlp_tc_pack(bagel_ctx* c, const float* theta, cudaStream_t st) {
     c->ws.mlp_wpk_cap = total;
   }
   mtc::k_pack_mlp<<<dim3(16, a.nch), 256, 0, st>>>(a, theta, c->ws.mlp_wpk);
+  mtc::k_pack_mlp_bwd<<<dim3(16, ab.nch), 256, 0, st>>>(ab, theta, c->ws.mlp_wpk);
+  return 2;
+}
+
+// One adjoint step t of a wide policy on the tensor cores (replaces k_mlp_bwd; the caller runs
+// k_xbar_init first and the steps t = T-1 .. 0).
+int mlp_tc_backward_step(const bagel_ctx* c, const float* goals, int B, int t, long long B_global, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mtc::k_mlp_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mtc::smem_bytes());
+    attr = true;
+  }
+  const Workspace& w = c->ws;
+  mtc::Args af{};
+  af.P = c->pol;
+  size_t fwd = 0, total = 0;
+  mtc::chunk_table(c->pol, af, &fwd);
+  mtc::BArgs a{};
+  a.P = c->pol;
+  mtc::chunk_table_bwd(c->pol, a, fwd, &total);
+  a.rw = c->rw;
+  a.p = c->gp.p;
+  a.D = c->gp.d;
+  a.B = B;
+  a.wpk = w.mlp_wpk;
+  a.goals = goals;
+  a.x_t = w.tape_x + (size_t)t * B * a.p;
+  a.A_t = w.tape_A + (size_t)t * B * a.p * a.D;
+  a.act_t = w.tape_act + (size_t)t * B * c->pol.act_ld;
+  a.delta_t = w.tape_delta + (size_t)t * B * c->pol.d_ld;
+  a.xbar = w.xbar;
+  a.invB = (float)(1.0 / (double)B_global);
+  a.carry = c->gp.abs_target ? 0.0f : 1.0f;
+  mtc::k_mlp_bwd_tc<<<(B + mtc::ROWS - 1) / mtc::ROWS, mtc::THREADS, mtc::smem_bytes(), st>>>(a);
   return 1;
 }
 

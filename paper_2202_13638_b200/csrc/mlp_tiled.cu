@@ -361,7 +361,12 @@ int mlp_reverse(const bagel_ctx* c, const float* theta, const float* goals, int 
   const int p = c->gp.p, d = c->gp.d;
   const float invB = (float)(1.0 / (double)B_global);
   k_xbar_init<<<cdiv(B, 128), 128, 0, st>>>(c->rw, p, w.tape_x + (size_t)T * B * p, goals, B, invB, w.xbar);
+  const bool tcm = mlp_tc_enabled(c) && w.mlp_wpk;
   for (int t = T - 1; t >= 0; --t) {
+    if (tcm) {
+      mlp_tc_backward_step(c, goals, B, t, B_global, st);
+      continue;
+    }
     DISPATCH_D(d, (k_mlp_bwd<D><<<cdiv(B, MLP_RB), MLP_THREADS, mlp_smem(), st>>>(
                       c->pol, c->rw, p, w.thetaT, goals, B, w.tape_x + (size_t)t * B * p,
                       w.tape_A + (size_t)t * B * p * d, w.tape_act + (size_t)t * B * c->pol.act_ld,
