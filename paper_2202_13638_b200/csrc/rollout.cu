@@ -393,8 +393,12 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
 // arrive by 1-D bulk copies (TMA engine) into a TG_ST-stage ring; each thread owns up to TG_JOBS
 // 4 x 4 (o, i) weight tiles (or 4-bias groups) with register accumulators and reads its float4
 // slices of every staged row.
-constexpr int TG_THREADS = 256, TG_KC = 32, TG_ST = 3, TG_JOBS = 2;
+constexpr int TG_THREADS = 256, TG_KC = 32, TG_ST = 3;
+// TG_JOBS tiles per thread: every job batch streams the CTA's whole K range again, so wide policies
+// (C3: 8.5k tiles) take 8 per thread (5 passes over the tape instead of 17 -- the kernel is HBM
+// bound on those re-reads) and small ones 2 (one pass either way, fewer registers).
 
+template <int TG_JOBS>
 __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long long K, int KC,
                                                           const float* __restrict__ tape_act,
                                                           const float* __restrict__ tape_delta,
@@ -598,7 +602,8 @@ void ro_set_attributes() {
   static bool done = false;
   if (done) return;
   done = true;
-  bagel_set_smem_attr(k_theta_grad, 200 * 1024);
+  bagel_set_smem_attr(k_theta_grad<2>, 200 * 1024);
+  bagel_set_smem_attr(k_theta_grad<8>, 200 * 1024);
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
       bagel_set_smem_attr(k_reverse2<D, true>, 200 * 1024);
@@ -692,8 +697,15 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
 
 int ro_theta_grad(const bagel_ctx* c, int B, int T, int nblk, cudaStream_t st) {
   const Workspace& w = c->ws;
-  k_theta_grad<<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(c->pol, (long long)T * B, tg_chunk_rows(c->pol),
-                                                                      w.tape_act, w.tape_delta, w.theta_part);
+  int njobs = 0;
+  for (int l = 0; l < c->pol.n_layers; ++l)
+    njobs += ((c->pol.sizes[l + 1] + 3) / 4) * ((c->pol.sizes[l] + 3) / 4 + 1);
+  if (njobs > 2 * TG_THREADS * 2)
+    k_theta_grad<8><<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(
+        c->pol, (long long)T * B, tg_chunk_rows(c->pol), w.tape_act, w.tape_delta, w.theta_part);
+  else
+    k_theta_grad<2><<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(
+        c->pol, (long long)T * B, tg_chunk_rows(c->pol), w.tape_act, w.tape_delta, w.theta_part);
   return 1;
 }
 
