@@ -25,7 +25,8 @@ namespace mtc {
 
 constexpr int ROWS = 128;
 constexpr int KCH = 64;          // K elements per pipeline stage
-constexpr int NST = 3;           // ring stages
+constexpr int NST = 2;           // ring stages
+constexpr int WB_LD = 20;        // per-warp store staging: 32 rows x 16 columns, rows padded to 20 floats
 constexpr int EPI_WARPS = 16;    // 4 per TMEM lane quarter, each a quarter of the columns
 constexpr int THREADS = 32 * (EPI_WARPS + 2);
 constexpr int MAXCH = 32;        // chunks over all layers (8 layers x 4 chunks of 64)
@@ -87,15 +88,12 @@ __global__ void k_pack_mlp(Args a, const float* __restrict__ theta, uint8_t* __r
   }
 }
 
-// tanh with ~1e-7 absolute / few-ulp relative error at a third of tanhf's instructions: odd
-// Taylor polynomial for |v| < 1/8 (truncation < 1e-9 relative), else 1 - 2 / (e^{2v} + 1).
+// tanh(v) = sign(v) (1 - 2 / (e^{2|v|} + 1)): absolute error a few fp32 ulps of 1 everywhere (for
+// tiny |v| that is a large relative error, but an activation enters the next layer's sums -- and
+// the adjoint's 1 - h^2 -- through its absolute value, so the layer outputs keep fp32-class
+// accuracy), ~7 instructions instead of tanhf's ~25.
 __device__ __forceinline__ float tanh_fast(float v) {
-  const float a = fabsf(v);
-  if (a < 0.125f) {
-    const float v2 = v * v;
-    return v * fmaf(v2, fmaf(v2, fmaf(v2, -17.0f / 315.0f, 2.0f / 15.0f), -1.0f / 3.0f), 1.0f);
-  }
-  const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * a) + 1.0f);
+  const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * fabsf(v)) + 1.0f);
   return copysignf(t, v);
 }
 
@@ -108,18 +106,63 @@ __device__ __forceinline__ void split_pair(float v0, float v1, uint32_t& hw, uin
   lw = *reinterpret_cast<const uint32_t*>(&l2);
 }
 
+// Store a warp's 32 rows x 16 columns (row `lane` in v) to dst rows (row stride ld floats) with
+// coalesced 64-byte row segments instead of one 16-byte piece per row per instruction: through a
+// per-warp shared buffer, 8 rows per float4 store instruction.  rows_ok: rows of the warp that
+// exist (< B).  dst + row * ld must be 16-byte aligned.
+__device__ __forceinline__ void store_rows16(float* wb, const float* v, float* dst0, size_t ld, int rows_ok) {
+  const int lane = threadIdx.x % 32;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<float4*>(wb + lane * WB_LD + 4 * j) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int row = it * 8 + lane / 4, seg = lane % 4;
+    if (row < rows_ok)
+      *reinterpret_cast<float4*>(dst0 + (size_t)row * ld + 4 * seg) =
+          *reinterpret_cast<const float4*>(wb + row * WB_LD + 4 * seg);
+  }
+  __syncwarp();
+}
+
+// The mirror image: load a warp's 32 rows x 16 columns (row `lane` into v) with coalesced 64-byte
+// row segments; rows >= rows_ok read as 0.
+__device__ __forceinline__ void load_rows16(float* wb, const float* src0, size_t ld, int rows_ok, float* v) {
+  const int lane = threadIdx.x % 32;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int row = it * 8 + lane / 4, seg = lane % 4;
+    const float4 x = row < rows_ok ? __ldg(reinterpret_cast<const float4*>(src0 + (size_t)row * ld + 4 * seg))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(wb + row * WB_LD + 4 * seg) = x;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 x = *reinterpret_cast<const float4*>(wb + lane * WB_LD + 4 * j);
+    v[4 * j] = x.x;
+    v[4 * j + 1] = x.y;
+    v[4 * j + 2] = x.z;
+    v[4 * j + 3] = x.w;
+  }
+  __syncwarp();
+}
+
+
 __global__ void __launch_bounds__(THREADS, 1) k_mlp_fwd_tc(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t full[NST], empty[NST], mma_done, a_ready;
   __shared__ uint32_t tmem_base;
-  __shared__ float bias_s[BAGEL_MAX_LAYERS][BAGEL_MAX_WIDTH];
+  __shared__ __align__(16) float bias_s[BAGEL_MAX_LAYERS][BAGEL_MAX_WIDTH];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const PolicyDesc& P = a.P;
   const int L = P.n_layers;
   const int b0 = blockIdx.x * ROWS;
   if (warp == EPI_WARPS + 1) tc::tmem_alloc(&tmem_base, 512);
   for (int l = 0; l < P.n_layers; ++l)
-    for (int o = tid; o < P.sizes[l + 1]; o += THREADS) bias_s[l][o] = __ldg(a.theta + P.b_off[l] + o);
+    for (int o = tid; o < BAGEL_MAX_WIDTH; o += THREADS)
+      bias_s[l][o] = o < P.sizes[l + 1] ? __ldg(a.theta + P.b_off[l] + o) : 0.0f;
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       tc::mbar_init(&full[s], 1);
@@ -182,6 +225,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_fwd_tc(const __grid_constant
     const bool ok = b < a.B;
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;
     float* act = ok ? a.act + (size_t)b * P.act_ld : nullptr;
+    float* wb = reinterpret_cast<float*>(sm + NST * STAGE_BYTES) + warp * 32 * WB_LD;
+    const int rows_ok = min(32, a.B - (b0 + quarter * 32));
     // layer-0 input phi = [x, g] or [x, g, g - x], zero-padded to 16 K elements
     if (half == 0) {
       const int n0 = P.sizes[0];
@@ -221,26 +266,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_fwd_tc(const __grid_constant
         float v[16];
         tc::tmem_ld16(tmem + tl + ACC + (uint32_t)c0, v);
         tc::tmem_ld_wait();
+        float bb[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int o = c0 + i;
-          v[i] = o < out ? tanh_fast(v[i] + bias[o]) : 0.0f;
+        for (int j = 0; j < 4; ++j) {  // bias_s rows are zero-padded to 256 (16-byte loads, no bound checks)
+          const float4 b4 = *reinterpret_cast<const float4*>(bias + c0 + 4 * j);
+          bb[4 * j] = b4.x;
+          bb[4 * j + 1] = b4.y;
+          bb[4 * j + 2] = b4.z;
+          bb[4 * j + 3] = b4.w;
         }
-        if (ok) {
-          if (c0 + 16 <= out && ((P.act_ld | P.aoff[l + 1]) & 3) == 0) {
-            float4* dst = reinterpret_cast<float4*>(act + P.aoff[l + 1] + c0);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          } else {
+        for (int i = 0; i < 16; ++i) v[i] = c0 + i < out ? tanh_fast(v[i] + bb[i]) : 0.0f;
+        // activation tape: coalesced through the warp's staging buffer when aligned (warp-uniform)
+        if (((P.act_ld | P.aoff[l + 1]) & 3) == 0 && c0 + 16 <= out) {
+          store_rows16(wb, v, a.act + (size_t)(b0 + quarter * 32) * P.act_ld + P.aoff[l + 1] + c0, P.act_ld, rows_ok);
+        } else if (ok) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c0 + i < out) act[P.aoff[l + 1] + c0 + i] = v[i];
-          }
-          if (last)
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c0 + i < out) a.xstar[(size_t)b * a.D + a.p + c0 + i] = v[i];
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < out) act[P.aoff[l + 1] + c0 + i] = v[i];
         }
+        if (ok && last)
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < out) a.xstar[(size_t)b * a.D + a.p + c0 + i] = v[i];
         if (!last) {
           uint32_t hw[8], lw[8];
 #pragma unroll
@@ -399,6 +447,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_bwd_tc(const __grid_constant
     const int r = quarter * 32 + lane, b = b0 + r;
     const bool ok = b < a.B;
     const uint32_t tl = (uint32_t)(quarter * 32) << 16;
+    float* wb = reinterpret_cast<float*>(sm + NST * STAGE_BYTES) + warp * 32 * WB_LD;
+    const int rows_ok = min(32, a.B - (b0 + quarter * 32));
     // xs-bar_c = sum_m xbar_m A_t[m][c]
     float xs[BAGEL_MAX_D];
 #pragma unroll
@@ -442,26 +492,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_bwd_tc(const __grid_constant
         tc::tmem_ld_wait();
         if (l > 0) {
           // dl_{l-1} = hbar (1 - h^2), h = layer l's input activations (tape)
-          const float* h = a.act_t + (size_t)b * P.act_ld + P.aoff[l] + c0;
-          float* dst = a.delta_t + (size_t)b * P.d_ld + P.doff[l - 1] + c0;
           const bool vec = c0 + 16 <= in && ((P.act_ld | P.aoff[l] | P.d_ld | P.doff[l - 1]) & 3) == 0;
-          if (vec) {
-            float4 hv4[4];
+          if (vec) {  // warp-uniform: coalesced tape traffic through the warp's staging buffer
+            float hv[16];
+            load_rows16(wb, a.act_t + (size_t)(b0 + quarter * 32) * P.act_ld + P.aoff[l] + c0, P.act_ld, rows_ok, hv);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              hv4[i] = ok ? __ldg(reinterpret_cast<const float4*>(h) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              v[4 * i] *= 1.0f - hv4[i].x * hv4[i].x;
-              v[4 * i + 1] *= 1.0f - hv4[i].y * hv4[i].y;
-              v[4 * i + 2] *= 1.0f - hv4[i].z * hv4[i].z;
-              v[4 * i + 3] *= 1.0f - hv4[i].w * hv4[i].w;
-            }
-            if (ok)
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            for (int i = 0; i < 16; ++i) v[i] *= 1.0f - hv[i] * hv[i];
+            store_rows16(wb, v, a.delta_t + (size_t)(b0 + quarter * 32) * P.d_ld + P.doff[l - 1] + c0, P.d_ld, rows_ok);
           } else {
+            const float* h = a.act_t + (size_t)b * P.act_ld + P.aoff[l] + c0;
+            float* dst = a.delta_t + (size_t)b * P.d_ld + P.doff[l - 1] + c0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float hv = (ok && c0 + i < in) ? h[i] : 0.0f;
@@ -521,7 +561,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_bwd_tc(const __grid_constant
   }
 }
 
-size_t smem_bytes() { return NST * STAGE_BYTES; }
+size_t smem_bytes() { return NST * STAGE_BYTES + (size_t)EPI_WARPS * 32 * WB_LD * sizeof(float); }
+
+
 
 }  // namespace mtc
 
