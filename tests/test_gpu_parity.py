@@ -466,3 +466,17 @@ def test_maximum_sizes(bagel):
     seed = W.rollout_seed(6)
     cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), "max sizes")
+
+
+def test_wide_policy_ragged_widths(bagel):
+    """Tensor-core MLP kernels (mlp_tc.cu) with layer widths that are not multiples of 16 or 64
+    (zero-padded K and N, partial column chunks, the scalar tape paths) and a ragged batch."""
+    wl = W.make_workload(plant="boom", N=600, rank=64, hidden=(200, 136, 248), B=200, T=6)
+    assert W.n_params(wl.sizes) > 60000
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    goals = (wl.x0 + np.array([0.4, -0.2], dtype=np.float32)).astype(np.float32)
+    seed = W.rollout_seed(9)
+    cost, grad = _rollout_gpu(ctx, wl, goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "ragged wide policy")
