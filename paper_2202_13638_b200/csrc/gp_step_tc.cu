@@ -825,15 +825,27 @@ struct R1Args {
 //  r1b  grid (row groups of 32, m): per-row totals in j-group order -> v, sigma, J^mu,
 //       row scale; packs z as the fp16 hi/lo pass-2 A operand (row-major, the TMEM image).
 constexpr int R1_JG = 32;
+// lane = 4 consecutive rows (float4 traffic when B % 4 == 0: VEC), warp w = columns jg*32 + 4w .. +3,
+// CTA = 128 rows
+template <bool VEC>
+__device__ __forceinline__ float4 ld4(const float* p, int nrows) {
+  if (VEC) return __ldg(reinterpret_cast<const float4*>(p));
+  return make_float4(nrows > 0 ? __ldg(p) : 0.f, nrows > 1 ? __ldg(p + 1) : 0.f, nrows > 2 ? __ldg(p + 2) : 0.f,
+                     nrows > 3 ? __ldg(p + 3) : 0.f);
+}
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_r1a_tc(R1Args a, double* __restrict__ zz_part, float* __restrict__ zmax_part) {
   const Geo& g = a.g;
   const int m = blockIdx.y, jg = blockIdx.z;
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
-  const int row = blockIdx.x * 32 + lane;
+  const int row = blockIdx.x * 128 + lane * 4;  // first of this thread's 4 rows
   const bool ok = row < a.B;
-  __shared__ double zz_s[8][32];
-  __shared__ float zm_s[8][32];
-  float z[4] = {0.f, 0.f, 0.f, 0.f};
+  const int nrows = min(4, a.B - row);
+  __shared__ double zz_s[8][128];
+  __shared__ float zm_s[8][128];
+  float4 z[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) z[u] = make_float4(0.f, 0.f, 0.f, 0.f);
   const int j0 = jg * R1_JG + w * 4;
   if (ok) {
     const float* src[4];
@@ -844,44 +856,71 @@ __global__ void __launch_bounds__(256) k_r1a_tc(R1Args a, double* __restrict__ z
       src[u] = a.P1z + ((size_t)(m * g.nct + ct) * g.NZ + jr) * a.B + row;
     }
     const size_t sstride = (size_t)g.p * g.nct * g.NZ * a.B;
-    // 8 splits x 4 columns of independent loads in flight, then summed in split order
-    for (int s0 = 0; s0 < a.S1; s0 += 8) {
-      float v[8][4];
+    // 4 splits x 4 columns of independent 16-byte loads in flight, summed in split order
+    for (int s0 = 0; s0 < a.S1; s0 += 4) {
+      float4 v[4][4];
 #pragma unroll
-      for (int ss = 0; ss < 8; ++ss)
+      for (int ss = 0; ss < 4; ++ss)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[ss][u] = (s0 + ss < a.S1) ? __ldg(src[u] + (size_t)(s0 + ss) * sstride) : 0.0f;
+        for (int u = 0; u < 4; ++u)
+          v[ss][u] = (s0 + ss < a.S1) ? ld4<VEC>(src[u] + (size_t)(s0 + ss) * sstride, nrows) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int ss = 0; ss < 8; ++ss)
+      for (int ss = 0; ss < 4; ++ss)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) z[u] += v[ss][u];
+        for (int u = 0; u < 4; ++u) {
+          z[u].x += v[ss][u].x;
+          z[u].y += v[ss][u].y;
+          z[u].z += v[ss][u].z;
+          z[u].w += v[ss][u].w;
+        }
     }
   }
-  double zz = 0.0;
-  float zm = 0.0f;
+  double zz[4] = {0.0, 0.0, 0.0, 0.0};
+  float zm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int j = j0 + u;
     if (j < g.k && ok) {
-      const float v = z[u] * a.colscale[(size_t)m * g.k + j];
-      a.Z[((size_t)m * g.k + j) * a.B + row] = v;
-      zz += (double)v * (double)v;
-      zm = fmaxf(zm, fabsf(v));
+      const float cs = a.colscale[(size_t)m * g.k + j];
+      const float4 v = make_float4(z[u].x * cs, z[u].y * cs, z[u].z * cs, z[u].w * cs);
+      float* zd = a.Z + ((size_t)m * g.k + j) * a.B + row;
+      if (VEC) {
+        *reinterpret_cast<float4*>(zd) = v;
+      } else {
+        zd[0] = v.x;
+        if (nrows > 1) zd[1] = v.y;
+        if (nrows > 2) zd[2] = v.z;
+        if (nrows > 3) zd[3] = v.w;
+      }
+      zz[0] += (double)v.x * (double)v.x;
+      zz[1] += (double)v.y * (double)v.y;
+      zz[2] += (double)v.z * (double)v.z;
+      zz[3] += (double)v.w * (double)v.w;
+      zm[0] = fmaxf(zm[0], fabsf(v.x));
+      zm[1] = fmaxf(zm[1], fabsf(v.y));
+      zm[2] = fmaxf(zm[2], fabsf(v.z));
+      zm[3] = fmaxf(zm[3], fabsf(v.w));
     }
   }
-  zz_s[w][lane] = zz;
-  zm_s[w][lane] = zm;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    zz_s[w][lane * 4 + e] = zz[e];
+    zm_s[w][lane * 4 + e] = zm[e];
+  }
   __syncthreads();
-  if (w == 0 && ok) {
-    double t = 0.0;
-    float mx = 0.0f;
-    for (int i = 0; i < 8; ++i) {
-      t += zz_s[i][lane];
-      mx = fmaxf(mx, zm_s[i][lane]);
+  if (threadIdx.x < 128) {
+    const int rr = blockIdx.x * 128 + threadIdx.x;
+    if (rr < a.B) {
+      double t = 0.0;
+      float mx = 0.0f;
+      for (int i = 0; i < 8; ++i) {  // column order within the group: fixed
+        t += zz_s[i][threadIdx.x];
+        mx = fmaxf(mx, zm_s[i][threadIdx.x]);
+      }
+      const int njg = cdiv_dev(g.k, R1_JG);
+      zz_part[((size_t)m * njg + jg) * a.B + rr] = t;
+      zmax_part[((size_t)m * njg + jg) * a.B + rr] = mx;
     }
-    const int njg = cdiv_dev(g.k, R1_JG);
-    zz_part[((size_t)m * njg + jg) * a.B + row] = t;
-    zmax_part[((size_t)m * njg + jg) * a.B + row] = mx;
   }
 }
 
@@ -1544,7 +1583,10 @@ int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, fl
   a.var = c->ws.var;
   a.jmu = jmu_out;
   a.sig = sig_out;
-  k_r1a_tc<<<dim3(cdiv(B, 32), c->p, cdiv(c->k, R1_JG)), 256, 0, st>>>(a, T.zz_part, T.zmax_part);
+  if (B % 4 == 0)
+    k_r1a_tc<true><<<dim3(cdiv(B, 128), c->p, cdiv(c->k, R1_JG)), 256, 0, st>>>(a, T.zz_part, T.zmax_part);
+  else
+    k_r1a_tc<false><<<dim3(cdiv(B, 128), c->p, cdiv(c->k, R1_JG)), 256, 0, st>>>(a, T.zz_part, T.zmax_part);
   DISPATCH_D(c->d, (k_r1b_tc<D><<<dim3(cdiv(B, 32), c->p), 256, 0, st>>>(a, T.zz_part, T.zmax_part)));
   return 2;
 }
