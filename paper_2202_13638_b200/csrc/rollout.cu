@@ -391,14 +391,15 @@ __global__ void __launch_bounds__(32 * REV2_WARPS) k_reverse2(
 // contraction split over the CTAs (contiguous K ranges, one partial per CTA, summed in CTA order
 // by k_reduce_grad).  The tape rows of a range are contiguous, so TG_KC-row chunks of both tapes
 // arrive by 1-D bulk copies (TMA engine) into a TG_ST-stage ring; each thread owns up to TG_JOBS
-// 4 x 4 (o, i) weight tiles (or 4-bias groups) with register accumulators and reads its float4
+// TO x TI (o, i) weight tiles (or TO-bias groups) with register accumulators and reads its float4
 // slices of every staged row.
 constexpr int TG_THREADS = 256, TG_KC = 32, TG_ST = 3;
-// TG_JOBS tiles per thread: every job batch streams the CTA's whole K range again, so wide policies
-// (C3: 8.5k tiles) take 8 per thread (5 passes over the tape instead of 17 -- the kernel is HBM
-// bound on those re-reads) and small ones 2 (one pass either way, fewer registers).
+// Tiles of TO x TI (o, i) per job, TG_JOBS jobs per thread: every job batch streams the CTA's whole
+// K range again, and each staged row costs (TO + TI) / 4 shared-memory float4 loads per TO TI FMAs,
+// so wide policies (C3) use 2 jobs of 8 x 8 (5 passes over the tape instead of 17 with 4 x 4; half
+// the shared-memory traffic per FMA) and small ones 2 of 4 x 4 (one pass either way).
 
-template <int TG_JOBS>
+template <int TG_JOBS, int TO, int TI>
 __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long long K, int KC,
                                                           const float* __restrict__ tape_act,
                                                           const float* __restrict__ tape_delta,
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long lo
   }
   __syncthreads();
   int njobs = 0;
-  for (int l = 0; l < P.n_layers; ++l) njobs += ((P.sizes[l + 1] + 3) / 4) * ((P.sizes[l] + 3) / 4 + 1);
+  for (int l = 0; l < P.n_layers; ++l) njobs += ((P.sizes[l + 1] + TO - 1) / TO) * ((P.sizes[l] + TI - 1) / TI + 1);
   const int nbatch = (njobs + TG_THREADS * TG_JOBS - 1) / (TG_THREADS * TG_JOBS);
   const int total = nbatch * nchunks;  // the K range is streamed once per job batch
   // chunk g of the whole sequence: batch g / nchunks, rows of chunk g % nchunks; stage g % TG_ST
@@ -443,19 +444,19 @@ __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long lo
       jd[u] = -1;
       ja[u] = -1;
       for (int l = 0; l < P.n_layers && j >= 0; ++l) {
-        const int no = (P.sizes[l + 1] + 3) / 4, ni = (P.sizes[l] + 3) / 4 + 1;
+        const int no = (P.sizes[l + 1] + TO - 1) / TO, ni = (P.sizes[l] + TI - 1) / TI + 1;
         if (j < no * ni) {
-          jd[u] = P.doff[l] + (j / ni) * 4;
-          ja[u] = (j % ni) == ni - 1 ? -1 : P.aoff[l] + (j % ni) * 4;
+          jd[u] = P.doff[l] + (j / ni) * TO;
+          ja[u] = (j % ni) == ni - 1 ? -1 : P.aoff[l] + (j % ni) * TI;
         }
         j -= no * ni;
       }
     }
-    float acc[TG_JOBS][16];
+    float acc[TG_JOBS][TO * TI];
 #pragma unroll
     for (int u = 0; u < TG_JOBS; ++u)
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc[u][e] = 0.0f;
+      for (int e = 0; e < TO * TI; ++e) acc[u][e] = 0.0f;
     for (int c = 0; c < nchunks; ++c) {
       const int g = batch * nchunks + c, s = g % TG_ST;
       const int rows = (int)min((long long)KC, k1 - (k0 + (long long)c * KC));
@@ -465,23 +466,36 @@ __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long lo
 #pragma unroll
       for (int u = 0; u < TG_JOBS; ++u) {
         if (jd[u] < 0) continue;
+        // (a tile may read past its segment -- into the next segment, row or the stage padding;
+        // those accumulators belong to parameters that are never written)
         if (ja[u] >= 0) {
           for (int r = 0; r < rows; ++r) {
-            const float4 d4 = *reinterpret_cast<const float4*>(ds + r * DL + jd[u]);
-            const float4 h4 = *reinterpret_cast<const float4*>(hs + r * AL + ja[u]);
-            const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hv[4] = {h4.x, h4.y, h4.z, h4.w};
+            float dv[TO], hv[TI];
 #pragma unroll
-            for (int eo = 0; eo < 4; ++eo)
+            for (int q = 0; q < TO / 4; ++q) {
+              const float4 d4 = *reinterpret_cast<const float4*>(ds + r * DL + jd[u] + 4 * q);
+              dv[4 * q] = d4.x; dv[4 * q + 1] = d4.y; dv[4 * q + 2] = d4.z; dv[4 * q + 3] = d4.w;
+            }
 #pragma unroll
-              for (int ei = 0; ei < 4; ++ei) acc[u][eo * 4 + ei] = fmaf(dv[eo], hv[ei], acc[u][eo * 4 + ei]);
+            for (int q = 0; q < TI / 4; ++q) {
+              const float4 h4 = *reinterpret_cast<const float4*>(hs + r * AL + ja[u] + 4 * q);
+              hv[4 * q] = h4.x; hv[4 * q + 1] = h4.y; hv[4 * q + 2] = h4.z; hv[4 * q + 3] = h4.w;
+            }
+#pragma unroll
+            for (int eo = 0; eo < TO; ++eo)
+#pragma unroll
+              for (int ei = 0; ei < TI; ++ei) acc[u][eo * TI + ei] = fmaf(dv[eo], hv[ei], acc[u][eo * TI + ei]);
           }
         } else {
           for (int r = 0; r < rows; ++r) {
-            const float4 d4 = *reinterpret_cast<const float4*>(ds + r * DL + jd[u]);
-            acc[u][0] += d4.x;
-            acc[u][1] += d4.y;
-            acc[u][2] += d4.z;
-            acc[u][3] += d4.w;
+#pragma unroll
+            for (int q = 0; q < TO / 4; ++q) {
+              const float4 d4 = *reinterpret_cast<const float4*>(ds + r * DL + jd[u] + 4 * q);
+              acc[u][4 * q] += d4.x;
+              acc[u][4 * q + 1] += d4.y;
+              acc[u][4 * q + 2] += d4.z;
+              acc[u][4 * q + 3] += d4.w;
+            }
           }
         }
       }
@@ -494,16 +508,18 @@ __global__ void __launch_bounds__(TG_THREADS) k_theta_grad(PolicyDesc P, long lo
       int j = jbase + u * TG_THREADS + threadIdx.x;
       for (int l = 0; l < P.n_layers && j >= 0; ++l) {
         const int in = P.sizes[l], outw = P.sizes[l + 1];
-        const int no = (outw + 3) / 4, ni = (in + 3) / 4 + 1;
+        const int no = (outw + TO - 1) / TO, ni = (in + TI - 1) / TI + 1;
         if (j < no * ni) {
-          const int o0 = (j / ni) * 4, it = j % ni;
-          for (int eo = 0; eo < 4; ++eo) {
+          const int o0 = (j / ni) * TO, it = j % ni;
+#pragma unroll
+          for (int eo = 0; eo < TO; ++eo) {
             if (o0 + eo >= outw) continue;
             if (it == ni - 1) {
               out[P.b_off[l] + o0 + eo] = nchunks ? acc[u][eo] : 0.0f;
             } else {
-              for (int ei = 0; ei < 4; ++ei)
-                if (it * 4 + ei < in) out[P.w_off[l] + (o0 + eo) * in + it * 4 + ei] = acc[u][eo * 4 + ei];
+#pragma unroll
+              for (int ei = 0; ei < TI; ++ei)
+                if (it * TI + ei < in) out[P.w_off[l] + (o0 + eo) * in + it * TI + ei] = acc[u][eo * TI + ei];
             }
           }
         }
@@ -585,11 +601,12 @@ size_t ro_reverse_smem(const PolicyDesc& P, int p, int d) {
 // TG_ST-stage ring stays within 200 KB
 int tg_chunk_rows(const PolicyDesc& P) {
   const size_t row_bytes = sizeof(float) * (size_t)(P.act_ld + P.d_ld);
-  const int kc = (int)std::min<size_t>(TG_KC, (200 * 1024) / (TG_ST * row_bytes));
+  const int kc = (int)std::min<size_t>(TG_KC, (200 * 1024 - 16 * sizeof(float)) / (TG_ST * row_bytes));
   return std::max(kc, 1);
 }
 size_t ro_theta_grad_smem(const PolicyDesc& P) {
-  return sizeof(float) * (size_t)TG_ST * tg_chunk_rows(P) * (P.act_ld + P.d_ld);
+  // + padding: an 8-wide tile of the stage's last row may read up to 8 floats past it
+  return sizeof(float) * ((size_t)TG_ST * tg_chunk_rows(P) * (P.act_ld + P.d_ld) + 16);
 }
 int ro_theta_blocks(const bagel_ctx* c, int B, int T) {
   const long long K = (long long)B * std::max(T, 1);
@@ -602,8 +619,8 @@ void ro_set_attributes() {
   static bool done = false;
   if (done) return;
   done = true;
-  bagel_set_smem_attr(k_theta_grad<2>, 200 * 1024);
-  bagel_set_smem_attr(k_theta_grad<8>, 200 * 1024);
+  bagel_set_smem_attr(k_theta_grad<2, 4, 4>, 200 * 1024);
+  bagel_set_smem_attr(k_theta_grad<2, 8, 8>, 200 * 1024);
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
       bagel_set_smem_attr(k_reverse2<D, true>, 200 * 1024);
@@ -701,10 +718,10 @@ int ro_theta_grad(const bagel_ctx* c, int B, int T, int nblk, cudaStream_t st) {
   for (int l = 0; l < c->pol.n_layers; ++l)
     njobs += ((c->pol.sizes[l + 1] + 3) / 4) * ((c->pol.sizes[l] + 3) / 4 + 1);
   if (njobs > 2 * TG_THREADS * 2)
-    k_theta_grad<8><<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(
+    k_theta_grad<2, 8, 8><<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(
         c->pol, (long long)T * B, tg_chunk_rows(c->pol), w.tape_act, w.tape_delta, w.theta_part);
   else
-    k_theta_grad<2><<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(
+    k_theta_grad<2, 4, 4><<<nblk, TG_THREADS, ro_theta_grad_smem(c->pol), st>>>(
         c->pol, (long long)T * B, tg_chunk_rows(c->pol), w.tape_act, w.tape_delta, w.theta_part);
   return 1;
 }
