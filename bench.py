@@ -191,10 +191,11 @@ def run_reference(args, wl, rank):
 
 
 def config_dict(args, wl, n_traj=None):
+    world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))  # torchrun's world wins over --gpus
     return {"workload": f"{args.config}: GP N={wl.N} d={wl.d} p={wl.p}, LOVE rank {wl.rank}, "
                         f"MLP {'-'.join(map(str, wl.sizes))}, B={wl.B} per GPU, T={wl.T}",
-            "global_batch": wl.B * args.gpus if n_traj is None else n_traj, "horizon": wl.T,
-            "parallelism": f"dp{args.gpus}", "l2": "flushed (256 MiB write) between timed iterations"}
+            "global_batch": wl.B * world if n_traj is None else n_traj, "horizon": wl.T,
+            "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) between timed iterations"}
 
 
 def main():
