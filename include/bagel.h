@@ -48,14 +48,17 @@ typedef struct bagel_ctx bagel_ctx;
  * *out receives the context.  Errors: E_ARG (out NULL), E_CUDA. */
 int bagel_create(bagel_ctx** out, int device, void* cuda_stream);
 
-/* Free every library buffer.  NULL is accepted. */
+/* Free every library buffer (synchronises the context's stream first).  NULL is
+ * accepted.  Errors: none (always BAGEL_OK). */
 int bagel_destroy(bagel_ctx* ctx);
 
-/* Re-target subsequent work to another stream on the same device. */
+/* Re-target subsequent work to another stream on the same device (cuda_stream as
+ * in bagel_create).  Errors: E_ARG for a NULL context. */
 int bagel_set_stream(bagel_ctx* ctx, void* cuda_stream);
 
 /* Message of the last failing call on this context ("" if none).  The pointer
- * stays valid until the next call on the context. */
+ * stays valid until the next call on the context; "null context" for NULL.
+ * Errors: none (returns a string). */
 const char* bagel_last_error(const bagel_ctx* ctx);
 
 /* --------------------------------------------------------------- GP model */
@@ -205,7 +208,8 @@ int policy_adam_step(bagel_ctx* ctx, float* params, const float* grad, float* m1
  * noise < 1e-8, workspace > 120 GB); E_NUMERIC if a Cholesky pivot <= 0; E_CUDA. */
 int gp_log_marginal_likelihood(bagel_ctx* ctx, int m, const double* log_hyp, double* mll, double* grad);
 
-/* Number of kernel launches the last rollout_cost_and_grad enqueued (host int). */
+/* Number of kernel launches the last rollout_cost_and_grad enqueued: launches [host]
+ * (the bench's gpu_launches count).  Errors: E_ARG for NULL pointers. */
 int bagel_last_launch_count(const bagel_ctx* ctx, int* launches);
 
 /* Per-kernel device timing for the roofline report (bench.py).  While enabled,
@@ -227,28 +231,36 @@ int bagel_profile_get(bagel_ctx* ctx, int kernel, double* total_ms, long long* l
 /* One GP query per row of xstar [dev] M x d with the LOVE variance and input
  * Jacobians (Appendix B of SURVEY.md; the autodiff of Eq.2-3):
  *   mean, var [dev] M x p; dmean, dvar [dev] M x p x d (dvar uses the unclamped v).
- * Runs the same kernels as the rollout's GP step. */
+ * Runs the same kernels as the rollout's GP step.  Errors: E_STATE without a cache;
+ * E_ARG (NULL pointers, M < 1); E_CUDA. */
 int bagel_gp_predict(bagel_ctx* ctx, const float* xstar, int M, float* mean, float* var,
                      float* dmean, float* dvar);
 
-/* Forward rollout with per-step traces (same kernels as rollout_cost_and_grad):
+/* Forward rollout with per-step traces (same kernels as rollout_cost_and_grad,
+ * Alg.1; Eq.9-10):
  *   x [dev] (T+1) x B x p states, mu / var [dev] T x B x p GP moments,
- *   ret [dev] B returns G_b.  Any trace pointer may be NULL. */
+ *   ret [dev] B returns G_b.  Any trace pointer may be NULL.  Other arguments and
+ *   errors as rollout_cost_and_grad (E_STATE, E_ARG, E_NUMERIC, E_CUDA). */
 int bagel_rollout_trace(bagel_ctx* ctx, const float* policy_params, const float* x0,
                         const float* goals, int B, int T, uint64_t seed, long long traj_offset,
                         float* x, float* mu, float* var, float* ret);
 
-/* Raw Philox4x32-10: ctr [dev] n x 4 u32, key [host] 2 u32, out [dev] n x 4 u32. */
+/* Raw Philox4x32-10 (Salmon et al., SC'11; the generator of reading R29 / DESIGN.md
+ * "Philox"): ctr [dev] n x 4 u32, key [host] 2 u32, out [dev] n x 4 u32.
+ * Synchronous.  Errors: E_ARG for NULL pointers or n < 0; E_CUDA. */
 int bagel_philox4x32_10(bagel_ctx* ctx, const uint32_t* ctr, const uint32_t* key, int n,
                         uint32_t* out);
 
-/* Rollout noise as the rollout draws it: out [dev] T x B x p floats,
- * out[t][b][m] = eps_{traj_offset + b, t, m} for `seed`. */
+/* Rollout noise as the rollout draws it (Eq.9, reparameterised, R18): out [dev]
+ * T x B x p floats, out[t][b][m] = eps_{traj_offset + b, t, m} for `seed`.
+ * Synchronous.  Errors: E_ARG (out NULL, B < 1, T < 1, p not in [1, 4]); E_CUDA. */
 int bagel_philox_normals(bagel_ctx* ctx, uint64_t seed, long long traj_offset, int B, int T,
                          int p, float* out);
 
-/* LOVE cache of output m as float64 device arrays: alpha [dev] N, R [dev] rank x N.
- * bagel_cache_rank returns the rank k (0 if no cache). */
+/* LOVE cache of output m as float64 device arrays: alpha [dev] N,
+ * R [dev] rank x N.  bagel_cache_rank returns the rank k (0 if no cache) in
+ * rank [host].  Errors: E_ARG (NULL pointers, m out of range); E_STATE without a
+ * cache; E_CUDA. */
 int bagel_cache_rank(const bagel_ctx* ctx, int* rank);
 int bagel_cache_get(bagel_ctx* ctx, int m, double* alpha, double* R);
 
@@ -283,7 +295,8 @@ int bagel_tc_selftest(bagel_ctx* ctx, const void* A, const void* B, int N, int K
 int bagel_debug_buffer(bagel_ctx* ctx, int which, void* dst, size_t bytes);
 
 /* Enable (1) / disable (0) per-CTA %globaltimer event stamps of the tensor-core GP kernels
- * (16 per CTA, up to 4096 CTAs; read with bagel_debug_buffer 4 = pass 1, 5 = pass 2). */
+ * (16 per CTA, up to 4096 CTAs; read with bagel_debug_buffer 4 = pass 1, 5 = pass 2).
+ * Errors: E_CUDA (stamp buffer allocation). */
 int bagel_debug_trace(bagel_ctx* ctx, int enable);
 
 /* Tensor-core issue-rate microbenchmark: `ctas` CTAs (one per SM) each issue `iters`

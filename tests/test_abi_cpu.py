@@ -79,3 +79,23 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(bagel, "LIB", str(tmp_path / "nope.so"))
     with pytest.raises(RuntimeError, match="missing"):
         bagel.lib()
+
+
+def test_every_declaration_states_its_errors_and_core_calls_cite_the_paper():
+    """include/bagel.h contract: each entry point documents its error behaviour; the calls of the
+    path and around it cite the passage that defines the operation."""
+    src = open(HEADER).read()
+    blocks = re.finditer(r"/\*(.*?)\*/\s*((?:#define[^\n]*\n\s*)*(?:(?:const\s+)?\w+\s*\*?\s*\w+\s*\([^;]*\);\s*)+)",
+                         src, flags=re.S)
+    seen = set()
+    for m in blocks:
+        comment = m.group(1)
+        names = re.findall(r"(\w+)\s*\(", re.sub(r"#define[^\n]*\n", "", m.group(2)))
+        seen.update(names)
+        assert re.search(r"Errors?:|E_ARG|E_CUDA|E_STATE", comment), names
+        core = {"gp_load", "love_cache_build", "exact_cache_build", "gp_target_mode", "policy_configure",
+                "reward_configure", "rollout_cost_and_grad", "bagel_sample_states", "policy_adam_step",
+                "gp_log_marginal_likelihood", "bagel_gp_predict", "bagel_rollout_trace"}
+        if core & set(names):
+            assert re.search(r"P:\d+", comment), names
+    assert set(declared_functions()) <= seen
