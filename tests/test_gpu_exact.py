@@ -80,3 +80,20 @@ def test_exact_cache_rejects_large_n(bagel):
         ctx.exact_cache_build()
     assert ei.value.code == E_ARG
     ctx.close()
+
+
+def test_exact_cache_with_absolute_targets(bagel):
+    """The two variants together: exact variance (R = L^-1) and absolute targets (x' = mu + sigma eps)."""
+    wl = W.make_workload(plant="boom", N=400, rank=50, hidden=(16, 16), B=48, T=8, target="abs")
+    ctx = bagel.setup(wl, device=0, build_cache=False)
+    ctx.gp_target_mode(True)
+    ctx.exact_cache_build()
+    alphas, Rs = zip(*[(a.cpu().numpy(), r.cpu().numpy()) for a, r in (ctx.cache_get(m) for m in range(wl.p))])
+    mdl = O.Model(wl.X, wl.ell, wl.s, np.stack(alphas), np.stack(Rs), abs_target=True)
+    cost, grad = ctx.rollout_cost_and_grad(torch.from_numpy(wl.theta).cuda(), torch.from_numpy(wl.x0).cuda(),
+                                           torch.from_numpy(wl.goals).cuda(), wl.T, W.rollout_seed(4))
+    ref = O.rollout(mdl, wl.sizes, "xg", wl.theta, wl.Q, wl.sigma_r, wl.x0, wl.goals, wl.T, W.rollout_seed(4))
+    assert abs(cost - ref["cost"]) <= 1e-3 * abs(ref["cost"])
+    g = grad.double().cpu().numpy()
+    assert np.linalg.norm(g - ref["grad"]) <= 1e-3 * np.linalg.norm(ref["grad"])
+    ctx.close()

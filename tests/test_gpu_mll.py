@@ -99,3 +99,36 @@ def test_fit_recovers_prior_hyperparameters(bagel):
                                        y.astype(np.float32).astype(np.float64), phi)
     assert np.abs(go).max() < 0.5
     ctx.close()
+
+
+def test_mll_c4_dims_and_fit_then_rebuild(bagel):
+    """d = 5 inputs (the C4 hydraulic plant's shape) at N = 900 against the oracle, then the fitted
+    hyperparameters drive a new gp_load + LOVE cache (the Alg.1 order: learn the GP, then roll out)."""
+    from paper_2202_13638_b200.fit import fit_hyperparameters
+
+    wl = W.config("C4", N=900, B=8, T=3, rank=64)
+    ctx = bagel.setup(wl, device=0)
+    Xf, Yf = wl.X.astype(np.float64), wl.Y.astype(np.float64)
+    for m in (0, 3):
+        h = ctx.loaded_log_hyp(m)
+        v, g = ctx.log_marginal_likelihood(m, h)
+        vo, go = O.log_marginal_likelihood(Xf, Yf[:, m], h)
+        assert v == pytest.approx(vo, rel=1e-10)
+        assert np.all(np.abs(g - go) <= 1e-7 * np.abs(go).max() + 1e-9 * abs(vo))
+    phis = [fit_hyperparameters(ctx, m, iters=30, lr=0.05)[0] for m in range(wl.p)]
+    ell = np.exp(np.stack([ph[:wl.d] for ph in phis])).astype(np.float32)
+    s = np.exp([ph[wl.d] for ph in phis]).astype(np.float32)
+    sn = np.exp([ph[wl.d + 1] for ph in phis]).astype(np.float32)
+    for m in range(wl.p):  # the fit improved every output's likelihood
+        assert ctx.log_marginal_likelihood(m, phis[m], want_grad=False)[0] > ctx.log_marginal_likelihood(m)[0]
+    ctx.gp_load(wl.X, wl.Y, ell, s, sn)
+    ctx.love_cache_build(64)
+    ctx.policy_configure(wl.sizes)
+    ctx.reward_configure(wl.Q, wl.sigma_r)
+    cost, grad = ctx.rollout_cost_and_grad(wl.theta, wl.x0, wl.goals, wl.T, W.rollout_seed(0))
+    mdl = O.Model.build(wl.X, wl.Y, ell, s, sn, 64)
+    ref = O.rollout(mdl, wl.sizes, "xg", wl.theta, wl.Q, wl.sigma_r, wl.x0, wl.goals, wl.T, W.rollout_seed(0))
+    assert abs(cost - ref["cost"]) <= 1e-3 * abs(ref["cost"])
+    g = grad.double().cpu().numpy()
+    assert np.linalg.norm(g - ref["grad"]) <= 1e-3 * np.linalg.norm(ref["grad"])
+    ctx.close()
