@@ -110,3 +110,20 @@ def test_training_run_matches_oracle_sampled_goals(bagel):
     t = th.cpu().numpy().astype(np.float64)
     assert np.linalg.norm(t - th_o) <= 1e-3 * np.linalg.norm(th_o)
     ctx.close()
+
+
+def test_exp1_shape_reaches_the_spec_return_bar(bagel):
+    """SPEC S:416's end-to-end bar on the Exp. 1 shape (workload E1: n = 2200, b = 100, H = 300,
+    policy [8, 8], fixed start and goal, Adam lr 1e-2): the mean return per step
+    exceeds 0.85 within 100 iterations.  (A property of the whole loop; the oracle is too slow for
+    this shape, its agreement with the GPU loop is checked above on small problems.)"""
+    from paper_2202_13638_b200.train import train_policy
+
+    wl = W.config("E1")
+    ctx = bagel.setup(wl, device=0)
+    th, log = train_policy(ctx, wl.theta, wl.T, 100, wl.B, x0=wl.x0, goals=wl.goals, lr=1e-2)
+    per_step = -np.array(log.cost) / (wl.T + 1)
+    assert per_step[:5].mean() < 0.2          # starts far from the goal
+    assert per_step[-5:].mean() > 0.85, per_step[-10:]
+    assert log.skipped == 0 and log.seconds[-1] < 30.0  # the paper's "under 30 seconds" (P:20), as a sanity bound
+    ctx.close()
