@@ -77,6 +77,7 @@ def lib():
             L.orc_love_predict.argtypes = [C.POINTER(GP), _dp, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
             L.orc_reward_fn.argtypes = [C.POINTER(Reward), C.c_int, _dp, _dp]
             L.orc_reward_fn.restype = C.c_double
+            L.orc_policy_act.argtypes = [C.POINTER(Policy), C.c_int, _dp, _dp, C.c_int, _dp]
             L.orc_rollout.argtypes = [C.POINTER(GP), C.POINTER(Policy), C.POINTER(Reward), _dp, _dp,
                                       C.c_int, C.c_int, C.c_uint64, C.c_longlong, C.c_longlong,
                                       C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_uint64]
@@ -219,6 +220,18 @@ def reward(Q, sigma_r, x, g) -> float:
     Q, x, g = _d(Q), _d(x), _d(g)
     rw = Reward(_ptr(Q), float(sigma_r))
     return lib().orc_reward_fn(C.byref(rw), x.shape[0], _ptr(x), _ptr(g))
+
+
+def policy_act(sizes, phi_mode, theta, x, g) -> np.ndarray:
+    """u = pi(x, g) for every row (the oracle's tanh MLP, PyTorch nn.Sequential parameter order)."""
+    x, g, theta = _d(np.atleast_2d(x)), _d(np.atleast_2d(g)), _d(theta)
+    B, p = x.shape
+    sz = np.ascontiguousarray(sizes, dtype=np.int32)
+    pm = {"xg": 0, "xgd": 1}[phi_mode] if isinstance(phi_mode, str) else int(phi_mode)
+    pol = Policy(len(sizes) - 1, sz.ctypes.data_as(_ip), pm, _ptr(theta))
+    u = np.zeros((B, int(sizes[-1])))
+    lib().orc_policy_act(C.byref(pol), p, _ptr(x), _ptr(g), B, _ptr(u))
+    return u
 
 
 def rollout(model: Model, sizes, phi_mode, theta, Q, sigma_r, x0, goals, T, seed, traj_offset=0,

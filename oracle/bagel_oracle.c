@@ -533,6 +533,19 @@ static void orc_mlp_forward(const orc_policy* pol, int p, const double* x, const
     }
 }
 
+/* Test export of the policy forward above: u_b = pi(x_b, g_b) for B rows (R13/R14),
+ * u is B x sizes[n_layers].  Pinned against torch.nn.Sequential in tests/test_oracle_rollout.py. */
+void orc_policy_act(const orc_policy* pol, int p, const double* x, const double* g, int B, double* u)
+{
+    const int maxw = orc_max_width(pol), q = pol->sizes[pol->n_layers];
+    double* h = (double*)malloc(sizeof(double) * (size_t)(pol->n_layers + 1) * maxw);
+    for (int b = 0; b < B; ++b) {
+        orc_mlp_forward(pol, p, x + (size_t)b * p, g + (size_t)b * p, h, maxw);
+        for (int o = 0; o < q; ++o) u[(size_t)b * q + o] = h[(size_t)pol->n_layers * maxw + o];
+    }
+    free(h);
+}
+
 /* Eq.8: r = exp(-(1/(2 sigma_r^2)) sum_c Q_c (x_c - g_c)^2) */
 double orc_reward_fn(const orc_reward* rw, int p, const double* x, const double* g)
 {

@@ -234,3 +234,39 @@ def test_gradient_directional_fd_absolute_targets():
     # and it is a different dynamics from the Delta form on the same data
     mdl_d = O.Model(mdl.X, mdl.ell, mdl.s, mdl.alpha, mdl.R, abs_target=False)
     assert abs(_run(wl, mdl_d, goals=goals)["cost"] - base["cost"]) > 1e-3
+
+
+@pytest.mark.parametrize("phi_mode", ["xg", "xgd"])
+@pytest.mark.parametrize("hidden", [(16,), (64, 64), (8, 8, 5)])
+def test_policy_forward_matches_torch_sequential(phi_mode, hidden):
+    """The oracle's policy (P:129 pi(x, x_g), P:149 "bounded in [-1, 1] using a saturating function";
+    readings R13/R14) against torch.nn.Sequential(Linear, Tanh, ..., Linear, Tanh) in float64 with
+    NONZERO weights.  theta is torch's own flattening of the module's parameters
+    (parameters_to_vector: W_l [out x in] row-major, then b_l, layer by layer), so a transposed W,
+    a swapped bias or a permuted phi block fails here.  phi = [x, g] (in = 2p) or [x, g, g - x]
+    (in = 3p)."""
+    import torch
+
+    p, q = 2, 1
+    n_in = (2 if phi_mode == "xg" else 3) * p
+    sizes = (n_in,) + tuple(hidden) + (q,)
+    torch.manual_seed(7)
+    layers = []
+    for a, b in zip(sizes[:-1], sizes[1:]):
+        layers += [torch.nn.Linear(a, b, dtype=torch.float64), torch.nn.Tanh()]
+    net = torch.nn.Sequential(*layers)
+    with torch.no_grad():
+        for prm in net.parameters():   # nonzero biases too (default init leaves them small)
+            prm.uniform_(-1.5, 1.5)
+    theta = torch.nn.utils.parameters_to_vector(net.parameters()).detach().numpy()
+    assert theta.shape[0] == W.n_params(sizes)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1.5, 1.5, (40, p))
+    g = rng.uniform(-1.5, 1.5, (40, p))
+    xt, gt = torch.from_numpy(x), torch.from_numpy(g)
+    phi = torch.cat([xt, gt] if phi_mode == "xg" else [xt, gt, gt - xt], dim=1)
+    with torch.no_grad():
+        ref = net(phi).numpy()
+    u = O.policy_act(sizes, phi_mode, theta, x, g)
+    assert np.max(np.abs(u - ref)) <= 1e-14
+    assert np.std(ref) > 0.1  # the check is not vacuous (saturated or constant outputs)
