@@ -61,6 +61,11 @@ int bagel_set_stream(bagel_ctx* ctx, void* cuda_stream);
  * Errors: none (returns a string). */
 const char* bagel_last_error(const bagel_ctx* ctx);
 
+/* SHA-256 (hex) of the sources, headers and compiler flags this library was
+ * built from (paper_2202_13638_b200/build.py); the binding refuses a library
+ * whose hash differs from the tree it is loaded from.  Errors: none. */
+const char* bagel_build_hash(void);
+
 /* --------------------------------------------------------------- GP model */
 
 /* gp_load -- the GP transition model of Eq.1-4: one independent

@@ -9,11 +9,13 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import subprocess
 import threading
 
 import numpy as np
 import torch
 
+from . import build as _build
 from .build import LIB
 
 _lock = threading.Lock()
@@ -34,9 +36,22 @@ def lib() -> C.CDLL:
     global _lib
     with _lock:
         if _lib is None:
+            # content-hash check: a stale library (sources changed since it was built) is rebuilt
+            # with nvcc, never silently used; no nvcc and no library -> loud failure
+            in_tree = LIB == _build.LIB
+            if in_tree:
+                try:
+                    _build.ensure_built()
+                except (OSError, subprocess.CalledProcessError) as e:
+                    raise RuntimeError(f"{LIB} is missing or stale and could not be rebuilt ({e}); build it with "
+                                       "`python -c 'import __graft_entry__ as g; g.build()'`") from e
             if not os.path.exists(LIB):
                 raise RuntimeError(f"{LIB} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
             L = C.CDLL(LIB)
+            L.bagel_build_hash.restype = C.c_char_p
+            got, want = L.bagel_build_hash().decode(), _build.source_hash()
+            if in_tree and got != want:
+                raise RuntimeError(f"{LIB} was built from other sources (hash {got[:12]} != tree {want[:12]})")
             L.bagel_create.argtypes = [C.POINTER(_vp), C.c_int, _vp]
             L.bagel_destroy.argtypes = [_vp]
             L.bagel_set_stream.argtypes = [_vp, _vp]
@@ -77,7 +92,7 @@ def lib() -> C.CDLL:
     return _lib
 
 
-EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_error", "gp_load", "love_cache_build",
+EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_error", "bagel_build_hash", "gp_load", "love_cache_build",
            "policy_configure", "reward_configure", "rollout_cost_and_grad", "bagel_last_launch_count",
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",

@@ -316,7 +316,15 @@ void prof_drain(bagel_ctx* c) {
   c->prof_pending.clear();
 }
 
-bool use_tc(const bagel_ctx* c) { return c->gp_kernel == 1 && tc_supported(c); }
+// The tensor-core GP step is THE path; the v0 CUDA-core kernels run only when a test selects them
+// explicitly (bagel_set_gp_kernel(0), a precision cross-check).  A shape the tensor-core kernels
+// cannot hold is an error, never a silent switch to another implementation.
+bool use_tc(bagel_ctx* c) {
+  if (c->gp_kernel != 1) return false;
+  REQUIRE(tc_supported(c), BAGEL_E_ARG, "GP shape (N=%d, d=%d, k=%d) exceeds the tensor-core kernels' shared memory",
+          c->N, c->d, c->k);
+  return true;
+}
 
 // Forward rollout (shared by rollout_cost_and_grad and bagel_rollout_trace).
 int forward(bagel_ctx* c, const float* theta, const float* x0, const float* goals, int B, int T,
@@ -363,6 +371,9 @@ void load_common_rollout_args(bagel_ctx* c, const float* theta, const float* x0,
   require_ready(c, true);
   REQUIRE(B >= 1, BAGEL_E_ARG, "B must be >= 1 (got %d)", B);
   REQUIRE(T >= 0, BAGEL_E_ARG, "T must be >= 0 (got %d)", T);
+  // the numeric-fault report encodes (step, row) as one int (t * B + b)
+  REQUIRE((long long)B * (long long)(T + 1) < 2147483647LL, BAGEL_E_ARG,
+          "B * (T + 1) must be < 2^31 (got B = %d, T = %d)", B, T);
   REQUIRE(theta && x0 && goals, BAGEL_E_ARG, "policy_params, x0 and goals must be non-NULL");
   const size_t np = (size_t)c->pol.n_params, bp = (size_t)B * c->p;
   ensure_stage(c, np + 2 * bp + 256);
@@ -428,6 +439,11 @@ extern "C" int bagel_set_stream(bagel_ctx* c, void* cuda_stream) {
 }
 
 extern "C" const char* bagel_last_error(const bagel_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+#ifndef BAGEL_SRC_HASH
+#define BAGEL_SRC_HASH "unknown"
+#endif
+extern "C" const char* bagel_build_hash(void) { return BAGEL_SRC_HASH; }
 
 extern "C" int gp_load(bagel_ctx* c, const float* X, const float* y, int N, int d, int p,
                        const float* lengthscales, const float* outputscale, const float* noise) {

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <stdint.h>
 
 #include <string>
@@ -183,6 +184,16 @@ struct bagel_ctx {
   double prof_ms[8] = {};
   long long prof_n[8] = {};
 };
+
+// True the first time it is called for the current device: kernel attributes such as the
+// dynamic shared-memory opt-in are set per device, so a process driving several GPUs (one
+// context each) sets them once on every device, not once per process.
+inline bool bagel_first_on_device(std::atomic<unsigned long long>& devices) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  return !(devices.fetch_or(bit) & bit);
+}
 
 // Opt a kernel into the largest dynamic shared memory the device allows next to its
 // static shared memory (capped at `want`); never leaves a pending CUDA error behind.

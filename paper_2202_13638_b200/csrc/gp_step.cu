@@ -342,11 +342,8 @@ int gs_pass2(const bagel_ctx* c, const float* xstar, int B, cudaStream_t st) {
   dim3 grid(cdiv(B, P2_BM), c->gp.p, S2);
   const size_t smem = gs_pass2_smem(c->gp.k, c->gp.d);
   DISPATCH_D(c->gp.d, ({
-    static bool attr_set = false;  // per-process: the attribute is a function property
-    if (!attr_set) {
-      bagel_set_smem_attr(k_pass2<D>, 200 * 1024);
-      attr_set = true;
-    }
+    static std::atomic<unsigned long long> devices{0};  // the opt-in is per device
+    if (bagel_first_on_device(devices)) bagel_set_smem_attr(k_pass2<D>, 200 * 1024);
     k_pass2<D><<<grid, P2_THREADS, smem, st>>>(c->gp, xstar, B, c->X, c->Xs, c->V, c->ws.Z, nps, c->ws.P2);
   }));
   return 1;

@@ -1446,9 +1446,8 @@ size_t tc_zpart_count(const bagel_ctx* c, int B) { return (size_t)c->p * cdiv(c-
 size_t tc_gbar_count() { return (size_t)GB_STRIDE; }
 
 static void set_attrs() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static std::atomic<unsigned long long> devices{0};
+  if (!bagel_first_on_device(devices)) return;
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
       bagel_set_smem_attr(k_p1_tc<D, false>, 220 * 1024);

@@ -599,11 +599,9 @@ int mlp_tc_pack(bagel_ctx* c, const float* theta, cudaStream_t st) {
 // One adjoint step t of a wide policy on the tensor cores (replaces k_mlp_bwd; the caller runs
 // k_xbar_init first and the steps t = T-1 .. 0).
 int mlp_tc_backward_step(const bagel_ctx* c, const float* goals, int B, int t, long long B_global, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> devices{0};
+  if (bagel_first_on_device(devices))
     cudaFuncSetAttribute(mtc::k_mlp_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mtc::smem_bytes());
-    attr = true;
-  }
   const Workspace& w = c->ws;
   mtc::Args af{};
   af.P = c->pol;
@@ -630,11 +628,9 @@ int mlp_tc_backward_step(const bagel_ctx* c, const float* goals, int B, int t, l
 }
 
 int mlp_tc_forward_step(const bagel_ctx* c, const float* theta, const float* goals, int B, int t, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> devices{0};
+  if (bagel_first_on_device(devices))
     cudaFuncSetAttribute(mtc::k_mlp_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mtc::smem_bytes());
-    attr = true;
-  }
   const Workspace& w = c->ws;
   mtc::Args a{};
   a.P = c->pol;

@@ -328,9 +328,8 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp_bwd(PolicyDesc P, RewardDes
 size_t mlp_smem() { return sizeof(float) * (2 * MLP_RB * MLP_LD + 2 * BAGEL_MAX_WIDTH * MLP_WK); }
 
 void mlp_set_attrs() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static std::atomic<unsigned long long> devices{0};
+  if (!bagel_first_on_device(devices)) return;
   for (int dv = 2; dv <= 8; ++dv) {
     DISPATCH_D(dv, ({
       bagel_set_smem_attr(k_mlp_fwd<D>, mlp_smem());

@@ -616,9 +616,8 @@ size_t ro_policy_smem(const PolicyDesc& P) { return policy_smem(P); }
 size_t ro_epilogue_smem(const PolicyDesc& P) { return epi_smem(P); }
 
 void ro_set_attributes() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+  static std::atomic<unsigned long long> devices{0};
+  if (!bagel_first_on_device(devices)) return;
   bagel_set_smem_attr(k_theta_grad<2, 4, 4>, 200 * 1024);
   bagel_set_smem_attr(k_theta_grad<2, 8, 8>, 200 * 1024);
   for (int dv = 2; dv <= 8; ++dv) {

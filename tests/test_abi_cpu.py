@@ -81,6 +81,17 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
         bagel.lib()
 
 
+def test_stale_library_is_detected_by_content(monkeypatch):
+    """Staleness is the sources' content hash (compiled into the library and stored next to it), not
+    file mtimes: a library built from other sources is never reused."""
+    from paper_2202_13638_b200 import bagel, build
+
+    assert build.up_to_date()
+    assert bagel.lib().bagel_build_hash().decode() == build.source_hash()
+    monkeypatch.setattr(build, "built_hash", lambda: "0" * 64)
+    assert not build.up_to_date()
+
+
 def test_every_declaration_states_its_errors_and_core_calls_cite_the_paper():
     """include/bagel.h contract: each entry point documents its error behaviour; the calls of the
     path and around it cite the passage that defines the operation."""

@@ -2,8 +2,8 @@
 
 Tolerances (the north star's numbers read so that an
 fp32-accurate implementation can meet them):
-  mean      |d mu| <= 1e-4 |mu| + 32 u sum_n |k_n alpha_n|
-  variance  |d v|  <= 1e-4 |v|  + 32 u 2 sum_j |z_j| sum_n |R_jn k_n|
+  mean      |d mu| <= 1e-4 |mu| + 16 u sum_n |k_n alpha_n|
+  variance  |d v|  <= 1e-4 |v|  + 16 u 2 sum_j |z_j| sum_n |R_jn k_n|
   Jacobians |d J|  <= 1e-3 |J|  + 64 u (conditioning term) (|x*_c| + max|X_c|) / l_c^2
   cost      |d L|  <= 1e-3 |L|;  gradient ||d g|| <= 1e-3 ||g||
   eps       raw Philox u32 bit-identical; eps within 1e-6 (1 + |eps|)
@@ -77,8 +77,8 @@ def test_rollout_normals_match_oracle(bagel):
 def _check_predict(wl, mdl, mean, var, dmean, dvar, xs):
     om, ov, ojm, ojv, mb, vb = mdl.predict(xs)
     mean, var, dmean, dvar = [t.double().cpu().numpy() for t in (mean, var, dmean, dvar)]
-    tol_m = 1e-4 * np.abs(om) + 32 * U32 * mb
-    tol_v = 1e-4 * np.abs(ov) + 32 * U32 * vb
+    tol_m = 1e-4 * np.abs(om) + 16 * U32 * mb
+    tol_v = 1e-4 * np.abs(ov) + 16 * U32 * vb
     em = np.abs(mean - om)
     ev = np.abs(var - ov)
     assert np.all(em <= tol_m), f"mean: worst ratio {np.max(em / tol_m):.3g}"
@@ -115,6 +115,34 @@ def test_gp_predict_single_point_and_far_field(bagel, small):
     mean, var, dm, dv = ctx.gp_predict(torch.from_numpy(xs).cuda())
     assert np.all(np.abs(mean.cpu().numpy()) < 1e-12)
     assert np.allclose(var.cpu().numpy()[0], wl.s, rtol=1e-6)
+
+
+def test_c1_wellcond_literal_relative_1e4(bagel):
+    """The north star's literal per-step tolerance, relative 1e-4 on mean and variance, on the
+    well-conditioned instance SURVEY §8(c) names "C1-wellcond": C1 with noise = 0.1 s (Eq.2-3,
+    P:67-70), asserted on the points where a relative bound is meaningful: |mu| >= 0.1 std(y) for
+    the mean and v >= 1e-2 s for the variance (near mu = 0 crossings and v -> 0 any fp32
+    implementation loses relative accuracy; those points are covered by the conditioning-aware
+    bounds of _check_predict)."""
+    wl = W.config("C1")
+    wl.noise = (0.1 * wl.s).astype(np.float32)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl)
+    rng = np.random.default_rng(31)
+    xs = np.concatenate([wl.X[rng.integers(0, wl.N, 300)] + rng.normal(0, 0.1, (300, wl.d)),
+                         rng.uniform(-2.0, 2.0, (212, wl.d))]).astype(np.float32)
+    mean, var, _, _ = [t.double().cpu().numpy() for t in ctx.gp_predict(torch.from_numpy(xs).cuda())]
+    om, ov = mdl.predict(xs.astype(np.float64))[:2]
+    sy = wl.Y.astype(np.float64).std(axis=0)
+    sel_m = np.abs(om) >= 0.1 * sy[None, :]
+    sel_v = ov >= 1e-2 * wl.s.astype(np.float64)[None, :]
+    assert sel_m.sum() > 100 and sel_v.sum() > 100
+    rel_m = np.abs(mean - om)[sel_m] / np.abs(om)[sel_m]
+    rel_v = np.abs(var - ov)[sel_v] / ov[sel_v]
+    print(f"C1-wellcond: mean rel max {rel_m.max():.2e} ({sel_m.sum()} pts), var rel max {rel_v.max():.2e} "
+          f"({sel_v.sum()} pts)")
+    assert rel_m.max() <= 1e-4
+    assert rel_v.max() <= 1e-4
 
 
 # ------------------------------------------------------------------ cache build (a0)
