@@ -935,30 +935,35 @@ __global__ void __launch_bounds__(256) k_r1b_tc(R1Args a, const double* __restri
   __shared__ float scale_s[32];
   __shared__ double t_s[8][32];
   __shared__ float mx_s[8][32];
-  __shared__ float h_s[8][32][1 + D];
+  __shared__ double lv_s[32][33];  // nct == 1: the fused reduce's 32 "lane values" of ||z||^2, per row
   {
-    // warp w: j groups w, w+8, ... and splits w, w+8, ... (partials combined below in fixed order)
+    // warp w: j groups w, w+8, ... (max|z|; ||z||^2 partials when nct > 1)
     const int njg = cdiv_dev(g.k, R1_JG);
     double t = 0.0;
     float mx = 0.0f;
-    float h[1 + D];
-#pragma unroll
-    for (int c = 0; c <= D; ++c) h[c] = 0.0f;
     if (ok) {
       for (int i = w; i < njg; i += 8) {
-        t += zz_part[((size_t)m * njg + i) * a.B + row];
+        if (g.nct > 1) t += zz_part[((size_t)m * njg + i) * a.B + row];
         mx = fmaxf(mx, zmax_part[((size_t)m * njg + i) * a.B + row]);
       }
-      for (int s = w; s < a.S1; s += 8) {
-        const float* src = a.P1h + ((size_t)(s * g.p + m) * a.B + row) * (1 + D);
+      if (g.nct == 1) {
+        // ||z||^2 in EXACTLY the order of the fused reduce (p1_reduce), so a row's variance does not
+        // depend on which of the two paths the launch shape selects: "lane value" l = sequential sum
+        // of columns 4l..4l+3 then 128+4l..128+4l+3, then an xor butterfly over the 32 lane values
+        for (int l = w; l < 32; l += 8) {
+          double zl = 0.0;
 #pragma unroll
-        for (int c = 0; c <= D; ++c) h[c] += src[c];
+          for (int e = 0; e < 8; ++e) {
+            const int j = (e < 4 ? 0 : 128) + 4 * l + (e & 3);
+            const float v = j < g.k ? a.Z[((size_t)m * g.k + j) * a.B + row] : 0.0f;
+            zl += (double)v * (double)v;
+          }
+          lv_s[l][lane] = zl;
+        }
       }
     }
     t_s[w][lane] = t;
     mx_s[w][lane] = mx;
-#pragma unroll
-    for (int c = 0; c <= D; ++c) h_s[w][lane][c] = h[c];
   }
   __syncthreads();
   if (w == 0) {
@@ -966,14 +971,32 @@ __global__ void __launch_bounds__(256) k_r1b_tc(R1Args a, const double* __restri
     if (ok) {
       double t = 0.0;
       float mx = 0.0f;
-      float h[1 + D];
-#pragma unroll
-      for (int c = 0; c <= D; ++c) h[c] = 0.0f;
       for (int i = 0; i < 8; ++i) {  // fixed order
         t += t_s[i][lane];
         mx = fmaxf(mx, mx_s[i][lane]);
+      }
+      if (g.nct == 1) {
+        double v[32];
 #pragma unroll
-        for (int c = 0; c <= D; ++c) h[c] += h_s[i][lane][c];
+        for (int l = 0; l < 32; ++l) v[l] = lv_s[l][lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          double nv[32];
+#pragma unroll
+          for (int l = 0; l < 32; ++l) nv[l] = v[l] + v[l ^ o];
+#pragma unroll
+          for (int l = 0; l < 32; ++l) v[l] = nv[l];
+        }
+        t = v[0];
+      }
+      // mean columns: the S1 split partials in split order (as p1_reduce)
+      float h[1 + D];
+#pragma unroll
+      for (int c = 0; c <= D; ++c) h[c] = 0.0f;
+      for (int s = 0; s < a.S1; ++s) {
+        const float* src = a.P1h + ((size_t)(s * g.p + m) * a.B + row) * (1 + D);
+#pragma unroll
+        for (int c = 0; c <= D; ++c) h[c] += src[c];
       }
       float inv;
       sc = pow2_scale_for(mx, &inv);
@@ -1409,27 +1432,26 @@ int tc_pack(bagel_ctx* c, int m, cudaStream_t st) {
 }
 
 
-// Pass-1 N splits: one wave of (row tile, m, ct, split) CTAs.  With nct == 1 the whole wave is
-// launched cooperatively and reduce 1 runs inside pass 1 after a grid barrier (k_p1_tc<D, true>);
-// BAGEL_P1_FUSED=0 forces the separate reduce launches.
+// N splits of both passes.  The split boundaries depend on N ONLY (never on B or the launch
+// shape), so every trajectory's arithmetic -- which training points share a TMEM accumulation
+// chain, and the order in which the split partials are summed -- is the same whether it runs in
+// a batch of 1 or 65,536, on one GPU or as one shard of eight: per-trajectory results are bitwise
+// batch-invariant (tests/test_gpu_parity.py::test_batch_invariance_bitwise).  N is cut into about
+// SPLIT_TARGET ranges (the C2 shape -- 8 row tiles x 2 outputs x 9 splits -- fills the 148 SMs in
+// one wave), each at most P1_MAX_TILES pass-1 tiles long: the tensor core's fp32 accumulation error
+// grows with the chain length (measured: the whole N = 50,000 in one chain put ||z||^2 off by
+// 4e-4 s, 1.5x the fp32 tolerance).  With nct == 1 and a one-wave grid, reduce 1
+// runs inside pass 1 after a grid barrier (k_p1_tc<D, true>); it sums in exactly the order of the
+// separate reduce kernels.  BAGEL_P1_FUSED=0 forces the separate reduce launches.
+constexpr int SPLIT_TARGET = 9;
 void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2, int* p1_fused) {
   const Geo g = geo_of(c);
   const int rt = cdiv(B, 128);
-  const int target = c->num_sms;  // one CTA per SM (smem-bound), one wave
-  int s1 = target / (rt * g.p * g.nct);  // floor: never more CTAs than SMs (one wave)
-  // ... but never a longer tcgen05 accumulation chain than P1_MAX_TILES N-tiles per TMEM
-  // accumulator: the tensor core's fp32 accumulation error grows with the chain length (measured:
-  // the whole N = 50,000 in one chain put ||z||^2 off by 4e-4 s, 1.5x the fp32 tolerance; DESIGN.md
-  // §7), so long ranges are split and the partials summed on the CUDA cores (multi-wave grids)
-  s1 = s1 < cdiv(g.nt1, P1_MAX_TILES) ? cdiv(g.nt1, P1_MAX_TILES) : s1;
-  s1 = s1 < 1 ? 1 : (s1 > g.nt1 ? g.nt1 : s1);
-  *tps1 = cdiv(g.nt1, s1);
+  *tps1 = std::min(P1_MAX_TILES, std::max(1, cdiv(g.nt1, SPLIT_TARGET)));
   *S1 = cdiv(g.nt1, *tps1);
   const char* env = getenv("BAGEL_P1_FUSED");
-  *p1_fused = g.nct == 1 && rt * g.p * *S1 <= target && !(env && env[0] == '0');
-  int s2 = target / (rt * g.p * g.njt);
-  s2 = s2 < 1 ? 1 : (s2 > g.nt2 ? g.nt2 : s2);
-  *tps2 = cdiv(g.nt2, s2);
+  *p1_fused = g.nct == 1 && rt * g.p * *S1 <= c->num_sms && !(env && env[0] == '0');
+  *tps2 = std::max(1, cdiv(g.nt2, SPLIT_TARGET));
   *S2 = cdiv(g.nt2, *tps2);
 }
 

@@ -48,3 +48,40 @@ def rollout_cost_and_grad_dp(local_fn, theta, x0_global, goals_global, T: int, s
     off, bl = shard(B, world, rank)
     cost, grad = local_fn(theta, x0_global[off:off + bl], goals_global[off:off + bl], T, seed, off, B)
     return allreduce_cost_grad(cost, grad, group)
+
+
+def pin_nccl() -> None:
+    """Fix NCCL's algorithm and protocol (SURVEY §8(e) determinism): with them pinned the one
+    all_reduce per iteration sums in the same order every run, so results are bitwise repeatable at
+    a fixed world size.  Ring + LL: the message is |theta| + 1 doubles (tens of KB, latency bound).
+    Call before init_process_group; explicit user settings win."""
+    import os
+
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "LL")
+
+
+def cache_digest(ctx, p: int) -> torch.Tensor:
+    """Order-sensitive 64-bit digest of the context's LOVE cache (alpha and R of every output, as raw
+    float64 bits), as a 1-element int64 tensor on the context's device."""
+    acc = torch.zeros(1, dtype=torch.int64, device=ctx.dev)
+    for m in range(p):
+        a, R = ctx.cache_get(m)
+        for t in (a, R):
+            bits = t.contiguous().view(torch.int64).reshape(-1)
+            w = torch.arange(1, bits.numel() + 1, device=bits.device, dtype=torch.int64) * 0x9E3779B1
+            acc = acc * 1000003 + (bits ^ w).sum().reshape(1)   # int64 arithmetic wraps
+    return acc
+
+
+def verify_replicated_cache(ctx, p: int, group=None) -> None:
+    """Each rank builds the replicated LOVE cache itself (deterministic fixed-order fp64 build); check
+    that every rank's copy is bit-identical (min == max of the digest over ranks), else raise."""
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size(group) == 1:
+        return
+    d = cache_digest(ctx, p)
+    lo, hi = d.clone(), d.clone()
+    tdist.all_reduce(lo, op=tdist.ReduceOp.MIN, group=group)
+    tdist.all_reduce(hi, op=tdist.ReduceOp.MAX, group=group)
+    if int(lo.item()) != int(hi.item()):
+        raise RuntimeError("LOVE caches differ across ranks (non-deterministic cache build)")

@@ -1,5 +1,7 @@
-"""Diagnostic (GPU box): per-trajectory gradient error of the CUDA path vs the oracle at C2,
-with each trajectory's minimum LOVE variance / s and how far it strays from the data box."""
+"""Diagnostic (GPU box): per-trajectory C2 gradients of the tensor-core path (gp kernel 1) and the
+v0 CUDA-core FFMA path (gp kernel 0), one B = 1 launch per trajectory (bitwise equal to the
+full-batch launch, test_batch_invariance_bitwise), saved for comparison with the oracle on the CPU.
+    python scripts/diag_c2_grad.py OUTDIR [seed_iterations...]"""
 import os
 import sys
 
@@ -7,38 +9,31 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import oracle as O  # noqa: E402
 import workloads as W  # noqa: E402
 from paper_2202_13638_b200 import bagel  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+out = sys.argv[1]
+its = [int(a) for a in sys.argv[2:]] or [1]
+os.makedirs(out, exist_ok=True)
 wl = W.config("C2")
-mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
 ctx = bagel.setup(wl, device=0)
-seed = W.rollout_seed(1)
-tr = ctx.rollout_trace(wl.theta, wl.x0, wl.goals, wl.T, seed)
-var = tr["var"].double().cpu().numpy()  # T x B x p
-x = tr["x"].double().cpu().numpy()
-lo, hi = wl.X[:, :2].min(0), wl.X[:, :2].max(0)
-rows = []
-gsum_g = np.zeros(wl.n_params)
-gsum_o = np.zeros(wl.n_params)
-for b in range(n):
-    c, g = ctx.rollout_cost_and_grad(torch.from_numpy(wl.theta).cuda(), torch.from_numpy(wl.x0[b:b + 1]).cuda(),
-                                     torch.from_numpy(wl.goals[b:b + 1]).cuda(), wl.T, seed, traj_offset=b,
-                                     B_global=wl.B)
-    g = g.double().cpu().numpy()
-    ref = O.rollout(mdl, wl.sizes, "xg", wl.theta, wl.Q, wl.sigma_r, wl.x0[b:b + 1], wl.goals[b:b + 1], wl.T,
-                    seed, traj_offset=b, B_global=wl.B)
-    gsum_g += g
-    gsum_o += ref["grad"]
-    out = np.maximum(0, np.maximum(lo - x[:, b], x[:, b] - hi)).max()
-    rows.append((np.linalg.norm(g - ref["grad"]), np.linalg.norm(ref["grad"]), abs(c - ref["cost"]) / abs(ref["cost"]),
-                 (var[:, b] / wl.s).min(), out, b))
-rows.sort(reverse=True)
-print("abs_err  |g_b|  cost_rel  min(v/s)  out_of_box  b")
-for r in rows[:15]:
-    print("%.3e %.3e %.2e %.2e %.3f %d" % r)
-print("sum over %d trajectories: grad rel L2 = %.3e" % (n, np.linalg.norm(gsum_g - gsum_o) / np.linalg.norm(gsum_o)))
-print("global min v/s over batch:", (var / wl.s).min(), " fraction of (t,b,m) with v/s < 1e-4:",
-      np.mean(var / wl.s < 1e-4))
+th = torch.from_numpy(wl.theta).cuda()
+for kern in (1, 0):
+    ctx.set_gp_kernel(kern)
+    for it in its:
+        seed = W.rollout_seed(it)
+        G = np.zeros((wl.B, wl.n_params), dtype=np.float32)
+        cost = np.zeros(wl.B)
+        for b in range(wl.B):
+            c, g = ctx.rollout_cost_and_grad(th, torch.from_numpy(wl.x0[b:b + 1]).cuda(),
+                                             torch.from_numpy(wl.goals[b:b + 1]).cuda(), wl.T, seed, traj_offset=b,
+                                             B_global=wl.B)
+            G[b] = g.cpu().numpy()
+            cost[b] = c
+        cf, gf = ctx.rollout_cost_and_grad(th, torch.from_numpy(wl.x0).cuda(), torch.from_numpy(wl.goals).cuda(),
+                                           wl.T, seed)
+        np.savez_compressed(os.path.join(out, f"grad_k{kern}_it{it}.npz"), G=G, cost=cost, gfull=gf.cpu().numpy(),
+                            cfull=cf)
+        print(kern, it, "full-batch vs sum of B=1 runs:",
+              np.linalg.norm(G.astype(np.float64).sum(0) - gf.cpu().numpy()) / np.linalg.norm(gf.cpu().numpy()),
+              flush=True)

@@ -174,3 +174,71 @@ def test_two_rank_training_loop_equals_single_process():
     assert np.array_equal(t0, t1)  # replicated parameters stay identical on every rank
     np.testing.assert_allclose(c0, costs_ref, rtol=1e-5)
     np.testing.assert_allclose(t0, th_ref, rtol=1e-5, atol=1e-6)
+
+
+class _CacheCtx:
+    """Stand-in exposing cache_get (alpha, R per output) on CPU for the replicated-cache check."""
+
+    def __init__(self, rank, corrupt):
+        self.dev = torch.device("cpu")
+        g = torch.Generator().manual_seed(5)
+        self.a = [torch.randn(50, generator=g, dtype=torch.float64) for _ in range(2)]
+        self.R = [torch.randn(7, 50, generator=g, dtype=torch.float64) for _ in range(2)]
+        if corrupt and rank == 1:
+            self.R[1][3, 17] = torch.nextafter(self.R[1][3, 17], torch.tensor(1e9, dtype=torch.float64))
+
+    def cache_get(self, m):
+        return self.a[m], self.R[m]
+
+
+def _cache_worker(rank, world, port, corrupt, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_13638_b200.dist import verify_replicated_cache
+
+        try:
+            verify_replicated_cache(_CacheCtx(rank, corrupt), 2)
+            q.put((rank, "same"))
+        except RuntimeError:
+            q.put((rank, "differ"))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("corrupt", [False, True])
+def test_replicated_cache_check_detects_one_ulp(corrupt):
+    """the LOVE cache is replicated, each rank building it deterministically; the bench
+    checks the copies are bit-identical across ranks -- one ulp of one R entry on one rank is caught."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cache_worker, args=(r, world, port, corrupt, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert {r[1] for r in res} == {"differ" if corrupt else "same"}
+
+
+def test_nccl_algorithm_and_protocol_are_pinned(monkeypatch):
+    from paper_2202_13638_b200.dist import pin_nccl
+
+    monkeypatch.delenv("NCCL_ALGO", raising=False)
+    monkeypatch.delenv("NCCL_PROTO", raising=False)
+    pin_nccl()
+    assert os.environ["NCCL_ALGO"] == "Ring" and os.environ["NCCL_PROTO"] == "LL"
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_strong_scaling_shards_c5_batch(world):
+    """bench.py's default strong scaling: C5's 65,536 trajectories split over the launched world,
+    contiguous global ids, every trajectory exactly once (8,192 per GPU at 8 GPUs)."""
+    blocks = [shard(65536, world, r) for r in range(world)]
+    assert sum(n for _, n in blocks) == 65536
+    assert all(n == 65536 // world for _, n in blocks)
+    assert [o for o, _ in blocks] == [r * (65536 // world) for r in range(world)]
