@@ -88,7 +88,10 @@ int gp_load(bagel_ctx* ctx, const float* X, const float* y, int N, int d, int p,
  * difference y = Delta x = x_{k+1} - x_k"):
  *   absolute = 0 (default, reading R6): Delta targets, x' = x + mu + sigma eps;
  *   absolute = 1 (NEXT-4): absolute targets, x' = mu + sigma eps, and the
- *   reverse pass drops the identity path dx'/dx = I.
+ *   reverse pass drops the identity path dx'/dx = I.  The GP step then runs on
+ *   the round-to-nearest CUDA-core kernels: with y = x_{k+1} the prior variance
+ *   is the states' variance and v = s - ||z||^2 cancels to ~1e-6 s, below what
+ *   the tensor core's truncating TMEM accumulation resolves (R38).
  * Applies to every later rollout / trace call; kept across gp_load.
  * Errors: E_ARG if absolute is not 0 or 1. */
 int gp_target_mode(bagel_ctx* ctx, int absolute);
@@ -101,7 +104,7 @@ int gp_target_mode(bagel_ctx* ctx, int absolute);
  *   then packs V_m = s_m [alpha_m | alpha_m o X | R_m^T] for the hot path.
  * Synchronous.  seconds_out [host, nullable] receives the wall time.
  * Errors: E_STATE without gp_load; E_ARG for rank < 1 or rank > N or rank >
- * 768; E_NUMERIC if a Cholesky pivot <= 0 (message carries the pivot index)
+ * 8192; E_NUMERIC if a Cholesky pivot <= 0 (message carries the pivot index)
  * or T is not positive definite; E_CUDA (incl. out of memory). */
 int love_cache_build(bagel_ctx* ctx, int rank, double* seconds_out);
 
@@ -112,8 +115,8 @@ int love_cache_build(bagel_ctx* ctx, int rank, double* seconds_out);
  * so every rollout / predict call afterwards uses the exact Eq.3 variance
  * k** - ||L^-1 k||^2 instead of the LOVE estimate (K^-1 = R^T R exactly).
  * Synchronous; seconds_out [host, nullable].  Replaces any LOVE cache.
- * Errors: E_STATE without gp_load; E_ARG if N > 768 (the largest rank the
- * hot-path kernels hold); E_NUMERIC if a Cholesky pivot <= 0; E_CUDA. */
+ * Errors: E_STATE without gp_load; E_ARG if N > 8192 (the largest rank the
+ * cache accepts; the paper's exact baseline is n = 2200); E_NUMERIC if a Cholesky pivot <= 0; E_CUDA. */
 int exact_cache_build(bagel_ctx* ctx, double* seconds_out);
 
 /* ------------------------------------------------------- policy / reward */
@@ -279,8 +282,8 @@ int bagel_cache_set(bagel_ctx* ctx, int m, int rank, const double* alpha, const 
 /* GP-step implementation selector (bench / A-B parity tests):
  *   1 (default) tcgen05 tensor-core kernels (csrc/gp_step_tc.cu),
  *   0 the v0 CUDA-core FFMA kernels (csrc/gp_step.cu), kept as a reference.
- * bagel_get_gp_kernel reports the path the next call will take (1 only if the
- * problem fits the tensor-core kernels' shared-memory budget).  Errors: E_ARG. */
+ * bagel_get_gp_kernel reports the path the next call will take (1 unless
+ * absolute targets are selected, gp_target_mode).  Errors: E_ARG. */
 int bagel_set_gp_kernel(bagel_ctx* ctx, int version);
 int bagel_get_gp_kernel(const bagel_ctx* ctx, int* version);
 

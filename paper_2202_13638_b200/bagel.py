@@ -180,7 +180,7 @@ class Context:
         self._check(self.L.gp_target_mode(self.h, int(bool(absolute))))
 
     def exact_cache_build(self) -> float:
-        """Exact-GP cache (R = L^-1 at rank N, N <= 768): exact Eq.3 variances from here on."""
+        """Exact-GP cache (R = L^-1 at rank N, N <= 8192): exact Eq.3 variances from here on."""
         sec = C.c_double(0.0)
         self._check(self.L.exact_cache_build(self.h, C.byref(sec)))
         return sec.value

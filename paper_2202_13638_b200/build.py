@@ -42,7 +42,9 @@ def deps():
 
 def source_hash() -> str:
     h = hashlib.sha256()
-    h.update(" ".join(ARCH + CFLAGS + LDFLAGS).encode())
+    # flags without the (machine-specific) absolute include path: a library built here must hash
+    # the same on the GPU box, where the tree lives elsewhere
+    h.update(" ".join(ARCH + [f for f in CFLAGS if not f.startswith("-I")] + LDFLAGS).encode())
     for f in deps():
         h.update(os.path.relpath(f, ROOT).encode())
         with open(f, "rb") as fh:

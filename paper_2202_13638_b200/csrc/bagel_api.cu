@@ -319,8 +319,14 @@ void prof_drain(bagel_ctx* c) {
 // The tensor-core GP step is THE path; the v0 CUDA-core kernels run only when a test selects them
 // explicitly (bagel_set_gp_kernel(0), a precision cross-check).  A shape the tensor-core kernels
 // cannot hold is an error, never a silent switch to another implementation.
+//
+// Absolute targets (gp_target_mode(1)) run on the v0 kernels: the tensor core accumulates in
+// TMEM with truncation (~1 ulp of the accumulator per MMA step, scripts/diag_tmem_acc.py), which
+// biases ||z|| low by ~steps x 2^-24 relative; with y = x_{k+1} the prior variance s is the states'
+// variance, v / s falls to ~1e-6 and v = s - ||z||^2 loses all accuracy (measured: gradient 7.5e-3
+// off at T = 40 vs 5.3e-4 for the round-to-nearest FFMA path; R38).
 bool use_tc(bagel_ctx* c) {
-  if (c->gp_kernel != 1) return false;
+  if (c->gp_kernel != 1 || c->gp.abs_target) return false;
   REQUIRE(tc_supported(c), BAGEL_E_ARG, "GP shape (N=%d, d=%d, k=%d) exceeds the tensor-core kernels' shared memory",
           c->N, c->d, c->k);
   return true;
@@ -926,7 +932,7 @@ extern "C" int bagel_set_gp_kernel(bagel_ctx* c, int version) {
 
 extern "C" int bagel_get_gp_kernel(const bagel_ctx* c, int* version) {
   if (!c || !version) return BAGEL_E_ARG;
-  *version = (c->gp_kernel == 1 && c->k > 0 && tc_supported(c)) ? 1 : (c->gp_kernel == 1 && c->k == 0 ? 1 : 0);
+  *version = (c->gp_kernel == 1 && !c->gp.abs_target && (c->k == 0 || tc_supported(c))) ? 1 : 0;
   return BAGEL_OK;
 }
 

@@ -13,7 +13,7 @@
 #define BAGEL_MAX_D 8        // d = p + q <= 8
 #define BAGEL_MAX_WIDTH 256  // widest MLP layer
 #define BAGEL_MAX_LAYERS 8
-#define BAGEL_MAX_RANK 768
+#define BAGEL_MAX_RANK 8192  // tensor-core kernels tile any k (256-column z tiles, 256-j pass-2 tiles)
 #define BAGEL_VAR_FLOOR 1e-12f
 #define BAGEL_BARRIER_TIMEOUT (-2)  // err_flag value: a grid barrier timed out (grid not co-resident)  // S:252 clamp (reading R19)
 

@@ -24,6 +24,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "bagel_internal.h"
 #include "policy_rows.cuh"
@@ -79,6 +80,14 @@ inline Geo make_geo(int N, int d, int p, int k) {
 // share a block of 2 x AUXW floats, field-major, point-minor -- so one float4 holds two fields
 // of both points, i.e. the two lanes of two fp32x2 operands.
 __host__ __device__ inline int aux_idx(int nn, int f) { return ((nn >> 1) * AUXW + f) * 2 + (nn & 1); }
+
+// Every split operand is carried at 2^14 times its (power-of-two normalised) value: fp16's normal
+// range starts at 2^-14, so the lo half of a value x (|lo| ~ 2^-12 |x|) stays normal -- i.e. keeps
+// its 11 significant bits -- down to |x| ~ 2^-16 instead of 2^-2 of the operand's scale.  Without
+// it, every ktilde < 1/4 (most of the training points a query sees) and every small R / z entry lost
+// precision to the absolute 2^-25 spacing of fp16 subnormals.  Values stay below 2^14 < 65504.
+// The 2^14 factors are exact and are undone in the epilogues (colscale, zrow_inv, aux 2^f_n).
+constexpr float SPLIT_UP = 16384.0f, SPLIT_DOWN = 1.0f / 16384.0f;
 
 __device__ __forceinline__ void split_f16(float v, __half& hi, __half& lo) {
   hi = __float2half_rn(v);
@@ -149,8 +158,8 @@ __global__ void k_colscale(const double* __restrict__ R, int N, int k, double s,
   if (threadIdx.x == 0) {
     float inv;
     const float sc = pow2_scale_for(red[0], &inv);
-    cs_inv[j] = sc;
-    cs[j] = inv;
+    cs_inv[j] = sc * SPLIT_UP;                // B operand at 2^14 x its normalised value
+    cs[j] = inv * (SPLIT_DOWN * SPLIT_DOWN);  // undoes the column scale and both operands' 2^14
   }
 }
 
@@ -176,8 +185,8 @@ __global__ void k_pack2(Geo g, const float* __restrict__ X, const double* __rest
     for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
     if (lane == 0) {
       float inv;
-      rsc[nn] = pow2_scale_for(a, &inv);
-      rinv[nn] = inv;
+      rsc[nn] = pow2_scale_for(a, &inv) * SPLIT_UP;
+      rinv[nn] = inv * SPLIT_DOWN;
     }
   }
   __syncthreads();
@@ -531,6 +540,10 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     float2 hacc2[1 + D];
 #pragma unroll
     for (int c = 0; c <= D; ++c) hacc2[c] = make_float2(0.0f, 0.0f);
+    // the mean columns belong to the z-column tile ct = 0 only; the other column tiles' CTAs skip
+    // that arithmetic (a third of the generator's FP32 work; C4 / C5 have two column tiles)
+    auto gen_tiles = [&](auto mean_tag) {
+    constexpr bool MEAN = decltype(mean_tag)::value;
     for (int i = 0; i < ntile; ++i) {
       const int s = i % ST1, x = i % STA;
       tc::mbar_wait(&full_x[x], (uint32_t)(i / STA) & 1u);             // aux rows of tile i landed
@@ -555,12 +568,15 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         // (no x* mu - sum k alpha X_c cancellation between two large sums)
         // mu keeps the fused k * (s alpha) + acc (one rounding per term: the mean is the most
         // cancellation-sensitive output); the Jacobian columns take the rounded product
-        hacc2[0] = fma2(kt, an[D], hacc2[0]);
-        const float2 ka = mul2(kt, an[D]);
+        if (MEAN) {
+          hacc2[0] = fma2(kt, an[D], hacc2[0]);
+          const float2 ka = mul2(kt, an[D]);
 #pragma unroll
-        for (int c = 0; c < D; ++c) hacc2[1 + c] = fma2(ka, dx[c], hacc2[1 + c]);
-        const __half2 h2 = __floats2half2_rn(kt.x, kt.y);
-        const float2 res = sub2(kt, __half22float2(h2));
+          for (int c = 0; c < D; ++c) hacc2[1 + c] = fma2(ka, dx[c], hacc2[1 + c]);
+        }
+        const float2 kts = mul2(kt, make_float2(SPLIT_UP, SPLIT_UP));  // exact
+        const __half2 h2 = __floats2half2_rn(kts.x, kts.y);
+        const float2 res = sub2(kts, __half22float2(h2));
         const __half2 l2 = __floats2half2_rn(res.x, res.y);
         hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
@@ -578,6 +594,9 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
       tc::mbar_arrive(&full_a[s]);
       tc::mbar_arrive(&empty_x[x]);
     }
+    };
+    if (ct == 0) gen_tiles(std::true_type{});
+    else gen_tiles(std::false_type{});
     if (gt == 0) stamp(a.dbg, 3);
     float hacc[1 + D];
 #pragma unroll
@@ -737,7 +756,8 @@ __device__ __forceinline__ void p1_reduce(const P1Args& a, const int bx, const i
         zm = fmaxf(zm, __shfl_xor_sync(0xffffffffu, zm, o));
       }
       float inv;
-      const float sc = pow2_scale_for(zm, &inv);
+      const float sc = pow2_scale_for(zm, &inv) * SPLIT_UP;
+      inv *= SPLIT_DOWN;
       const float h0 = __shfl_sync(0xffffffffu, hv, 0);
       const float v = (float)((double)a.s[mm] - zz);
       if (tid == 0) stamp(a.dbg, 10);
@@ -999,8 +1019,8 @@ __global__ void __launch_bounds__(256) k_r1b_tc(R1Args a, const double* __restri
         for (int c = 0; c <= D; ++c) h[c] += src[c];
       }
       float inv;
-      sc = pow2_scale_for(mx, &inv);
-      a.zrow_inv[(size_t)m * a.B + row] = inv;
+      sc = pow2_scale_for(mx, &inv) * SPLIT_UP;
+      a.zrow_inv[(size_t)m * a.B + row] = inv * SPLIT_DOWN;
       const float v = (float)((double)a.s[m] - t);
       const float sg = sqrtf(fmaxf(v, BAGEL_VAR_FLOOR));
       a.mu[(size_t)m * a.B + row] = h[0];
@@ -1447,7 +1467,9 @@ constexpr int SPLIT_TARGET = 9;
 void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2, int* p1_fused) {
   const Geo g = geo_of(c);
   const int rt = cdiv(B, 128);
-  *tps1 = std::min(P1_MAX_TILES, std::max(1, cdiv(g.nt1, SPLIT_TARGET)));
+  int max_tiles = P1_MAX_TILES;
+  if (const char* e = getenv("BAGEL_P1_MAX_TILES")) max_tiles = std::max(1, atoi(e));  // diagnostics only
+  *tps1 = std::min(max_tiles, std::max(1, cdiv(g.nt1, SPLIT_TARGET)));
   *S1 = cdiv(g.nt1, *tps1);
   const char* env = getenv("BAGEL_P1_FUSED");
   *p1_fused = g.nct == 1 && rt * g.p * *S1 <= c->num_sms && !(env && env[0] == '0');

@@ -63,8 +63,9 @@ def test_full_size_sampled_rows(bagel, name):
         ref = O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[b:b + 1], wl.goals[b:b + 1], wl.T, seed,
                         traj_offset=b, B_global=1, trace=True)
         # fp32 floor of this row (R30, R35): at N = 50,000 the predictive variance reaches
-        # v/s ~ 1e-5, below fp32's resolution of s - ||z||^2, so sigma (and the sampled state) carry
-        # percent-level errors there; the oracle's 2^-22 kernel-value perturbation measures it
+        # v/s ~ 1e-5, below fp32's resolution of s - ||z||^2 (and the tensor core's truncating
+        # accumulation over 80-tile chains, R37), so sigma and the sampled state carry percent-level
+        # errors there; the oracle's 2^-22 kernel-value perturbation of the same row measures it
         refp = O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[b:b + 1], wl.goals[b:b + 1], wl.T,
                          seed, traj_offset=b, B_global=1, perturb_mode=1, perturb_seed=7)
         floor = abs(refp["ret"][0] - ref["ret"][0])
