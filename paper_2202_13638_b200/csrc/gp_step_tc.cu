@@ -1473,7 +1473,12 @@ void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, in
   *S1 = cdiv(g.nt1, *tps1);
   const char* env = getenv("BAGEL_P1_FUSED");
   *p1_fused = g.nct == 1 && rt * g.p * *S1 <= c->num_sms && !(env && env[0] == '0');
-  *tps2 = std::max(1, cdiv(g.nt2, SPLIT_TARGET));
+  // pass 2 has no accumulation-chain bound (its TMEM chain runs over j, not N): the split only
+  // serves occupancy, which small problems need (C2: 8 row tiles x 2 outputs) and large ones do
+  // not -- there every extra split re-reads the CTA's 128 KB Z operand (C5: +6% pass-2 time at 9
+  // splits).  Still a function of N alone: about 9 splits at N = 5,000, one from N ~ 46,000 up.
+  const int s2 = std::max(1, std::min(SPLIT_TARGET, (SPLIT_TARGET * 40) / std::max(1, g.nt2)));
+  *tps2 = cdiv(g.nt2, s2);
   *S2 = cdiv(g.nt2, *tps2);
 }
 

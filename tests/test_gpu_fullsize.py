@@ -62,20 +62,41 @@ def test_full_size_sampled_rows(bagel, name):
     for b in rows:
         ref = O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[b:b + 1], wl.goals[b:b + 1], wl.T, seed,
                         traj_offset=b, B_global=1, trace=True)
-        # fp32 floor of this row (R30, R35): at N = 50,000 the predictive variance reaches
-        # v/s ~ 1e-5, below fp32's resolution of s - ||z||^2 (and the tensor core's truncating
-        # accumulation over 80-tile chains, R37), so sigma and the sampled state carry percent-level
-        # errors there; the oracle's 2^-22 kernel-value perturbation of the same row measures it
+        # the oracle's own fp32 floor of this row (2^-22 kernel-value perturbation), printed as
+        # context: at N = 50,000 the predictive variance reaches v/s ~ 1e-5 (R35, R37)
         refp = O.rollout(mdl, wl.sizes, phi, wl.theta, wl.Q, wl.sigma_r, wl.x0[b:b + 1], wl.goals[b:b + 1], wl.T,
                          seed, traj_offset=b, B_global=1, perturb_mode=1, perturb_seed=7)
         floor = abs(refp["ret"][0] - ref["ret"][0])
         err = abs(ret[b] - ref["ret"][0])
         print(f"{name} row {b}: return rel err {err / abs(ref['ret'][0]):.2e}, fp32 floor {floor / abs(ref['ret'][0]):.2e}")
-        assert err <= max(1e-3 * abs(ref["ret"][0]), 3 * floor), (name, b)
+        assert err <= 1e-3 * abs(ref["ret"][0]), (name, b)
         if name == "C4":
             np.testing.assert_allclose(x[:, b, :], ref["x"][:, 0, :], atol=1e-3, err_msg=f"{name} row {b}")
     cost, grad = ctx.rollout_cost_and_grad(torch.from_numpy(wl.theta).cuda(), torch.from_numpy(wl.x0).cuda(),
                                            torch.from_numpy(wl.goals).cuda(), wl.T, seed)
     assert cost == pytest.approx(-ret.sum() / wl.B, rel=1e-6)
     assert torch.isfinite(grad).all()
+    ctx.close()
+
+
+def test_c4_cache_build_matches_oracle_own_build(bagel):
+    """The GPU's one-time LOVE cache at C4's full N = 20,000 (k = 512) against the ORACLE'S OWN build
+    (float64 Cholesky for alpha, naive dense Lanczos with CGS twice for R) for output 0 --
+    the oracle takes minutes here, so one output is compared: the mean weights through k(x*, X) alpha
+    and the LOVE variances s - ||R k||^2 at 64 query points near and away from the data."""
+    wl = W.config("C4", B=8, T=1)
+    ctx = bagel.setup(wl, device=0)
+    m = 0
+    a_g, R_g = [t.cpu().numpy() for t in ctx.cache_get(m)]
+    a_o, _ = O.exact_fit(wl.X, wl.Y[:, m], wl.ell[m], float(wl.s[m]), float(wl.noise[m]), want_L=False)
+    R_o = O.love_build(wl.X, wl.Y[:, m], wl.ell[m], float(wl.s[m]), float(wl.noise[m]), wl.rank, m_index=m)[0]
+    rng = np.random.default_rng(9)
+    xs = np.concatenate([wl.X[rng.integers(0, wl.N, 48)] + rng.normal(0, 0.05, (48, wl.d)),
+                         rng.uniform(-2, 2, (16, wl.d))])
+    kx = O.kernel_matrix(xs, wl.X, wl.ell[m], float(wl.s[m]))
+    assert np.all(np.abs(kx @ a_g - kx @ a_o) <= 1e-8 * np.abs(kx) @ np.abs(a_o))
+    vg = wl.s[m] - np.sum((kx @ R_g.T) ** 2, axis=1)
+    vo = wl.s[m] - np.sum((kx @ R_o.T) ** 2, axis=1)
+    print(f"C4 cache: max |v_gpu - v_oracle| / s = {np.max(np.abs(vg - vo)) / wl.s[m]:.2e}")
+    assert np.max(np.abs(vg - vo)) <= 1e-7 * wl.s[m]
     ctx.close()
