@@ -297,6 +297,14 @@ int bagel_get_gp_kernel(const bagel_ctx* ctx, int* version);
  * (128 + N) K 2 bytes <= 200 KB.  Errors: E_ARG, E_CUDA. */
 int bagel_tc_selftest(bagel_ctx* ctx, const void* A, const void* B, int N, int K, int mode, float* D);
 
+/* CTA-pair probe (tcgen05.mma.cta_group::2): a 2-CTA cluster computes D[256 x N] = A[256 x K] .
+ * B[N x K]^T, A and B [dev] fp16 given as two halves each in the canonical packing above (A rows
+ * 0-127 | 128-255; B rows 0..N/2-1 | N/2..N-1), D [dev] 256 x N fp32 row-major.  mode 0: A from
+ * shared memory; mode 1: A from each CTA's TMEM (A [dev] then also carries the 256 x K rows
+ * row-major after the packed halves).  N in {32, 64, ..., 256}, (128 + N/2) K 2 bytes <= 200 KB.
+ * Synchronous.  Errors: E_ARG, E_CUDA. */
+int bagel_tc_selftest2(bagel_ctx* ctx, const void* A, const void* B, int N, int K, int mode, float* D);
+
 /* Debug copy of an internal per-step buffer into host memory dst [host] (bytes <= its size):
  * 0 pass-1 mean-column partials, 1 pass-1 z partials, 2 pass-2 partials, 3 step means.
  * Layouts are internal (csrc/gp_step_tc.cu).  Errors: E_ARG. */
@@ -309,7 +317,9 @@ int bagel_debug_trace(bagel_ctx* ctx, int enable);
 
 /* Tensor-core issue-rate microbenchmark: `ctas` CTAs (one per SM) each issue `iters`
  * back-to-back tcgen05.mma (M = 128, N, K = 16; mode 0: A from shared memory, 1: A from
- * TMEM) and write the elapsed SM cycles to cycles [dev] (ctas int64).  Errors: E_ARG. */
+ * TMEM) and write the elapsed SM cycles to cycles [dev] (ctas int64).  mode 64: `ctas` CTA
+ * pairs (<= 74), each leader issuing tcgen05.mma.cta_group::2 (M = 256, N, both operands from
+ * shared memory).  Errors: E_ARG. */
 int bagel_tc_bench(bagel_ctx* ctx, int N, int iters, int mode, int ctas, long long* cycles);
 
 #ifdef __cplusplus

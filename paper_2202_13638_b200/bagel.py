@@ -78,6 +78,7 @@ def lib() -> C.CDLL:
             L.bagel_profile_get.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
             L.bagel_tc_selftest.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]
             L.bagel_set_gp_kernel.argtypes = [_vp, C.c_int]
+            L.bagel_tc_selftest2.argtypes = [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp]
             L.bagel_tc_bench.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp]
             L.bagel_debug_buffer.argtypes = [_vp, C.c_int, _vp, C.c_size_t]
             L.bagel_debug_trace.argtypes = [_vp, C.c_int]
@@ -96,7 +97,7 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "policy_configure", "reward_configure", "rollout_cost_and_grad", "bagel_last_launch_count",
            "bagel_gp_predict", "bagel_rollout_trace", "bagel_philox4x32_10", "bagel_philox_normals",
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
-           "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench",
+           "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench", "bagel_tc_selftest2",
            "bagel_debug_buffer", "bagel_debug_trace", "bagel_sample_states", "policy_adam_step",
            "gp_log_marginal_likelihood", "exact_cache_build",
            "gp_target_mode"]
@@ -314,6 +315,12 @@ class Context:
     def tc_selftest(self, A: torch.Tensor, B_packed: torch.Tensor, N: int, K: int, mode: int = 0) -> torch.Tensor:
         D = torch.empty(128, N, dtype=torch.float32, device=self.dev)
         self._check(self.L.bagel_tc_selftest(self.h, _ptr(A), _ptr(B_packed), int(N), int(K), int(mode), _ptr(D)))
+        return D
+
+    def tc_selftest2(self, A_packed: torch.Tensor, B_packed: torch.Tensor, N: int, K: int, mode: int = 0) -> torch.Tensor:
+        D = torch.empty(256, N, dtype=torch.float32, device=self.dev)
+        self._check(self.L.bagel_tc_selftest2(self.h, _ptr(A_packed), _ptr(B_packed), int(N), int(K), int(mode),
+                                              _ptr(D)))
         return D
 
     def tc_bench(self, N: int, iters: int, mode: int = 0, ctas: int = 1) -> np.ndarray:

@@ -21,6 +21,7 @@ size_t ro_reverse_smem(const PolicyDesc& P, int p, int d);
 size_t ro_epilogue_smem(const PolicyDesc& P);
 size_t ro_policy_smem(const PolicyDesc& P);
 int tc_selftest_launch(const void* A, const void* B, int N, int K, float* D, int mode, cudaStream_t st);
+int tc_selftest2_launch(const void* A, const void* B, int N, int K, float* D, int ts, cudaStream_t st);
 int tc_bench_launch(int N, int iters, int mode, int ctas, long long* cycles, cudaStream_t st);
 
 namespace {
@@ -923,6 +924,17 @@ extern "C" int bagel_tc_selftest(bagel_ctx* c, const void* A, const void* B, int
   });
 }
 
+extern "C" int bagel_tc_selftest2(bagel_ctx* c, const void* A, const void* B, int N, int K, int mode, float* D) {
+  return guarded(c, [&] {
+    REQUIRE(A && B && D && N >= 32 && N <= 256 && N % 32 == 0 && K >= 16 && K % 16 == 0 &&
+                (size_t)(128 + N / 2) * K * 2 <= 200 * 1024 && (mode == 0 || (mode == 1 && N + K / 2 <= 512)),
+            BAGEL_E_ARG, "bagel_tc_selftest2: bad shape N=%d K=%d mode=%d", N, K, mode);
+    tc_selftest2_launch(A, B, N, K, D, mode, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 extern "C" int bagel_set_gp_kernel(bagel_ctx* c, int version) {
   return guarded(c, [&] {
     REQUIRE(version == 0 || version == 1, BAGEL_E_ARG, "bagel_set_gp_kernel: version must be 0 or 1 (got %d)", version);
@@ -938,7 +950,8 @@ extern "C" int bagel_get_gp_kernel(const bagel_ctx* c, int* version) {
 
 extern "C" int bagel_tc_bench(bagel_ctx* c, int N, int iters, int mode, int ctas, long long* cycles) {
   return guarded(c, [&] {
-    REQUIRE(cycles && N >= 16 && N <= 256 && N % 16 == 0 && iters >= 1 && ctas >= 1 && mode >= 0 && mode < 32,
+    REQUIRE(cycles && N >= 16 && N <= 256 && N % 16 == 0 && iters >= 1 && ctas >= 1 && mode >= 0 &&
+                (mode < 32 || (mode == 64 && N % 32 == 0 && ctas <= 74)),
             BAGEL_E_ARG, "bagel_tc_bench: bad arguments");
     tc_bench_launch(N, iters, mode, ctas, cycles, c->stream);
     CK(cudaGetLastError());

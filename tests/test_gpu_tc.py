@@ -77,3 +77,22 @@ def test_three_pass_split_reaches_fp32_accuracy(ctx):
     err = np.abs(D - ref) / scale
     print("3-pass max error / sum|a b|:", err.max(), " (2^-24 =", 2.0 ** -24, ")")
     assert err.max() < 64 * 2.0 ** -24
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("N,K", [(256, 64), (128, 32), (64, 128), (128, 256)])
+def test_cta_pair_mma_matches_exact_products(ctx, N, K, mode):
+    """tcgen05.mma.cta_group::2 (M = 256 over a 2-CTA cluster): A rows 0-127 / 128-255 live in the
+    leader's / peer's shared memory (mode 0) or TMEM (mode 1, the TS form), B columns 0..N/2-1 /
+    N/2..N-1 in the leader's / peer's shared memory; D rows land in each CTA's TMEM."""
+    if mode == 1 and N + K // 2 > 512:
+        pytest.skip("TMEM columns")
+    rng = np.random.default_rng(N + K)
+    A = rng.uniform(-1, 1, (256, K)).astype(np.float16)
+    B = rng.uniform(-1, 1, (N, K)).astype(np.float16)
+    a = torch.from_numpy(np.concatenate([pack(A[:128]), pack(A[128:]), A.reshape(-1)]).view(np.int16)).cuda()
+    b = torch.from_numpy(np.concatenate([pack(B[: N // 2]), pack(B[N // 2:])]).view(np.int16)).cuda()
+    D = ctx.tc_selftest2(a, b, N, K, mode).cpu().numpy().astype(np.float64)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64)).T
+    assert np.all(np.abs(D - ref) <= 4 * K * 2.0 ** -24 * scale + 1e-30), np.abs(D - ref).max()
