@@ -319,7 +319,7 @@ int bagel_debug_trace(bagel_ctx* ctx, int enable);
  * back-to-back tcgen05.mma (M = 128, N, K = 16; mode 0: A from shared memory, 1: A from
  * TMEM) and write the elapsed SM cycles to cycles [dev] (ctas int64).  mode 64: `ctas` CTA
  * pairs (<= 74), each leader issuing tcgen05.mma.cta_group::2 (M = 256, N, both operands from
- * shared memory).  Errors: E_ARG. */
+ * shared memory; 65: A from TMEM).  Errors: E_ARG. */
 int bagel_tc_bench(bagel_ctx* ctx, int N, int iters, int mode, int ctas, long long* cycles);
 
 #ifdef __cplusplus

@@ -951,7 +951,7 @@ extern "C" int bagel_get_gp_kernel(const bagel_ctx* c, int* version) {
 extern "C" int bagel_tc_bench(bagel_ctx* c, int N, int iters, int mode, int ctas, long long* cycles) {
   return guarded(c, [&] {
     REQUIRE(cycles && N >= 16 && N <= 256 && N % 16 == 0 && iters >= 1 && ctas >= 1 && mode >= 0 &&
-                (mode < 32 || (mode == 64 && N % 32 == 0 && ctas <= 74)),
+                (mode < 32 || ((mode == 64 || mode == 65) && N % 32 == 0 && ctas <= 74)),
             BAGEL_E_ARG, "bagel_tc_bench: bad arguments");
     tc_bench_launch(N, iters, mode, ctas, cycles, c->stream);
     CK(cudaGetLastError());

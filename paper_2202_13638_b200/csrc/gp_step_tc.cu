@@ -38,7 +38,7 @@ constexpr int A1C = 32;      // TMEM columns of one A stage: hi (KT1 / 2 columns
 constexpr int AUXW = 20;     // floats of per-n side data per stage row
 constexpr int NT2 = 128;     // training points per pass-2 tile (the MMA N dimension)
 constexpr int KS2 = 64;      // j per pass-2 K slab (one pipeline stage)
-constexpr int ST2 = 6;       // pass-2 slab ring stages (Z lives in TMEM)
+constexpr int ST2 = 8;       // pass-2 slab ring stages (Z lives in TMEM; each CTA of a pair holds half a slab)
 constexpr int STX2 = 2;      // pass-2 aux ring stages (one per tile)
 constexpr int STA = 8;       // pass-1 aux (per-n side data) ring stages
 constexpr int P1_MAX_TILES = 80;  // longest pass-1 accumulation chain (N-tiles of KT1 points per split; C3 keeps S1 = 2)
@@ -1088,13 +1088,23 @@ struct P2Args {
 // c * R + w, ... (R = ceil(B / CTAs)) -- the separate epilogue launch disappears.
 template <int D>
 struct P2Shared {
-  uint64_t zready[4], full_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2], tempty[2], mma_done;
+  uint64_t zready[4], full_s[ST2], pfull_s[ST2], empty_s[ST2], full_x[STX2], empty_x[STX2], tfull[2], tempty[2],
+      mma_done;
   float asum[3][128][1 + D];
 };
 
 // Pass 2 of the CTA with grid coordinates (bx, by, bz) (TMEM: 512 columns at `tmem`).  EPI: the
 // control warps stage theta^T in the stage memory once every MMA has completed.  Ends with every
 // thread past a __syncthreads and the barriers retired.
+//
+// CTA pairs (cta_group::2): the two CTAs of a cluster along x (row tiles 2c, 2c + 1) run ONE chain
+// of M = 256 MMAs issued by the leader (rank 0): each CTA holds its 128 rows of Z in its own TMEM
+// (the TS-form A operand) and HALF of every R slab (64 of the tile's 128 training points) in its
+// shared memory; each CTA's accumulator receives its own rows x all 128 points.  A pair MMA of
+// N = 128 issues at the tensor floor (64.1 cycles per 256 x 128 x 16 vs 108.8 for one CTA's
+// 128 x 128 x 16, profiles/r02_b_tc_pair_issue_rate.txt).  Cross-CTA hand-offs: the peer's slab
+// loads are forwarded to the leader's pfull_s, both CTAs' epilogue warps arrive on the leader's
+// zready / tempty (cluster scope), the leader's commits multicast to both CTAs.
 template <int D, bool EPI>
 __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int by, const int bz, uint8_t* sm,
                                         P2Shared<D>& sh, const uint32_t tmem, const bool stage_theta) {
@@ -1102,10 +1112,12 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
   const int KJ = g.KJ;
   const int nsl = KJ / KS2;                            // slabs per tile
   constexpr int NAUX = D + 1;
-  constexpr size_t slab_bytes = (size_t)4 * NT2 * KS2;  // hi + lo of one slab
+  constexpr size_t slab_bytes = (size_t)2 * NT2 * KS2;  // this CTA's half (NT2/2 points) of a slab, hi + lo
+  constexpr size_t half_bytes = (size_t)NT2 * KS2;      // hi (or lo) of NT2/2 points
   constexpr size_t x_bytes = (size_t)NT2 * AUXW * 4;    // aux rows of one tile
   uint64_t* zready = sh.zready;  // per K slab: that slab's Z columns are in TMEM
   uint64_t* full_s = sh.full_s;
+  uint64_t* pfull_s = sh.pfull_s;  // leader: the peer's half of slab s landed
   uint64_t* empty_s = sh.empty_s;
   uint64_t* full_x = sh.full_x;
   uint64_t* empty_x = sh.empty_x;
@@ -1115,7 +1127,9 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
   float (*asum)[128][1 + D] = sh.asum;
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const uint32_t rank = tc::cluster_rank();  // 0: leader (issues the pair MMAs), 1: peer
   const int row0 = bx * 128;
+  const bool rows_valid = row0 < a.B;        // the odd-count padding CTA holds no rows
   const int m = by / g.njt, jt = by % g.njt;
   const int split = bz;
   const int t_begin = split * a.tiles_per_split;
@@ -1129,9 +1143,11 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
 
   if (tid == 0) stamp(a.dbg, 0);
   if (tid == 0) {
-    for (int z = 0; z < 4; ++z) tc::mbar_init(&zready[z], 32 * GEN_WARPS);
+    // zready / tempty: one arrival per epilogue warp of BOTH CTAs (on the leader's barriers)
+    for (int z = 0; z < 4; ++z) tc::mbar_init(&zready[z], 2 * GEN_WARPS);
     for (int s = 0; s < ST2; ++s) {
       tc::mbar_init(&full_s[s], 1);
+      tc::mbar_init(&pfull_s[s], 1);
       tc::mbar_init(&empty_s[s], 1);
     }
     for (int s = 0; s < STX2; ++s) {
@@ -1140,12 +1156,13 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 32 * GEN_WARPS);
+      tc::mbar_init(&tempty[b], 2 * GEN_WARPS);
     }
     tc::mbar_init(&mma_done, 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
+  tc::cluster_sync();  // both CTAs' barriers exist before any remote arrival or multicast commit
   tc::tc_fence_after();
   if (tid == 0) stamp(a.dbg, 7);
   pdl_launch_dependents();
@@ -1161,7 +1178,12 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
           const int s = q % ST2;
           tc::mbar_wait(&empty_s[s], ((uint32_t)(q / ST2) & 1u) ^ 1u);
           tc::mbar_arrive_expect_tx(&full_s[s], (uint32_t)slab_bytes);
-          tc::bulk_g2s(ssm + (size_t)s * slab_bytes, src + (size_t)sl * slab_bytes, (uint32_t)slab_bytes, &full_s[s]);
+          // packed slab = [hi: NT2 points x KS2 | lo: same]; this CTA's NT2/2 points are the
+          // rank-th half of each (canonical layout: row groups outermost)
+          const uint8_t* sp = src + (size_t)sl * 2 * slab_bytes;
+          uint8_t* dst = ssm + (size_t)s * slab_bytes;
+          tc::bulk_g2s(dst, sp + rank * half_bytes, (uint32_t)half_bytes, &full_s[s]);
+          tc::bulk_g2s(dst + half_bytes, sp + 2 * half_bytes + rank * half_bytes, (uint32_t)half_bytes, &full_s[s]);
         }
       }
     }
@@ -1172,44 +1194,61 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
         tc::mbar_wait(&empty_x[x], ((uint32_t)(i / STX2) & 1u) ^ 1u);
         tc::mbar_arrive_expect_tx(&full_x[x], (uint32_t)x_bytes);
         tc::bulk_g2s(xsm + (size_t)x * x_bytes, tiles + (size_t)(t_begin + i) * g.t2_bytes + (size_t)4 * NT2 * KJ,
-                     (uint32_t)x_bytes, &full_x[x]);
+                     (uint32_t)x_bytes, &full_x[x]);  // every point's aux: both CTAs' epilogues see all NT2
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16(128, NT2);
+    if (rank == 0) {
+      // ---- the leader issues the pair's MMAs (M = 256: its rows and the peer's); the whole warp
+      // runs the loop (barrier waits), one elected lane issues each slab's 12 MMAs back to back
+      const uint32_t idesc = tc::idesc_f16(256, NT2);
       constexpr uint32_t SBO = (KS2 / 8) * 128u;
       const uint32_t zhi = tmem + ZC, zlo = tmem + ZC + (uint32_t)(KJ / 2);
-      stamp(a.dbg, 1);
+      if (lane == 0) stamp(a.dbg, 1);
       int q = 0;
       for (int i = 0; i < ntile; ++i) {
         const int b = i & 1;
-        tc::mbar_wait(&tempty[b], ((uint32_t)(i / 2) & 1u) ^ 1u);  // epilogue drained accumulator b
+        tc::mbar_wait(&tempty[b], ((uint32_t)(i / 2) & 1u) ^ 1u);  // both epilogues drained acc b
         tc::tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * NT2);
         for (int sl = 0; sl < nsl; ++sl, ++q) {
           const int s = q % ST2;
-          if (i == 0) tc::mbar_wait(&zready[sl], 0);  // the first tile starts as Z arrives slab by slab
-          tc::mbar_wait(&full_s[s], (uint32_t)(q / ST2) & 1u);
+          const uint32_t ph = (uint32_t)(q / ST2) & 1u;
+          if (i == 0) tc::mbar_wait(&zready[sl], 0);  // both CTAs' Z slab sl is in TMEM
+          tc::mbar_wait(&full_s[s], ph);
+          tc::mbar_wait(&pfull_s[s], ph);
           tc::tc_fence_after();
           const uint32_t sb = tc::smem_u32(ssm + (size_t)s * slab_bytes);
           const uint64_t dbhi = tc::umma_desc(sb, 128, SBO);
-          const uint64_t dblo = tc::umma_desc(sb + (uint32_t)(NT2 * KS2 * 2), 128, SBO);
+          const uint64_t dblo = tc::umma_desc(sb + (uint32_t)half_bytes, 128, SBO);
+          if (tc::elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < KS2 / 16; ++ks) {
-            const uint64_t o = (uint64_t)(ks * 16);
-            const uint32_t ac = (uint32_t)(sl * (KS2 / 2) + ks * 8);
-            tc::mma_f16_ts(d, zhi + ac, dbhi + o, idesc, (sl > 0 || ks > 0) ? 1u : 0u);
-            tc::mma_f16_ts(d, zhi + ac, dblo + o, idesc, 1u);
-            tc::mma_f16_ts(d, zlo + ac, dbhi + o, idesc, 1u);
+            for (int ks = 0; ks < KS2 / 16; ++ks) {
+              const uint64_t o = (uint64_t)(ks * 16);
+              const uint32_t ac = (uint32_t)(sl * (KS2 / 2) + ks * 8);
+              tc::mma_f16_ts2(d, zhi + ac, dbhi + o, idesc, (sl > 0 || ks > 0) ? 1u : 0u);
+              tc::mma_f16_ts2(d, zhi + ac, dblo + o, idesc, 1u);
+              tc::mma_f16_ts2(d, zlo + ac, dbhi + o, idesc, 1u);
+            }
+            tc::umma_commit2_mc(&empty_s[s], 3);
           }
-          tc::umma_commit(&empty_s[s]);
+          __syncwarp();
         }
-        tc::umma_commit(&tfull[b]);
-        if (i == 0) stamp(a.dbg, 2);
+        if (tc::elect_one()) tc::umma_commit2_mc(&tfull[b], 3);
+        __syncwarp();
+        if (i == 0 && lane == 0) stamp(a.dbg, 2);
       }
-      tc::umma_commit(&mma_done);  // single phase: every MMA of this CTA has completed
-      stamp(a.dbg, 3);
+      if (tc::elect_one()) tc::umma_commit2_mc(&mma_done, 3);  // single phase: every MMA of the pair has completed
+      __syncwarp();
+      if (lane == 0) stamp(a.dbg, 3);
+    } else if (lane == 0) {
+      // ---- the peer forwards "my half of slab s landed" to the leader's pfull_s
+      const int nq = ntile * nsl;
+      for (int q = 0; q < nq; ++q) {
+        const int s = q % ST2;
+        tc::mbar_wait(&full_s[s], (uint32_t)(q / ST2) & 1u);
+        tc::mbar_arrive_remote(&pfull_s[s], 0);
+      }
     }
   } else {
     const int quarter = warp % 4, cg = (warp - CTRL_WARPS) / 4;  // lane quarter, 32-column group
@@ -1231,8 +1270,8 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
           for (int h = 0; h < 2; ++h) {
             const int w0 = cg * 8 + (h ? nsl + sl : sl) * 32;
             // L2 loads (not the read-only path): Z is rewritten every step
-            q[sl][h][0] = __ldcg(zrow + (size_t)(w0 / 4) * 128);
-            q[sl][h][1] = __ldcg(zrow + (size_t)(w0 / 4 + 1) * 128);
+            q[sl][h][0] = rows_valid ? __ldcg(zrow + (size_t)(w0 / 4) * 128) : make_uint4(0u, 0u, 0u, 0u);
+            q[sl][h][1] = rows_valid ? __ldcg(zrow + (size_t)(w0 / 4 + 1) * 128) : make_uint4(0u, 0u, 0u, 0u);
           }
         }
       }
@@ -1249,7 +1288,8 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
           }
           tc::tmem_st_wait();
           tc::tc_fence_before();
-          tc::mbar_arrive(&zready[sl]);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote(&zready[sl], 0);  // the leader's barrier (both CTAs)
         }
       }
       if (tid == 32 * CTRL_WARPS) stamp(a.dbg, 6);
@@ -1278,7 +1318,8 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
       tmem_ld8(ta + 24, w + 24);
       tc::tmem_ld_wait();
       tc::tc_fence_before();
-      tc::mbar_arrive(&tempty[b]);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_remote(&tempty[b], 0);  // the leader's barrier (both CTAs)
       tc::mbar_wait(&full_x[x], (uint32_t)(i / STX2) & 1u);
       const float* aux = reinterpret_cast<const float*>(xsm + (size_t)x * x_bytes);
 #pragma unroll
@@ -1327,11 +1368,13 @@ __device__ __forceinline__ void p2_main(const P2Args& a, const int bx, const int
   }
   tc::tc_fence_before();
   __syncthreads();
+  tc::cluster_sync();  // no remote arrival or multicast commit still targets either CTA's barriers
   if (tid == 0) {
     stamp(a.dbg, 5);
     for (int z = 0; z < 4; ++z) tc::mbar_inval(&zready[z]);
     for (int s = 0; s < ST2; ++s) {
       tc::mbar_inval(&full_s[s]);
+      tc::mbar_inval(&pfull_s[s]);
       tc::mbar_inval(&empty_s[s]);
     }
     for (int s = 0; s < STX2; ++s) {
@@ -1371,12 +1414,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_p2_tc(P2Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ P2Shared<D> sh;
   __shared__ uint32_t tmem_base;
-  if (threadIdx.x / 32 == 1) tc::tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x / 32 == 1) tc::tmem_alloc2(&tmem_base, 512);  // the pair's TMEM, same address in both
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   p2_main<D, EPI>(a, blockIdx.x, blockIdx.y, blockIdx.z, sm, sh, tmem_base, a.e.t + 1 < a.e.T);
-  if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, 512);
+  if (threadIdx.x / 32 == 1) tc::tmem_dealloc2(tmem_base, 512);
   if (EPI) {
     // arrive, then the pass-1-only half of this CTA's rows while the other CTAs finish pass 2
     const unsigned long long target = grid_arrive(a.gbar);
@@ -1418,7 +1461,7 @@ size_t p1_smem(const Geo& g) {
 }
 size_t p2_smem(const Geo& g) {
   (void)g;
-  return (size_t)ST2 * 4 * NT2 * KS2 + (size_t)STX2 * NT2 * AUXW * 4;
+  return (size_t)ST2 * 2 * NT2 * KS2 + (size_t)STX2 * NT2 * AUXW * 4;  // half slabs (CTA pairs)
 }
 
 }  // namespace
@@ -1491,6 +1534,7 @@ size_t tc_zp_bytes(const bagel_ctx* c, int B) {
   return (size_t)g.p * cdiv(B, 128) * g.njt * 128 * g.KJ * 2 * 2;
 }
 int tc_njt(const bagel_ctx* c) { return geo_of(c).njt; }
+int tc_pair_row_tiles(int B) { return (cdiv(B, 128) + 1) / 2 * 2; }
 size_t tc_zpart_count(const bagel_ctx* c, int B) { return (size_t)c->p * cdiv(c->k, R1_JG) * B; }
 size_t tc_gbar_count() { return (size_t)GB_STRIDE; }
 
@@ -1643,7 +1687,7 @@ int tc_reduce1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, fl
 // per-warp buffers fit the stage memory)?
 bool tc_pass2_epi_ok(const bagel_ctx* c, int B) {
   const Geo g = geo_of(c);
-  const long long ctas = (long long)cdiv(B, 128) * c->p * g.njt * c->ws.S2tc;
+  const long long ctas = (long long)tc_pair_row_tiles(B) * c->p * g.njt * c->ws.S2tc;
   const size_t need = sizeof(float) * (((size_t)c->pol.n_params + 3) / 4 * 4 +
                                        (size_t)(THREADS / 32) * (2 * BAGEL_MAX_WIDTH + rows::epi_scratch_floats<8, 1>()));
   const char* env = getenv("BAGEL_P2_EPI");
@@ -1669,14 +1713,19 @@ int tc_pass2(const bagel_ctx* c, const float* xstar, int B, const EpiArgs* epi, 
   a.dbg = T.dbg2;
   for (int m = 0; m < c->p; ++m)
     for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
-  dim3 grid(cdiv(B, 128), c->p * g.njt, c->ws.S2tc);
+  dim3 grid(tc_pair_row_tiles(B), c->p * g.njt, c->ws.S2tc);  // CTA pairs along the row tiles
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS, 1, 1);
   cfg.dynamicSmemBytes = p2_smem(g);
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int na = 0;
+  at[na].id = cudaLaunchAttributeClusterDimension;
+  at[na].val.clusterDim.x = 2;
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
   if (tc_pdl_enabled()) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;

@@ -187,6 +187,21 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync): issuing a run of tcgen05.mma from inside a single
+// elected branch lets the compiler emit them back to back, instead of wrapping every MMA of a
+// lane-0-only branch in its own elect loop (measured: that wrapping, plus issue slots shared with
+// the epilogue warps of the same SM sub-partition, held the pair MMAs of pass 2 at ~105 cycles
+// instead of the 64-cycle floor).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- CTA pairs (cta_group::2)
 // Two CTAs of a cluster (ranks 0 and 1, one TPC) execute one M = 256 MMA together: A's rows
 // 0-127 come from the leader's (rank 0) shared memory and 128-255 from the peer's, at the same
@@ -235,6 +250,18 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
       "{\n\t.reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
       "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+// Arrive on the mbarrier at `bar`'s offset in CTA `rank` with the default (.release.cta)
+// semantics -- the CTA-pair hand-offs of tensor-memory and async-proxy state (the arriving thread
+// has already waited for its tcgen05.ld / tcgen05.st / bulk copy), without the GPU-scope membar
+// that .release.cluster costs (measured: 17% of pass 2's stall samples).
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
       "r"(rank)
       : "memory");
 }

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(128) k_tc_bench(int N, int iters, int mode, lo
 // CTA pairs: every 2-CTA cluster's leader issues `iters` back-to-back tcgen05.mma.cta_group::2
 // (M = 256, N, K = 16, A and B from shared memory) into one accumulator.
 namespace {
-__global__ void __launch_bounds__(128) k_tc_bench2(int N, int iters, long long* cycles) {
+__global__ void __launch_bounds__(128) k_tc_bench2(int N, int iters, int ts, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -287,7 +287,10 @@ __global__ void __launch_bounds__(128) k_tc_bench2(int N, int iters, long long* 
     const uint64_t ad = tc::umma_desc(tc::smem_u32(sm), 128, 256);
     const uint64_t bd = tc::umma_desc(tc::smem_u32(sm) + 128 * 16 * 2, 128, 256);
     const long long c0 = clock64();
-    for (int i = 0; i < iters; ++i) tc::mma_f16_2(t, ad, bd, idesc, i > 0 ? 1u : 0u);
+    if (ts)
+      for (int i = 0; i < iters; ++i) tc::mma_f16_ts2(t, t + 256u, bd, idesc, i > 0 ? 1u : 0u);
+    else
+      for (int i = 0; i < iters; ++i) tc::mma_f16_2(t, ad, bd, idesc, i > 0 ? 1u : 0u);
     tc::umma_commit2_mc(&bar, 3);
     tc::mbar_wait(&bar, 0);
     cycles[blockIdx.x / 2] = clock64() - c0;
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(128) k_tc_bench2(int N, int iters, long long* 
 
 int tc_bench_launch(int N, int iters, int mode, int ctas, long long* cycles, cudaStream_t st) {
   const size_t smem = 200 * 1024;  // one CTA per SM
-  if (mode & 64) {  // CTA pairs: `ctas` clusters of 2
+  if (mode & 64) {  // CTA pairs: `ctas` clusters of 2 (mode 65: A from TMEM)
     bagel_set_smem_attr(k_tc_bench2, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * ctas, 1, 1);
@@ -317,7 +320,7 @@ int tc_bench_launch(int N, int iters, int mode, int ctas, long long* cycles, cud
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    (void)cudaLaunchKernelEx(&cfg, k_tc_bench2, N, iters, cycles);
+    (void)cudaLaunchKernelEx(&cfg, k_tc_bench2, N, iters, mode & 1, cycles);
     return 1;
   }
   bagel_set_smem_attr(k_tc_bench, smem);
