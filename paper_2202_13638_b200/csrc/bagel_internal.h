@@ -294,6 +294,7 @@ int mll_launch(const float* X, const float* Y, int ystride, int N, int d, const 
 size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1);
 size_t tc_zp_bytes(const bagel_ctx* c, int B);
 int tc_njt(const bagel_ctx* c);
+int tc_pair_row_tiles(int B);  // row tiles rounded up to whole CTA pairs
 size_t tc_zpart_count(const bagel_ctx* c, int B);
 size_t tc_gbar_count();
 int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st);

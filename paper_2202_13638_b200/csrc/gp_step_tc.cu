@@ -33,8 +33,8 @@
 namespace tcg {
 
 constexpr int KT1 = 32;      // training points per pass-1 stage
-constexpr int ST1 = 6;       // pass-1 ring stages: A (ktilde, in TMEM) and B (R tile, shared memory)
-constexpr int A1C = 32;      // TMEM columns of one A stage: hi (KT1 / 2 columns) | lo
+constexpr int ST1 = 6;       // pass-1 ring stages (max): A (ktilde) and B (R tile halves), shared memory
+
 constexpr int AUXW = 20;     // floats of per-n side data per stage row
 constexpr int NT2 = 128;     // training points per pass-2 tile (the MMA N dimension)
 constexpr int KS2 = 64;      // j per pass-2 K slab (one pipeline stage)
@@ -49,6 +49,8 @@ constexpr int P2_LD = 1 + BAGEL_MAX_D;
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 __host__ __device__ inline int cdiv_dev(int a, int b) { return (a + b - 1) / b; }
+// pass-1 ring depth for NC z-column tiles per CTA pair (stage = A 16 KB + NC x 16 KB of B halves)
+__host__ __device__ constexpr int p1_stages(int NC) { return NC > 1 ? 4 : 6; }
 
 struct Geo {
   int N, d, p, k;
@@ -66,7 +68,7 @@ inline Geo make_geo(int N, int d, int p, int k) {
   Geo g{};
   g.N = N; g.d = d; g.p = p; g.k = k;
   g.nct = cdiv(k, 256);
-  g.NZ = cdiv(cdiv(k, g.nct), 16) * 16;
+  g.NZ = cdiv(cdiv(k, g.nct), 32) * 32;  // CTA pairs: each CTA holds NZ/2 columns of B
   g.njt = cdiv(k, 256);
   g.KJ = cdiv(cdiv(k, g.njt), KS2) * KS2;
   g.nt1 = cdiv(N, KT1);
@@ -395,56 +397,62 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 // measured first: cluster residency caps S1 at 6 here and DSMEM moves ~20 B/clk/SM -- slower.)
 template <int D>
 struct P1Shared {
-  uint64_t full_a[ST1], empty_a[ST1], full_b[ST1], empty_b[ST1], full_x[STA], empty_x[STA], done;
+  uint64_t full_a[ST1], full_b[ST1], pfull_b[ST1], empty[ST1], full_x[STA], empty_x[STA], done;
   float hsum[3][128][1 + D];
 };
 
-// Pass 1 of the CTA with grid coordinates (bx, by, bz): the N-split partial z tile of 128 rows
-// (TMEM accumulator at column `tmem`) and the mean columns.  FUSED: the partial tile is parked
-// in shared memory and the rows this CTA does not finish are written to P1z (p1_reduce runs
-// after a grid barrier).  Ends with every thread past a __syncthreads and the barriers retired.
+// Pass 1 of the CTA with grid coordinates (bx, by, bz) on CTA pairs (cta_group::2): the two CTAs
+// of a cluster along x (row tiles 2c, 2c + 1) share (output m, column-tile pair ctp, split) and run
+// ONE chain of M = 256 MMAs issued by the leader (rank 0), SS form.  Each CTA's generator warps
+// write the ktilde hi/lo A operand of ITS 128 rows to its own shared memory (canonical K-major,
+// st.shared + proxy fence); each CTA holds HALF of the z columns of every R tile (B); the pair
+// computes NC = min(2, nct - 2 ctp) column tiles of NZ columns at once (accumulators NC x NZ TMEM
+// columns in each CTA), so at k = 512 (C4, C5) every ktilde is generated once per row instead of
+// once per column tile, and the MMA runs at the pair floor (profiles/r02_b_tc_pair_issue_rate.txt).
+// FUSED: the partial z tile is parked in shared memory and the rows this CTA does not finish are
+// written to P1z (p1_reduce runs after a grid barrier).  Ends with every thread past a
+// __syncthreads and the barriers retired.
 template <int D, bool FUSED>
 __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int by, const int bz, const int nbz,
                                         uint8_t* sm, P1Shared<D>& sh, const uint32_t tmem) {
   const Geo& g = a.g;
   const int NZ = g.NZ;
   constexpr int NAUX = D + 1;  // X_n (d) | s alpha_n
-  const size_t b_bytes = (size_t)4 * NZ * KT1;   // B hi + lo of one tile
-  const size_t x_bytes = (size_t)KT1 * AUXW * 4; // aux rows of one tile
-  uint8_t* bsm = sm;                             // ST1 x (B hi | B lo)
-  uint8_t* xsm = bsm + ST1 * b_bytes;            // STA x aux
-  // TMEM: the z accumulator in columns [0, NZ), then ST1 A stages of A1C columns
-  const uint32_t acol0 = (uint32_t)((NZ + 31) / 32 * 32);
+  const int nctp = cdiv_dev(g.nct, 2);
+  const int m = by / nctp, ctp = by % nctp, ct0 = 2 * ctp;
+  const int NC = min(2, g.nct - ct0);
+  const int nst = p1_stages(NC);
+  const size_t a_bytes = (size_t)128 * KT1 * 2 * 2;      // A hi | lo of this CTA's 128 rows
+  const size_t bh_bytes = (size_t)(NZ / 2) * KT1 * 2;    // B hi (or lo) of this CTA's NZ/2 columns
+  const size_t st_bytes = a_bytes + (size_t)NC * 2 * bh_bytes;
+  const size_t x_bytes = (size_t)KT1 * AUXW * 4;         // aux rows of one tile
+  uint8_t* ssm = sm;                                     // nst x (A hi | A lo | [B hi | B lo] x NC)
+  uint8_t* xsm = ssm + (size_t)nst * st_bytes;           // STA x aux
   uint64_t* full_a = sh.full_a;
-  uint64_t* empty_a = sh.empty_a;
   uint64_t* full_b = sh.full_b;
-  uint64_t* empty_b = sh.empty_b;
+  uint64_t* pfull_b = sh.pfull_b;
+  uint64_t* empty = sh.empty;
   uint64_t* full_x = sh.full_x;
   uint64_t* empty_x = sh.empty_x;
   uint64_t& done = sh.done;
   float (*hsum)[128][1 + D] = sh.hsum;
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const uint32_t rank = tc::cluster_rank();  // 0: leader (issues the pair MMAs), 1: peer
   const int row0 = bx * 128;
-  const int m = by / g.nct, ct = by % g.nct;
   const int split = bz;
   const int t_begin = split * a.tiles_per_split;
   const int t_end = min(g.nt1, t_begin + a.tiles_per_split);
   const int ntile = max(0, t_end - t_begin);
-  const uint8_t* tiles = a.tiles + (size_t)m * a.m_stride + ((size_t)ct * g.nt1) * g.t1_bytes;
+  const uint8_t* mtiles = a.tiles + (size_t)m * a.m_stride;  // [ct][t] tiles of output m
 
-  // clusters of csize CTAs along the row tiles share (m, split) and hence every B tile: each CTA
-  // loads 1/csize of a tile multicast to all, and a stage is refilled once every CTA's MMAs
-  // released it (empty_b counts csize arrivals)
-  const uint32_t csize = tc::cluster_size(), crank = tc::cluster_rank();
-  const uint16_t cmask = (uint16_t)((1u << csize) - 1u);
   if (tid == 0) stamp(a.dbg, 0);
   if (tid == 0) {
     for (int s = 0; s < ST1; ++s) {
-      tc::mbar_init(&full_a[s], 32 * GEN_WARPS);
-      tc::mbar_init(&empty_a[s], 1);
+      tc::mbar_init(&full_a[s], 2 * GEN_WARPS);  // the leader's: every generator warp of both CTAs
       tc::mbar_init(&full_b[s], 1);
-      tc::mbar_init(&empty_b[s], csize);
+      tc::mbar_init(&pfull_b[s], 1);
+      tc::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < STA; ++s) {
       tc::mbar_init(&full_x[s], 1);
@@ -454,7 +462,7 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     tc::fence_mbar_init();
   }
   __syncthreads();
-  if (csize > 1) tc::cluster_sync();  // the partners' barriers exist before any multicast lands
+  tc::cluster_sync();  // both CTAs' barriers exist before any remote arrival or multicast commit
   tc::tc_fence_after();
   pdl_launch_dependents();
   // the operand tiles are static (cache build): the producers start now; everything that reads
@@ -462,72 +470,90 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
   if (warp >= CTRL_WARPS) pdl_wait();
 
   if (warp == 0) {
-    // ------------------------------------------------ B-tile producer (one elected lane)
+    // ------------------------------------------------ B producer: this CTA's half of each column tile
     if (lane == 0) {
-      const uint32_t slice = (uint32_t)b_bytes / csize;
       for (int i = 0; i < ntile; ++i) {
-        const int s = i % ST1;
-        tc::mbar_wait(&empty_b[s], ((uint32_t)(i / ST1) & 1u) ^ 1u);
-        tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)b_bytes);
-        const uint8_t* src = tiles + (size_t)(t_begin + i) * g.t1_bytes;
-        if (csize == 1)
-          tc::bulk_g2s(bsm + (size_t)s * b_bytes, src, (uint32_t)b_bytes, &full_b[s]);
-        else
-          tc::bulk_g2s_mc(bsm + (size_t)s * b_bytes + crank * slice, src + crank * slice, slice, &full_b[s], cmask);
+        const int s = i % nst;
+        tc::mbar_wait(&empty[s], ((uint32_t)(i / nst) & 1u) ^ 1u);
+        tc::mbar_arrive_expect_tx(&full_b[s], (uint32_t)(NC * 2 * bh_bytes));
+        uint8_t* dst = ssm + (size_t)s * st_bytes + a_bytes;
+        for (int c = 0; c < NC; ++c) {
+          // packed tile = [B hi: NZ x KT1 | B lo | aux]; this CTA's NZ/2 columns are the rank-th half
+          const uint8_t* src = mtiles + ((size_t)(ct0 + c) * g.nt1 + t_begin + i) * g.t1_bytes;
+          tc::bulk_g2s(dst + (size_t)c * 2 * bh_bytes, src + rank * bh_bytes, (uint32_t)bh_bytes, &full_b[s]);
+          tc::bulk_g2s(dst + (size_t)c * 2 * bh_bytes + bh_bytes, src + 2 * bh_bytes + rank * bh_bytes,
+                       (uint32_t)bh_bytes, &full_b[s]);
+        }
       }
     }
   } else if (warp == 2) {
     // ------------------------------------------------ aux producer (runs up to STA tiles ahead)
     if (lane == 0) {
+      const uint8_t* t0 = mtiles + ((size_t)ct0 * g.nt1 + t_begin) * g.t1_bytes + (size_t)4 * NZ * KT1;
       for (int i = 0; i < ntile; ++i) {
         const int x = i % STA;
         tc::mbar_wait(&empty_x[x], ((uint32_t)(i / STA) & 1u) ^ 1u);
         tc::mbar_arrive_expect_tx(&full_x[x], (uint32_t)x_bytes);
-        tc::bulk_g2s(xsm + (size_t)x * x_bytes, tiles + (size_t)(t_begin + i) * g.t1_bytes + b_bytes,
-                     (uint32_t)x_bytes, &full_x[x]);
+        tc::bulk_g2s(xsm + (size_t)x * x_bytes, t0 + (size_t)i * g.t1_bytes, (uint32_t)x_bytes, &full_x[x]);
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_f16(128, NZ);
+    if (rank == 0) {
+      // ------------------------------------------------ MMA issuer (the leader): the warp waits,
+      // one elected lane issues each tile's 6 NC MMAs back to back
+      const uint32_t idesc = tc::idesc_f16(256, NZ);
       constexpr uint32_t SBO = (KT1 / 8) * 128;
       for (int i = 0; i < ntile; ++i) {
-        const int s = i % ST1;
-        const uint32_t ph = (uint32_t)(i / ST1) & 1u;
+        const int s = i % nst;
+        const uint32_t ph = (uint32_t)(i / nst) & 1u;
         tc::mbar_wait(&full_b[s], ph);
+        tc::mbar_wait(&pfull_b[s], ph);
         tc::mbar_wait(&full_a[s], ph);
         tc::tc_fence_after();
-        const uint32_t bbase = tc::smem_u32(bsm + (size_t)s * b_bytes);
-        const uint32_t ahi = tmem + acol0 + (uint32_t)(s * A1C), alo = ahi + (uint32_t)(KT1 / 2);
-        const uint64_t dbhi = tc::umma_desc(bbase, 128, SBO);
-        const uint64_t dblo = tc::umma_desc(bbase + (uint32_t)NZ * KT1 * 2u, 128, SBO);
-        if (!(a.diag & 2)) {
+        const uint32_t sbase = tc::smem_u32(ssm + (size_t)s * st_bytes);
+        const uint64_t dahi = tc::umma_desc(sbase, 128, SBO);
+        const uint64_t dalo = tc::umma_desc(sbase + (uint32_t)(a_bytes / 2), 128, SBO);
+        if (tc::elect_one()) {
+          if (!(a.diag & 2)) {
 #pragma unroll
-          for (int ks = 0; ks < KT1 / 16; ++ks) {
-            const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
-            const uint32_t ac = (uint32_t)(ks * 8);  // 16 K elements = 8 TMEM columns
-            const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
-            tc::mma_f16_ts(tmem, ahi + ac, dbhi + o, idesc, acc0);
-            tc::mma_f16_ts(tmem, ahi + ac, dblo + o, idesc, 1u);
-            tc::mma_f16_ts(tmem, alo + ac, dbhi + o, idesc, 1u);
+            for (int ks = 0; ks < KT1 / 16; ++ks) {
+              const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
+              const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
+              for (int c = 0; c < NC; ++c) {
+                const uint32_t bb = sbase + (uint32_t)(a_bytes + (size_t)c * 2 * bh_bytes);
+                const uint64_t dbhi = tc::umma_desc(bb, 128, SBO), dblo = tc::umma_desc(bb + (uint32_t)bh_bytes, 128, SBO);
+                const uint32_t d = tmem + (uint32_t)(c * NZ);
+                tc::mma_f16_2(d, dahi + o, dbhi + o, idesc, acc0);
+                tc::mma_f16_2(d, dahi + o, dblo + o, idesc, 1u);
+                tc::mma_f16_2(d, dalo + o, dbhi + o, idesc, 1u);
+              }
+            }
           }
+          tc::umma_commit2_mc(&empty[s], 3);
         }
-        tc::umma_commit(&empty_a[s]);
-        if (csize == 1) tc::umma_commit(&empty_b[s]);
-        else tc::umma_commit_mc(&empty_b[s], cmask);
-        if (i == 0) stamp(a.dbg, 1);
+        __syncwarp();
+        if (i == 0 && lane == 0) stamp(a.dbg, 1);
       }
-      tc::umma_commit(&done);
-      stamp(a.dbg, 2);
+      if (tc::elect_one()) tc::umma_commit2_mc(&done, 3);
+      __syncwarp();
+      if (lane == 0) stamp(a.dbg, 2);
+    } else if (lane == 0) {
+      // ------------------------------------------------ the peer forwards "my B half of stage s landed"
+      for (int i = 0; i < ntile; ++i) {
+        const int s = i % nst;
+        tc::mbar_wait(&full_b[s], (uint32_t)(i / nst) & 1u);
+        tc::mbar_arrive_remote(&pfull_b[s], 0);
+      }
     }
   } else {
     // ------------------------------------------------ ktilde generators (4 threads per row, 8 n each)
-    // warp w writes TMEM lane quarter w % 4, so row r = 32 (w % 4) + lane; qd = which 8 of the 32
+    // warp w serves TMEM lane quarter w % 4 (row r = 32 (w % 4) + lane); qd = which 8 of the 32
+    // points; the A tile is written to shared memory as the canonical K-major SS operand
     const int gt = tid - 32 * CTRL_WARPS;  // 0..511
     const int r = (warp % 4) * 32 + lane, qd = (warp - CTRL_WARPS) / 4;
     const int row = row0 + r;
-    const uint32_t tlane = (uint32_t)((warp % 4) * 32) << 16;
+    // element (r, 8 qd .. 8 qd + 7) of the canonical layout: one 16-byte chunk
+    const uint32_t aoff = (uint32_t)((((r >> 3) * (KT1 / 8) + qd) << 6) + ((r & 7) << 3)) * 2u;
     // exponent as (x*_c - X_nc) * kappa / l_c: difference first, then scale (4x smaller fp32
     // error in ktilde than scaling first, scripts/fp32_floor.py)
     float xq[D], sc[D];
@@ -540,14 +566,14 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     float2 hacc2[1 + D];
 #pragma unroll
     for (int c = 0; c <= D; ++c) hacc2[c] = make_float2(0.0f, 0.0f);
-    // the mean columns belong to the z-column tile ct = 0 only; the other column tiles' CTAs skip
-    // that arithmetic (a third of the generator's FP32 work; C4 / C5 have two column tiles)
+    // the mean columns belong to the column-tile pair ctp = 0 only (C4 / C5 run a single pair: k =
+    // 512 is two column tiles)
     auto gen_tiles = [&](auto mean_tag) {
     constexpr bool MEAN = decltype(mean_tag)::value;
     for (int i = 0; i < ntile; ++i) {
-      const int s = i % ST1, x = i % STA;
-      tc::mbar_wait(&full_x[x], (uint32_t)(i / STA) & 1u);             // aux rows of tile i landed
-      tc::mbar_wait(&empty_a[s], ((uint32_t)(i / ST1) & 1u) ^ 1u);     // MMA done reading A[s]
+      const int s = i % nst, x = i % STA;
+      tc::mbar_wait(&full_x[x], (uint32_t)(i / STA) & 1u);               // aux rows of tile i landed
+      tc::mbar_wait(&empty[s], ((uint32_t)(i / nst) & 1u) ^ 1u);        // the pair's MMAs released stage s
       const float* aux = reinterpret_cast<const float*>(xsm + (size_t)x * x_bytes);
       uint32_t hw[4], lw[4];
       if (!(a.diag & 1))
@@ -581,21 +607,21 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
       }
-      // A tile (row r, K pairs 4 qd .. 4 qd + 3) -> TMEM stage s, hi then lo
-      tc::tc_fence_after();
-      const uint32_t ta = tmem + tlane + acol0 + (uint32_t)(s * A1C + qd * 4);
-      tc::tmem_st4(ta, hw);
-      tc::tmem_st4(ta + (uint32_t)(KT1 / 2), lw);
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
+      // A tile (row r, K 8 qd .. 8 qd + 7) -> stage s, hi then lo; then make the generic-proxy
+      // writes visible to the tensor core (async proxy) before the leader may issue on them
+      uint8_t* abase = ssm + (size_t)s * st_bytes;
+      *reinterpret_cast<uint4*>(abase + aoff) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(abase + a_bytes / 2 + aoff) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      tc::fence_proxy_async();
       // MEMBAR.CTA: every aux load above has returned before the aux stage is released
       // (SYNCS.ARRIVE does not wait for pending LDS)
       if (!(a.diag & 4)) __threadfence_block();
-      tc::mbar_arrive(&full_a[s]);
       tc::mbar_arrive(&empty_x[x]);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_remote(&full_a[s], 0);  // the leader's barrier (both CTAs)
     }
     };
-    if (ct == 0) gen_tiles(std::true_type{});
+    if (ctp == 0) gen_tiles(std::true_type{});
     else gen_tiles(std::false_type{});
     if (gt == 0) stamp(a.dbg, 3);
     float hacc[1 + D];
@@ -605,7 +631,7 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     if (qd > 0)
       for (int c = 0; c <= D; ++c) hsum[qd - 1][r][c] = hacc[c];
     asm volatile("bar.sync 1, %0;" ::"n"(32 * GEN_WARPS) : "memory");
-    if (qd == 0 && row < a.B && ct == 0) {
+    if (qd == 0 && row < a.B && ctp == 0) {
       float* o = a.P1h + ((size_t)(split * a.m_count + m) * a.B + row) * (1 + D);
       for (int c = 0; c <= D; ++c) o[c] = ((hacc[c] + hsum[0][r][c]) + hsum[1][r][c]) + hsum[2][r][c];
     }
@@ -620,7 +646,8 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     const int c_begin = cg * gw, c_end = min(NZ, c_begin + gw);
     if (gt == 0) stamp(a.dbg, 4);
     if (FUSED) {
-      // partial z tile -> own stage memory [128][NZ + 4] (padded rows: conflict-free v4 stores)
+      // partial z tile (nct == 1: NC == 1) -> stage memory [128][NZ + 4] (padded rows: conflict-free
+      // v4 stores); the pair's MMAs are complete, so no operand in this memory is still read
       float* zs = reinterpret_cast<float*>(sm) + (size_t)wrow * (NZ + 4);
       for (int c0 = c_begin; c0 < c_end; c0 += 8) {
         float v[8];
@@ -633,15 +660,17 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         *reinterpret_cast<float4*>(zs + c0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
       }
     } else {
-      float* zout = a.P1z + ((size_t)((split * a.m_count + m) * g.nct + ct) * NZ) * a.B;
       const int grow = row0 + wrow;
-      for (int c0 = c_begin; c0 < c_end; c0 += 8) {
-        float v[8];
-        tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
-        tc::tmem_ld_wait();
-        if (grow < a.B) {
+      for (int c = 0; c < NC; ++c) {
+        float* zout = a.P1z + ((size_t)((split * a.m_count + m) * g.nct + ct0 + c) * NZ) * a.B;
+        for (int c0 = c_begin; c0 < c_end; c0 += 8) {
+          float v[8];
+          tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(c * NZ + c0), v);
+          tc::tmem_ld_wait();
+          if (grow < a.B) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) zout[(size_t)(c0 + u) * a.B + grow] = ntile > 0 ? v[u] : 0.0f;
+            for (int u = 0; u < 8; ++u) zout[(size_t)(c0 + u) * a.B + grow] = ntile > 0 ? v[u] : 0.0f;
+          }
         }
       }
     }
@@ -649,13 +678,14 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
   if (warp < CTRL_WARPS) pdl_wait();
   tc::tc_fence_before();
   __syncthreads();
+  tc::cluster_sync();  // no remote arrival or multicast commit still targets either CTA's barriers
   if (tid == 0) {
     stamp(a.dbg, 5);
     for (int s = 0; s < ST1; ++s) {
       tc::mbar_inval(&full_a[s]);
-      tc::mbar_inval(&empty_a[s]);
       tc::mbar_inval(&full_b[s]);
-      tc::mbar_inval(&empty_b[s]);
+      tc::mbar_inval(&pfull_b[s]);
+      tc::mbar_inval(&empty[s]);
     }
     for (int s = 0; s < STA; ++s) {
       tc::mbar_inval(&full_x[s]);
@@ -663,7 +693,6 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     }
     tc::mbar_inval(&done);
   }
-  if (csize > 1) tc::cluster_sync();  // no CTA leaves while multicasts / remote arrivals may target it
   if (FUSED) {
     const int LDZ = NZ + 4;
     const int rtn = cdiv_dev(a.B, 128);
@@ -803,14 +832,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ P1Shared<D> sh;
   __shared__ uint32_t tmem_base;
+  const int nctp = cdiv_dev(a.g.nct, 2);
+  const int NC = min(2, a.g.nct - 2 * ((int)blockIdx.y % nctp));
   uint32_t ncols = 32;
-  while ((int)ncols < (a.g.NZ + 31) / 32 * 32 + ST1 * A1C) ncols <<= 1;
-  if (threadIdx.x / 32 == 1) tc::tmem_alloc(&tmem_base, ncols);
+  while ((int)ncols < NC * a.g.NZ) ncols <<= 1;
+  if (threadIdx.x / 32 == 1) tc::tmem_alloc2(&tmem_base, ncols);  // the pair's accumulators
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   p1_main<D, FUSED>(a, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, sm, sh, tmem_base);
-  if (threadIdx.x / 32 == 1) tc::tmem_dealloc(tmem_base, ncols);
+  if (threadIdx.x / 32 == 1) tc::tmem_dealloc2(tmem_base, ncols);
   if (FUSED) {
     grid_barrier(a.gbar, a.err_flag);
     if (threadIdx.x == 0) stamp(a.dbg, 6);
@@ -1455,8 +1486,11 @@ namespace {
 Geo geo_of(const bagel_ctx* c) { return make_geo(c->N, c->d, c->p, c->k); }
 
 size_t p1_smem(const Geo& g) {
-  // B ring + aux ring; the FUSED tail parks a [128][NZ + 4] fp32 partial tile in the same memory
-  const size_t ring = (size_t)ST1 * ((size_t)4 * g.NZ * KT1) + (size_t)STA * KT1 * AUXW * 4;
+  // stage ring (A | NC B halves) + aux ring; the FUSED tail parks a [128][NZ + 4] fp32 partial tile
+  // in the same memory
+  const int NC = g.nct > 1 ? 2 : 1;
+  const size_t st = (size_t)128 * KT1 * 4 + (size_t)NC * g.NZ * KT1 * 2;
+  const size_t ring = (size_t)p1_stages(NC) * st + (size_t)STA * KT1 * AUXW * 4;
   return std::max(ring, (size_t)128 * (g.NZ + 4) * 4);
 }
 size_t p2_smem(const Geo& g) {
@@ -1509,13 +1543,12 @@ int tc_pack(bagel_ctx* c, int m, cudaStream_t st) {
 constexpr int SPLIT_TARGET = 9;
 void tc_choose_splits(const bagel_ctx* c, int B, int* S1, int* S2, int* tps1, int* tps2, int* p1_fused) {
   const Geo g = geo_of(c);
-  const int rt = cdiv(B, 128);
   int max_tiles = P1_MAX_TILES;
   if (const char* e = getenv("BAGEL_P1_MAX_TILES")) max_tiles = std::max(1, atoi(e));  // diagnostics only
   *tps1 = std::min(max_tiles, std::max(1, cdiv(g.nt1, SPLIT_TARGET)));
   *S1 = cdiv(g.nt1, *tps1);
   const char* env = getenv("BAGEL_P1_FUSED");
-  *p1_fused = g.nct == 1 && rt * g.p * *S1 <= c->num_sms && !(env && env[0] == '0');
+  *p1_fused = g.nct == 1 && tc_pair_row_tiles(B) * g.p * *S1 <= c->num_sms && !(env && env[0] == '0');
   // pass 2 has no accumulation-chain bound (its TMEM chain runs over j, not N): the split only
   // serves occupancy, which small problems need (C2: 8 row tiles x 2 outputs) and large ones do
   // not -- there every extra split re-reads the CTA's 128 KB Z operand (C5: +6% pass-2 time at 9
@@ -1550,16 +1583,6 @@ static void set_attrs() {
     }));
   }
   cudaGetLastError();
-}
-
-// Cluster size along the row tiles (TMA multicast of the shared B operand tiles).  Measured
-// neutral at the bench shape (pass 1 is bound by the ktilde generators and the MMAs, not by L2),
-// so off by default; BAGEL_TC_CLUSTER=2 enables it when the row-tile count is even.
-int tc_cluster_x(const bagel_ctx* c, int B) {
-  (void)c;
-  const char* env = getenv("BAGEL_TC_CLUSTER");
-  if (env && env[0] == '2') return cdiv(B, 128) % 2 == 0 ? 2 : 1;
-  return 1;
 }
 
 // The grid-barrier kernels launch WITHOUT the cooperative attribute by default: a cooperative
@@ -1599,7 +1622,8 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, floa
   a.dbg = T.dbg1;
   for (int m = 0; m < c->p; ++m)
     for (int j = 0; j < BAGEL_MAX_D; ++j) a.qscale[m][j] = c->gp.qscale[m][j];
-  dim3 grid(cdiv(B, 128), c->p * g.nct, c->ws.S1tc);
+  // CTA pairs along the row tiles; a pair covers two z-column tiles
+  dim3 grid(tc_pair_row_tiles(B), c->p * cdiv(g.nct, 2), c->ws.S1tc);
   if (c->ws.p1_fused) {
     a.colscale = T.colscale;
     for (int m = 0; m < c->p; ++m) {
@@ -1628,14 +1652,11 @@ int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, floa
     at[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  const int cl = tc_cluster_x(c, B);
-  if (cl > 1) {
-    at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = (unsigned)cl;
-    at[na].val.clusterDim.y = 1;
-    at[na].val.clusterDim.z = 1;
-    ++na;
-  }
+  at[na].id = cudaLaunchAttributeClusterDimension;
+  at[na].val.clusterDim.x = 2;
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
   if (c->ws.p1_fused && tc_coop_enabled()) {
     at[na].id = cudaLaunchAttributeCooperative;
     at[na].val.cooperative = 1;

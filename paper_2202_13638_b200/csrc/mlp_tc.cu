@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_fwd_tc(const __grid_constant
     }
   } else if (warp == EPI_WARPS + 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    {  // the warp runs the loop; one elected lane issues each chunk's MMAs back to back
       int q = 0;
       for (int l = 0; l < L; ++l) {
         tc::mbar_wait(&a_ready, (uint32_t)l & 1u);  // this layer's input H is in TMEM
@@ -205,17 +205,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_fwd_tc(const __grid_constant
           const uint32_t sbo = (uint32_t)(kc / 8) * 128u;
           const uint64_t bhi = tc::umma_desc(base, 128, sbo);
           const uint64_t blo = tc::umma_desc(base + (uint32_t)a.Np[l] * kc * 2u, 128, sbo);
-          for (int ks = 0; ks < kc / 16; ++ks) {
-            const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4
-            const uint32_t ac = (uint32_t)((k0 + 16 * ks) / 2);
-            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, bhi + o, idesc, first ? 0u : 1u);
-            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, blo + o, idesc, 1u);
-            tc::mma_f16_ts(tmem + ACC, tmem + ALO + ac, bhi + o, idesc, 1u);
-            first = false;
+          if (tc::elect_one()) {
+            for (int ks = 0; ks < kc / 16; ++ks) {
+              const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4
+              const uint32_t ac = (uint32_t)((k0 + 16 * ks) / 2);
+              tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, bhi + o, idesc, (first && ks == 0) ? 0u : 1u);
+              tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, blo + o, idesc, 1u);
+              tc::mma_f16_ts(tmem + ACC, tmem + ALO + ac, bhi + o, idesc, 1u);
+            }
+            tc::umma_commit(&empty[s]);
           }
-          tc::umma_commit(&empty[s]);
+          __syncwarp();
+          first = false;
         }
-        tc::umma_commit(&mma_done);
+        if (tc::elect_one()) tc::umma_commit(&mma_done);
+        __syncwarp();
       }
     }
   } else {
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_bwd_tc(const __grid_constant
       }
     }
   } else if (warp == EPI_WARPS + 1) {
-    if (lane == 0) {
+    {  // the warp runs the loop; one elected lane issues each chunk's MMAs back to back
       int c = 0;
       for (int j = 0; j < L; ++j) {
         const int l = L - 1 - j;
@@ -429,17 +433,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_mlp_bwd_tc(const __grid_constant
           const uint32_t sbo = (uint32_t)(kc / 8) * 128u;
           const uint64_t bhi = tc::umma_desc(base, 128, sbo);
           const uint64_t blo = tc::umma_desc(base + (uint32_t)a.Np[l] * kc * 2u, 128, sbo);
-          for (int ks = 0; ks < kc / 16; ++ks) {
-            const uint64_t o = (uint64_t)(ks * 16);
-            const uint32_t ac = (uint32_t)((k0 + 16 * ks) / 2);
-            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, bhi + o, idesc, first ? 0u : 1u);
-            tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, blo + o, idesc, 1u);
-            tc::mma_f16_ts(tmem + ACC, tmem + ALO + ac, bhi + o, idesc, 1u);
-            first = false;
+          if (tc::elect_one()) {
+            for (int ks = 0; ks < kc / 16; ++ks) {
+              const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4
+              const uint32_t ac = (uint32_t)((k0 + 16 * ks) / 2);
+              tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, bhi + o, idesc, (first && ks == 0) ? 0u : 1u);
+              tc::mma_f16_ts(tmem + ACC, tmem + AHI + ac, blo + o, idesc, 1u);
+              tc::mma_f16_ts(tmem + ACC, tmem + ALO + ac, bhi + o, idesc, 1u);
+            }
+            tc::umma_commit(&empty[s]);
           }
-          tc::umma_commit(&empty[s]);
+          __syncwarp();
+          first = false;
         }
-        tc::umma_commit(&mma_done);
+        if (tc::elect_one()) tc::umma_commit(&mma_done);
+        __syncwarp();
       }
     }
   } else {
