@@ -49,8 +49,10 @@ constexpr int P2_LD = 1 + BAGEL_MAX_D;
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 __host__ __device__ inline int cdiv_dev(int a, int b) { return (a + b - 1) / b; }
-// pass-1 ring depth for NC z-column tiles per CTA pair (stage = A 16 KB + NC x 16 KB of B halves)
+// pass-1 ring depth for NC z-column tiles per CTA pair (NC = 1: A in TMEM, stage = B halves 16 KB;
+// NC = 2: stage = A 16 KB + 2 x 16 KB of B halves in shared memory)
 __host__ __device__ constexpr int p1_stages(int NC) { return NC > 1 ? 4 : 6; }
+constexpr int A1C = 32;      // TMEM columns of one A stage when A lives in TMEM (NC = 1): hi (16) | lo (16)
 
 struct Geo {
   int N, d, p, k;
@@ -421,8 +423,13 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
   const int nctp = cdiv_dev(g.nct, 2);
   const int m = by / nctp, ctp = by % nctp, ct0 = 2 * ctp;
   const int NC = min(2, g.nct - ct0);
+  // NC = 1 (k <= 256, and an odd last column tile): ktilde goes to TMEM and the pair MMA reads it
+  // there (TS form) -- TMEM has room for one accumulator plus the A ring; NC = 2 needs all 512
+  // columns for the two accumulators, so A goes to shared memory (SS form)
+  const bool ats = NC == 1;
   const int nst = p1_stages(NC);
-  const size_t a_bytes = (size_t)128 * KT1 * 2 * 2;      // A hi | lo of this CTA's 128 rows
+  const uint32_t acol0 = (uint32_t)NZ;                   // TMEM A ring (ats): columns [NZ, NZ + nst A1C)
+  const size_t a_bytes = ats ? 0 : (size_t)128 * KT1 * 2 * 2;  // A hi | lo of this CTA's 128 rows (smem)
   const size_t bh_bytes = (size_t)(NZ / 2) * KT1 * 2;    // B hi (or lo) of this CTA's NZ/2 columns
   const size_t st_bytes = a_bytes + (size_t)NC * 2 * bh_bytes;
   const size_t x_bytes = (size_t)KT1 * AUXW * 4;         // aux rows of one tile
@@ -513,19 +520,33 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         const uint32_t sbase = tc::smem_u32(ssm + (size_t)s * st_bytes);
         const uint64_t dahi = tc::umma_desc(sbase, 128, SBO);
         const uint64_t dalo = tc::umma_desc(sbase + (uint32_t)(a_bytes / 2), 128, SBO);
+        const uint32_t tahi = tmem + acol0 + (uint32_t)(s * A1C), talo = tahi + (uint32_t)(KT1 / 2);
         if (tc::elect_one()) {
           if (!(a.diag & 2)) {
+            if (ats) {
 #pragma unroll
-            for (int ks = 0; ks < KT1 / 16; ++ks) {
-              const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
-              const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
-              for (int c = 0; c < NC; ++c) {
-                const uint32_t bb = sbase + (uint32_t)(a_bytes + (size_t)c * 2 * bh_bytes);
-                const uint64_t dbhi = tc::umma_desc(bb, 128, SBO), dblo = tc::umma_desc(bb + (uint32_t)bh_bytes, 128, SBO);
-                const uint32_t d = tmem + (uint32_t)(c * NZ);
-                tc::mma_f16_2(d, dahi + o, dbhi + o, idesc, acc0);
-                tc::mma_f16_2(d, dahi + o, dblo + o, idesc, 1u);
-                tc::mma_f16_2(d, dalo + o, dbhi + o, idesc, 1u);
+              for (int ks = 0; ks < KT1 / 16; ++ks) {
+                const uint64_t o = (uint64_t)(ks * 16);  // 256 bytes >> 4, start-address field
+                const uint32_t ac = (uint32_t)(ks * 8);  // 16 K elements = 8 TMEM columns
+                const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
+                const uint64_t dbhi = tc::umma_desc(sbase, 128, SBO), dblo = tc::umma_desc(sbase + (uint32_t)bh_bytes, 128, SBO);
+                tc::mma_f16_ts2(tmem, tahi + ac, dbhi + o, idesc, acc0);
+                tc::mma_f16_ts2(tmem, tahi + ac, dblo + o, idesc, 1u);
+                tc::mma_f16_ts2(tmem, talo + ac, dbhi + o, idesc, 1u);
+              }
+            } else {
+#pragma unroll
+              for (int ks = 0; ks < KT1 / 16; ++ks) {
+                const uint64_t o = (uint64_t)(ks * 16);
+                const uint32_t acc0 = (i > 0 || ks > 0) ? 1u : 0u;
+                for (int c = 0; c < NC; ++c) {
+                  const uint32_t bb = sbase + (uint32_t)(a_bytes + (size_t)c * 2 * bh_bytes);
+                  const uint64_t dbhi = tc::umma_desc(bb, 128, SBO), dblo = tc::umma_desc(bb + (uint32_t)bh_bytes, 128, SBO);
+                  const uint32_t d = tmem + (uint32_t)(c * NZ);
+                  tc::mma_f16_2(d, dahi + o, dbhi + o, idesc, acc0);
+                  tc::mma_f16_2(d, dahi + o, dblo + o, idesc, 1u);
+                  tc::mma_f16_2(d, dalo + o, dbhi + o, idesc, 1u);
+                }
               }
             }
           }
@@ -552,6 +573,7 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
     const int gt = tid - 32 * CTRL_WARPS;  // 0..511
     const int r = (warp % 4) * 32 + lane, qd = (warp - CTRL_WARPS) / 4;
     const int row = row0 + r;
+    const uint32_t tlane = (uint32_t)((warp % 4) * 32) << 16;
     // element (r, 8 qd .. 8 qd + 7) of the canonical layout: one 16-byte chunk
     const uint32_t aoff = (uint32_t)((((r >> 3) * (KT1 / 8) + qd) << 6) + ((r & 7) << 3)) * 2u;
     // exponent as (x*_c - X_nc) * kappa / l_c: difference first, then scale (4x smaller fp32
@@ -607,12 +629,22 @@ __device__ __forceinline__ void p1_main(const P1Args& a, const int bx, const int
         hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l2);
       }
-      // A tile (row r, K 8 qd .. 8 qd + 7) -> stage s, hi then lo; then make the generic-proxy
-      // writes visible to the tensor core (async proxy) before the leader may issue on them
-      uint8_t* abase = ssm + (size_t)s * st_bytes;
-      *reinterpret_cast<uint4*>(abase + aoff) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      *reinterpret_cast<uint4*>(abase + a_bytes / 2 + aoff) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-      tc::fence_proxy_async();
+      if (ats) {
+        // A tile (row r, K pairs 4 qd .. 4 qd + 3) -> TMEM stage s, hi then lo
+        tc::tc_fence_after();
+        const uint32_t ta = tmem + tlane + acol0 + (uint32_t)(s * A1C + qd * 4);
+        tc::tmem_st4(ta, hw);
+        tc::tmem_st4(ta + (uint32_t)(KT1 / 2), lw);
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+      } else {
+        // A tile (row r, K 8 qd .. 8 qd + 7) -> stage s, hi then lo; then make the generic-proxy
+        // writes visible to the tensor core (async proxy) before the leader may issue on them
+        uint8_t* abase = ssm + (size_t)s * st_bytes;
+        *reinterpret_cast<uint4*>(abase + aoff) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(abase + a_bytes / 2 + aoff) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        tc::fence_proxy_async();
+      }
       // MEMBAR.CTA: every aux load above has returned before the aux stage is released
       // (SYNCS.ARRIVE does not wait for pending LDS)
       if (!(a.diag & 4)) __threadfence_block();
@@ -835,7 +867,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_p1_tc(P1Args a) {
   const int nctp = cdiv_dev(a.g.nct, 2);
   const int NC = min(2, a.g.nct - 2 * ((int)blockIdx.y % nctp));
   uint32_t ncols = 32;
-  while ((int)ncols < NC * a.g.NZ) ncols <<= 1;
+  const int need = NC == 1 ? a.g.NZ + p1_stages(1) * A1C : NC * a.g.NZ;  // NC = 1: + the TMEM A ring
+  while ((int)ncols < need) ncols <<= 1;
   if (threadIdx.x / 32 == 1) tc::tmem_alloc2(&tmem_base, ncols);  // the pair's accumulators
   tc::tc_fence_before();
   __syncthreads();
@@ -1489,7 +1522,7 @@ size_t p1_smem(const Geo& g) {
   // stage ring (A | NC B halves) + aux ring; the FUSED tail parks a [128][NZ + 4] fp32 partial tile
   // in the same memory
   const int NC = g.nct > 1 ? 2 : 1;
-  const size_t st = (size_t)128 * KT1 * 4 + (size_t)NC * g.NZ * KT1 * 2;
+  const size_t st = (NC > 1 ? (size_t)128 * KT1 * 4 : 0) + (size_t)NC * g.NZ * KT1 * 2;
   const size_t ring = (size_t)p1_stages(NC) * st + (size_t)STA * KT1 * AUXW * 4;
   return std::max(ring, (size_t)128 * (g.NZ + 4) * 4);
 }
