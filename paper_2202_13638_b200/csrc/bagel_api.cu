@@ -158,6 +158,8 @@ void free_workspace(bagel_ctx* c) {
   w.B = w.T = 0;
   w.S1 = w.S2 = 0;
   w.theta_part_cap = 0;
+  dev_free(w.theta_colmax);
+  w.theta_colmax_cap = 0;
 }
 
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
@@ -246,6 +248,13 @@ void ensure_workspace(bagel_ctx* c, int B, int T) {
       dev_alloc(c, w.tape_act, rows * c->pol.act_ld);
       dev_alloc(c, w.tape_delta, rows * c->pol.d_ld);
       w.tape_pol_cap = rows;
+    }
+    if (theta_tc_enabled(c->pol)) {
+      const size_t cm = theta_tc_colmax_floats(c->pol, (long long)std::max(w.T, 1) * w.B);
+      if (w.theta_colmax_cap < cm) {
+        dev_alloc(c, w.theta_colmax, cm);
+        w.theta_colmax_cap = cm;
+      }
     }
     if (!w.grad_tmp) dev_alloc(c, w.grad_tmp, (size_t)c->pol.n_params + 64);
     if (!w.thetaT) dev_alloc(c, w.thetaT, (size_t)c->pol.n_params + 64);
@@ -773,7 +782,11 @@ extern "C" int rollout_cost_and_grad(bagel_ctx* c, const float* policy_params, c
     float* gout = dev_grad ? grad : c->ws.grad_tmp;
     int nblk = 0;
     launches += timed(c, PC_REVERSE, [&] { return ro_reverse(c, th, gd, B, T, seed, traj_offset, B_global, &nblk, st); });
-    launches += timed(c, PC_THETA, [&] { return ro_theta_grad(c, B, T, nblk, st); });
+    {
+      const int n = timed(c, PC_THETA, [&] { return ro_theta_grad(c, B, T, nblk, st); });
+      REQUIRE(n > 0, BAGEL_E_CUDA, "rollout: could not encode the tensor maps of the theta-gradient contraction");
+      launches += n;
+    }
     launches += timed(c, PC_REDUCE, [&] { return ro_reduce(c, nblk, B, B_global, gout, st); });
     CK(cudaGetLastError());
     double cost = 0.0;

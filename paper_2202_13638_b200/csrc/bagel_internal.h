@@ -109,6 +109,8 @@ struct Workspace {
   int p1_fused = 0;  // pass 1 launched cooperatively with reduce 1 fused in (k_p1_tc<D, true>)
   int S2eff = 0;            // number of pass-2 partial slices the epilogue sums
   float* xstar = nullptr;   // B x d
+  float* theta_colmax = nullptr;  // theta_tc.cu: per K block, max |delta| per tape column + max |phi|
+  size_t theta_colmax_cap = 0;
   float* P1 = nullptr;      // S1 x p x B x Cld partial [mu | k a X | z]
   float* Z = nullptr;       // p x B x k
   float* P2 = nullptr;      // S2 x p x B x (1 + MAX_D) partial [sum w k | sum w k X_c]
@@ -295,6 +297,12 @@ size_t tc_p1z_floats(const bagel_ctx* c, int B, int S1);
 size_t tc_zp_bytes(const bagel_ctx* c, int B);
 int tc_njt(const bagel_ctx* c);
 int tc_pair_row_tiles(int B);  // row tiles rounded up to whole CTA pairs
+// theta_tc.cu: the parameter gradient of wide policies on the tensor cores
+bool theta_tc_enabled(const PolicyDesc& P);
+int theta_tc_blocks(long long K);
+size_t theta_tc_colmax_floats(const PolicyDesc& P, long long K);
+int theta_grad_tc(const PolicyDesc& P, long long K, const float* act, const float* delta, float* colmax, float* part,
+                  cudaStream_t st);
 size_t tc_zpart_count(const bagel_ctx* c, int B);
 size_t tc_gbar_count();
 int tc_pass1(const bagel_ctx* c, const float* xstar, int B, float* jmu_out, float* sig_out, cudaStream_t st);

@@ -610,6 +610,7 @@ size_t ro_theta_grad_smem(const PolicyDesc& P) {
 }
 int ro_theta_blocks(const bagel_ctx* c, int B, int T) {
   const long long K = (long long)B * std::max(T, 1);
+  if (theta_tc_enabled(c->pol)) return theta_tc_blocks(K);  // tensor-core path: 4,096-row K blocks
   return (int)std::max(1LL, std::min((long long)c->num_sms, K / 64));
 }
 size_t ro_policy_smem(const PolicyDesc& P) { return policy_smem(P); }
@@ -713,6 +714,8 @@ int ro_reverse(const bagel_ctx* c, const float* theta, const float* goals, int B
 
 int ro_theta_grad(const bagel_ctx* c, int B, int T, int nblk, cudaStream_t st) {
   const Workspace& w = c->ws;
+  if (theta_tc_enabled(c->pol))  // wide policies: the delta^T H contraction on the tensor cores
+    return theta_grad_tc(c->pol, (long long)T * B, w.tape_act, w.tape_delta, w.theta_colmax, w.theta_part, st);
   int njobs = 0;
   for (int l = 0; l < c->pol.n_layers; ++l)
     njobs += ((c->pol.sizes[l + 1] + 3) / 4) * ((c->pol.sizes[l] + 3) / 4 + 1);
