@@ -88,6 +88,10 @@ def lib():
             L.orc_adam_step.restype = C.c_int
             L.orc_mll.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, _dp, _dp]
             L.orc_mll.restype = C.c_int
+            L.orc_mll_bbmm.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
+            L.orc_mll_bbmm.restype = C.c_int
+            L.orc_bbmm_probe.argtypes = [C.c_uint64, C.c_int, C.c_int]
+            L.orc_bbmm_probe.restype = C.c_double
             L.orc_num_threads.restype = C.c_int
             L.orc_set_num_threads.argtypes = [C.c_int]
             _lib = L
@@ -277,6 +281,27 @@ def log_marginal_likelihood(X, y, log_hyp, want_grad=True):
     if rc != 0:
         raise ArithmeticError(f"oracle Cholesky failed at pivot {rc - 1}")
     return val.value, g
+
+
+def log_marginal_likelihood_bbmm(X, y, log_hyp, n_probes, n_iter, seed, want_grad=True):
+    """BBMM estimate of (log p, d/dphi) -- mBCG with n_probes Rademacher probes and exactly n_iter CG
+    iterations, SLQ log-det, Hutchinson trace (NEXT-1 at large N, reading R39).  Returns
+    (mll, grad or None, logdet estimate, y^T u_0)."""
+    X, y, h = _d(X), _d(y).reshape(-1), _d(log_hyp).reshape(-1)
+    N, d = X.shape
+    assert h.shape == (d + 2,) and y.shape == (N,)
+    val, ld, qd = C.c_double(0.0), C.c_double(0.0), C.c_double(0.0)
+    g = np.zeros(d + 2) if want_grad else None
+    rc = lib().orc_mll_bbmm(_ptr(X), N, d, _ptr(y), _ptr(h), int(n_probes), int(n_iter), int(seed), C.byref(val),
+                            _ptr(g), C.byref(ld), C.byref(qd))
+    if rc != 0:
+        raise MemoryError("oracle BBMM: allocation failed")
+    return val.value, g, ld.value, qd.value
+
+
+def bbmm_probes(seed, n_probes, N) -> np.ndarray:
+    """The Rademacher probes of log_marginal_likelihood_bbmm (n_probes x N)."""
+    return np.array([[lib().orc_bbmm_probe(int(seed), i, n) for n in range(N)] for i in range(n_probes)])
 
 
 # ---------------------------------------------------------------- Algorithm 1 around the path

@@ -877,3 +877,193 @@ int orc_mll(const double* X, int N, int d, const double* y, const double* log_hy
     free(L);
     return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-1 at large N: the BBMM estimate of Eq.5-6 (P:77-81 defers to   */
+/* GPyTorch [gardner2018]; reading R39).  Probes z_1..z_t are Rademacher  */
+/* from Philox (key = seed, ctr = (i, n >> 2, 0x4242424D, 4), the sign   */
+/* bit of word n & 3).  One batched conjugate-gradient run of exactly J  */
+/* iterations (no preconditioner) solves Khat [u_0 .. u_t] = [y z_1 ..   */
+/* z_t]; every probe's CG coefficients give its Lanczos tridiagonal T_i, */
+/* and                                                                    */
+/*   log|Khat| ~ (1/t) sum_i ||z_i||^2 e_1^T log(T_i) e_1    (SLQ)        */
+/*   y^T Khat^-1 y ~ y^T u_0                                              */
+/*   tr(Khat^-1 dK) ~ (1/t) sum_i u_i^T dK z_i              (Hutchinson)  */
+/*   mll = -1/2 y^T u_0 - 1/2 log|Khat| - N/2 log 2 pi,                   */
+/*   d mll / d phi_j = 1/2 u_0^T dK_j u_0 - 1/2 tr(Khat^-1 dK_j).         */
+/* A column whose residual reaches exactly 0 stops early (its T is the   */
+/* iterations done).  The eigen-decomposition of T_i is cyclic Jacobi.   */
+/* ------------------------------------------------------------------ */
+double orc_bbmm_probe(uint64_t seed, int i, int n)
+{
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {(uint32_t)i, (uint32_t)(n >> 2), 0x4242424Du, 4u};
+    uint32_t o[4];
+    orc_philox4x32_10(ctr, key, o);
+    return (o[n & 3] >> 31) ? -1.0 : 1.0;
+}
+
+/* e_1^T log(T) e_1 of a symmetric tridiagonal (diag a[0..J-1], off b[0..J-2]) by cyclic Jacobi on the
+ * dense J x J matrix */
+static double orc_tridiag_e1_log_e1(const double* a, const double* b, int J)
+{
+    double* A = (double*)calloc((size_t)J * J, sizeof(double));
+    double* V = (double*)calloc((size_t)J * J, sizeof(double));
+    for (int i = 0; i < J; ++i) {
+        A[(size_t)i * J + i] = a[i];
+        V[(size_t)i * J + i] = 1.0;
+        if (i + 1 < J) A[(size_t)i * J + i + 1] = A[(size_t)(i + 1) * J + i] = b[i];
+    }
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0, diag = 0.0;
+        for (int p = 0; p < J; ++p)
+            for (int q = 0; q < J; ++q) {
+                if (p == q) diag += A[(size_t)p * J + p] * A[(size_t)p * J + p];
+                else off += A[(size_t)p * J + q] * A[(size_t)p * J + q];
+            }
+        if (off <= 1e-30 * diag) break;
+        for (int p = 0; p < J - 1; ++p)
+            for (int q = p + 1; q < J; ++q) {
+                double apq = A[(size_t)p * J + q];
+                if (fabs(apq) < 1e-300) continue;
+                double app = A[(size_t)p * J + p], aqq = A[(size_t)q * J + q];
+                double theta = (aqq - app) / (2.0 * apq);
+                double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+                for (int k = 0; k < J; ++k) { /* A <- A J (columns p, q) */
+                    double akp = A[(size_t)k * J + p], akq = A[(size_t)k * J + q];
+                    A[(size_t)k * J + p] = c * akp - sn * akq;
+                    A[(size_t)k * J + q] = sn * akp + c * akq;
+                }
+                for (int k = 0; k < J; ++k) { /* A <- J^T A (rows p, q) */
+                    double apk = A[(size_t)p * J + k], aqk = A[(size_t)q * J + k];
+                    A[(size_t)p * J + k] = c * apk - sn * aqk;
+                    A[(size_t)q * J + k] = sn * apk + c * aqk;
+                }
+                for (int k = 0; k < J; ++k) { /* V <- V J */
+                    double vkp = V[(size_t)k * J + p], vkq = V[(size_t)k * J + q];
+                    V[(size_t)k * J + p] = c * vkp - sn * vkq;
+                    V[(size_t)k * J + q] = sn * vkp + c * vkq;
+                }
+            }
+    }
+    double r = 0.0;
+    for (int k = 0; k < J; ++k) r += V[k] * V[k] * log(A[(size_t)k * J + k]); /* V[0][k]^2 log lambda_k */
+    free(A);
+    free(V);
+    return r;
+}
+
+int orc_mll_bbmm(const double* X, int N, int d, const double* y, const double* log_hyp, int t, int J,
+                 uint64_t seed, double* mll, double* grad, double* logdet_out, double* quad_out)
+{
+    double ell[16];
+    for (int c = 0; c < d; ++c) ell[c] = exp(log_hyp[c]);
+    double s = exp(log_hyp[d]), sn2 = exp(log_hyp[d + 1]);
+    double* K = orc_khat(X, N, d, ell, s, sn2);
+    if (!K) return -1;
+    const int nc = t + 1;
+    double* Z = (double*)malloc(sizeof(double) * (size_t)nc * N); /* rhs columns: y, z_1..z_t */
+    double* U = (double*)calloc((size_t)nc * N, sizeof(double));
+    double* Rr = (double*)malloc(sizeof(double) * (size_t)nc * N);
+    double* P = (double*)malloc(sizeof(double) * (size_t)nc * N);
+    double* Q = (double*)malloc(sizeof(double) * (size_t)N);
+    double* al = (double*)malloc(sizeof(double) * (size_t)nc * J);
+    double* be = (double*)malloc(sizeof(double) * (size_t)nc * J);
+    int* its = (int*)malloc(sizeof(int) * nc);
+    for (int n = 0; n < N; ++n) Z[n] = y[n];
+    for (int i = 1; i <= t; ++i)
+        for (int n = 0; n < N; ++n) Z[(size_t)i * N + n] = orc_bbmm_probe(seed, i - 1, n);
+    for (int c = 0; c < nc; ++c) {
+        const double* b = Z + (size_t)c * N;
+        double *u = U + (size_t)c * N, *r = Rr + (size_t)c * N, *p = P + (size_t)c * N;
+        double rr = 0.0;
+        for (int n = 0; n < N; ++n) {
+            r[n] = b[n];
+            p[n] = b[n];
+            rr += b[n] * b[n];
+        }
+        its[c] = 0;
+        for (int j = 0; j < J && rr > 0.0; ++j) {
+#pragma omp parallel for schedule(static)
+            for (int a = 0; a < N; ++a) {
+                double acc = 0.0;
+                for (int n = 0; n < N; ++n) acc += K[(size_t)a * N + n] * p[n];
+                Q[a] = acc;
+            }
+            double pq = 0.0;
+            for (int n = 0; n < N; ++n) pq += p[n] * Q[n];
+            const double alpha = rr / pq;
+            double rr2 = 0.0;
+            for (int n = 0; n < N; ++n) {
+                u[n] += alpha * p[n];
+                r[n] -= alpha * Q[n];
+                rr2 += r[n] * r[n];
+            }
+            const double beta = rr2 / rr;
+            for (int n = 0; n < N; ++n) p[n] = r[n] + beta * p[n];
+            al[(size_t)c * J + j] = alpha;
+            be[(size_t)c * J + j] = beta;
+            rr = rr2;
+            its[c] = j + 1;
+        }
+    }
+    /* SLQ over the probes */
+    double logdet = 0.0;
+    double* ta = (double*)malloc(sizeof(double) * J);
+    double* tb = (double*)malloc(sizeof(double) * J);
+    for (int i = 1; i <= t; ++i) {
+        const int n = its[i];
+        const double* a_ = al + (size_t)i * J;
+        const double* b_ = be + (size_t)i * J;
+        for (int j = 0; j < n; ++j) {
+            ta[j] = 1.0 / a_[j] + (j > 0 ? b_[j - 1] / a_[j - 1] : 0.0);
+            if (j + 1 < n) tb[j] = sqrt(b_[j]) / a_[j];
+        }
+        double zz = 0.0;
+        for (int m = 0; m < N; ++m) zz += Z[(size_t)i * N + m] * Z[(size_t)i * N + m];
+        logdet += zz * orc_tridiag_e1_log_e1(ta, tb, n);
+    }
+    logdet /= (double)t;
+    double quad = 0.0;
+    for (int n = 0; n < N; ++n) quad += y[n] * U[n];
+    *mll = -0.5 * quad - 0.5 * logdet - 0.5 * N * log(2.0 * 3.14159265358979323846);
+    if (logdet_out) *logdet_out = logdet;
+    if (quad_out) *quad_out = quad;
+    if (grad) {
+        for (int jp = 0; jp < d + 2; ++jp) {
+            /* w^T dK_jp v for (w, v) = (u_0, u_0) and (u_i, z_i) */
+            double q0 = 0.0, tr = 0.0;
+            for (int c = 0; c < nc; ++c) {
+                const double* w = U + (size_t)c * N;
+                const double* v = c == 0 ? U : Z + (size_t)c * N;
+                /* per-row terms in parallel, summed in row order (thread-count independent) */
+#pragma omp parallel for schedule(static)
+                for (int a = 0; a < N; ++a) {
+                    double row = 0.0;
+                    for (int b2 = 0; b2 < N; ++b2) {
+                        double dk;
+                        if (jp < d) {
+                            double diff = X[(size_t)a * d + jp] - X[(size_t)b2 * d + jp];
+                            dk = orc_kernel(X + (size_t)a * d, X + (size_t)b2 * d, d, ell, s) * diff * diff /
+                                 (ell[jp] * ell[jp]);
+                        } else if (jp == d) {
+                            dk = orc_kernel(X + (size_t)a * d, X + (size_t)b2 * d, d, ell, s);
+                        } else {
+                            dk = (a == b2) ? sn2 : 0.0;
+                        }
+                        row += dk * v[b2];
+                    }
+                    Q[a] = w[a] * row;
+                }
+                double acc = 0.0;
+                for (int a = 0; a < N; ++a) acc += Q[a];
+                if (c == 0) q0 = acc;
+                else tr += acc;
+            }
+            grad[jp] = 0.5 * q0 - 0.5 * tr / (double)t;
+        }
+    }
+    free(ta); free(tb); free(its); free(be); free(al); free(Q); free(P); free(Rr); free(U); free(Z); free(K);
+    return 0;
+}

@@ -85,3 +85,89 @@ def test_zero_targets_push_signal_variance_down():
     X, _, ell, s, noise = small_gp_data(N=30, d=2, p=1, seed=2)
     _, g = O.log_marginal_likelihood(X, np.zeros(30), np.log(np.r_[ell[0], s[0], noise[0]]))
     assert g[2] < 0 and g[3] < 0
+
+
+# ------------------------------------------------------------------ BBMM estimate (NEXT-1 at large N, R39)
+def _khat(X, ell, s, sn2):
+    K = O.kernel_matrix(X, X, ell, s)
+    return K + sn2 * np.eye(len(X))
+
+
+def _dK(X, ell, s, sn2, j):
+    d = X.shape[1]
+    K = O.kernel_matrix(X, X, ell, s)
+    if j < d:
+        diff = X[:, None, j] - X[None, :, j]
+        return K * diff ** 2 / ell[j] ** 2
+    if j == d:
+        return K
+    return sn2 * np.eye(len(X))
+
+
+def test_bbmm_probes_are_rademacher_from_philox():
+    """z_i[n] = -1 iff the sign bit of Philox4x32-10(key = seed, ctr = (i, n >> 2, 0x4242424D, 4)) word
+    n & 3 is set (the convention the GPU reproduces)."""
+    Z = O.bbmm_probes(0x1234, 3, 9)
+    for i in range(3):
+        for n in range(9):
+            o = O.philox4x32_10(np.array([i, n >> 2, 0x4242424D, 4], dtype=np.uint32), [0x1234, 0])
+            assert Z[i, n] == (-1.0 if o[n & 3] >> 31 else 1.0)
+    assert set(np.unique(Z)) <= {-1.0, 1.0}
+
+
+def test_bbmm_full_krylov_is_exact_per_probe():
+    """With J = N CG iterations (the Krylov space is the whole space) each probe's quadrature is exact:
+    ||z||^2 e_1^T log(T) e_1 = z^T log(Khat) z, so the SLQ estimate equals (1/t) sum_i z_i^T log(Khat) z_i
+    computed by numpy's eigh; y^T u_0 = y^T Khat^-1 y; the Hutchinson term equals (1/t) sum_i
+    z_i^T Khat^-1 dK z_i (numpy solve) -- deterministic identities for the same probes."""
+    X, Y, ell, s, noise = small_gp_data(N=24, d=3, p=1, seed=5)
+    y = Y[:, 0]
+    s, sn2 = float(s[0]), 0.3 * float(s[0])  # well conditioned: full CG converges to rounding
+    t, seed = 5, 77
+    h = np.log(np.r_[ell[0], s, sn2])
+    mll, g, logdet, quad = O.log_marginal_likelihood_bbmm(X, y, h, t, len(y), seed)
+    Kh = _khat(X, ell[0], s, sn2)
+    lam, V = np.linalg.eigh(Kh)
+    logK = (V * np.log(lam)) @ V.T
+    Z = O.bbmm_probes(seed, t, len(y))
+    ref_logdet = np.mean([z @ logK @ z for z in Z])
+    assert logdet == pytest.approx(ref_logdet, rel=1e-9)
+    assert quad == pytest.approx(y @ np.linalg.solve(Kh, y), rel=1e-9)
+    assert mll == pytest.approx(-0.5 * quad - 0.5 * logdet - 0.5 * len(y) * LOG2PI, rel=1e-14)
+    a = np.linalg.solve(Kh, y)
+    for j in range(X.shape[1] + 2):
+        D = _dK(X, ell[0], s, sn2, j)
+        tr = np.mean([z @ np.linalg.solve(Kh, D @ z) for z in Z])
+        assert g[j] == pytest.approx(0.5 * a @ D @ a - 0.5 * tr, rel=1e-8, abs=1e-10 * np.abs(g).max())
+
+
+def test_bbmm_is_an_unbiased_estimate_of_the_exact_mll():
+    """Many probes: the SLQ log-det and the Hutchinson gradient converge to the exact (Cholesky) values
+    of orc_mll within a few standard errors (Rademacher probes: E[z^T A z] = tr A)."""
+    X, Y, ell, s, noise = small_gp_data(N=40, d=2, p=1, seed=6)
+    y = Y[:, 0]
+    h = np.log(np.r_[ell[0], float(s[0]), float(noise[0]) * 10])
+    exact, g_exact = O.log_marginal_likelihood(X, y, h)
+    t = 600
+    mll, g, logdet, quad = O.log_marginal_likelihood_bbmm(X, y, h, t, 40, 11)
+    Kh = _khat(X, ell[0], np.exp(h[2]), np.exp(h[3]))
+    lam, V = np.linalg.eigh(Kh)
+    L = (V * np.log(lam)) @ V.T
+    # Var(z^T L z) = 4 sum_{i<j} L_ij^2 for Rademacher z; the mll carries half the log-det
+    sd_logdet = np.sqrt(4 * np.sum(np.triu(L, 1) ** 2) / t)
+    assert abs(mll - exact) <= 4 * 0.5 * sd_logdet + 1e-9
+    assert np.linalg.norm(g - g_exact) <= 0.1 * np.linalg.norm(g_exact)
+
+
+def test_bbmm_fixed_iterations_and_thread_count_independent():
+    X, Y, ell, s, noise = small_gp_data(N=50, d=3, p=1, seed=8)
+    h = np.log(np.r_[ell[0], float(s[0]), float(noise[0])])
+    n0 = O.num_threads()
+    try:
+        O.set_num_threads(1)
+        r1 = O.log_marginal_likelihood_bbmm(X, Y[:, 0], h, 4, 20, 5)
+        O.set_num_threads(max(2, n0))
+        r2 = O.log_marginal_likelihood_bbmm(X, Y[:, 0], h, 4, 20, 5)
+    finally:
+        O.set_num_threads(n0)
+    assert r1[0] == r2[0] and np.array_equal(r1[1], r2[1])
