@@ -216,6 +216,31 @@ int policy_adam_step(bagel_ctx* ctx, float* params, const float* grad, float* m1
  * noise < 1e-8, workspace > 120 GB); E_NUMERIC if a Cholesky pivot <= 0; E_CUDA. */
 int gp_log_marginal_likelihood(bagel_ctx* ctx, int m, const double* log_hyp, double* mll, double* grad);
 
+/* gp_log_marginal_likelihood_bbmm -- the same quantities estimated the way the
+ * paper's GP library does it at scale (GPyTorch; "blackbox matrix-matrix"
+ * inference, reading R39), in float64 on the GPU without any factorisation:
+ *   one batched conjugate-gradient run of exactly n_iter iterations (no
+ *   preconditioner) on Khat [u_0 .. u_t] = [y z_1 .. z_t], z_i Rademacher with
+ *   z_i[n] = sign bit of Philox4x32-10(key = (seed lo, seed hi),
+ *   ctr = (i, n >> 2, 0x4242424D, 4))[n & 3] (set -> -1, clear -> +1), i = 0..t-1;
+ *   log|Khat| ~ (1/t) sum_i N e_1^T log(T_i) e_1 with T_i the Lanczos tridiagonal
+ *   of probe i from its CG coefficients (stochastic Lanczos quadrature);
+ *   y^T Khat^-1 y ~ y^T u_0;  tr(Khat^-1 dK) ~ (1/t) sum_i u_i^T dK z_i;
+ *   mll = -1/2 y^T u_0 - 1/2 log|Khat| - N/2 log(2 pi);
+ *   grad_j = 1/2 u_0^T dK_j u_0 - 1/2 (1/t) sum_i u_i^T dK_j z_i.
+ * A column whose residual reaches exactly 0 stops early (its T_i is smaller).
+ *   m, log_hyp, mll, grad  as gp_log_marginal_likelihood.
+ *   n_probes t in [1, 16];  n_iter J in [1, min(N, 4096)];  seed  probe stream.
+ *   logdet   [host, nullable] receives the log-det estimate.
+ * Synchronous.  Cost O(J N^2) for the solves plus O(t N^2 d) for the gradient;
+ * workspace N^2 + 5 (t + 1) N float64 (kept for later calls).  Deterministic:
+ * every reduction runs in a fixed order.  Does not change the loaded model.
+ * Errors: E_STATE without gp_load; E_ARG (m, t, J out of range, non-finite
+ * log_hyp, noise < 1e-8, workspace > 120 GB); E_NUMERIC when the estimate is
+ * non-finite (Khat too ill-conditioned for J iterations); E_CUDA. */
+int gp_log_marginal_likelihood_bbmm(bagel_ctx* ctx, int m, const double* log_hyp, int n_probes, int n_iter,
+                                    uint64_t seed, double* mll, double* grad, double* logdet);
+
 /* Number of kernel launches the last rollout_cost_and_grad enqueued: launches [host]
  * (the bench's gpu_launches count).  Errors: E_ARG for NULL pointers. */
 int bagel_last_launch_count(const bagel_ctx* ctx, int* launches);

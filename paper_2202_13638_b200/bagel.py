@@ -87,6 +87,9 @@ def lib() -> C.CDLL:
                                               C.POINTER(C.c_float), C.POINTER(C.c_float), _vp]
             L.gp_log_marginal_likelihood.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                                      C.POINTER(C.c_double)]
+            L.gp_log_marginal_likelihood_bbmm.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int,
+                                                          C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                          C.POINTER(C.c_double)]
             L.policy_adam_step.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_longlong, C.c_float, C.c_float,
                                            C.c_float, C.c_float, C.POINTER(C.c_int)]
             _lib = L
@@ -99,7 +102,7 @@ EXPORTS = ["bagel_create", "bagel_destroy", "bagel_set_stream", "bagel_last_erro
            "bagel_cache_rank", "bagel_cache_get", "bagel_cache_set", "bagel_profile", "bagel_profile_get", "bagel_tc_selftest",
            "bagel_set_gp_kernel", "bagel_get_gp_kernel", "bagel_tc_bench", "bagel_tc_selftest2",
            "bagel_debug_buffer", "bagel_debug_trace", "bagel_sample_states", "policy_adam_step",
-           "gp_log_marginal_likelihood", "exact_cache_build",
+           "gp_log_marginal_likelihood", "gp_log_marginal_likelihood_bbmm", "exact_cache_build",
            "gp_target_mode"]
 
 PROFILE_CLASSES = ["gp_pass1", "gp_reduce1", "gp_pass2", "step_epilogue", "init", "reverse", "reduce", "theta_grad"]
@@ -227,6 +230,21 @@ class Context:
         self._check(self.L.gp_log_marginal_likelihood(self.h, int(m), None if h is None else h.ctypes.data_as(dp),
                                                       C.byref(val), None if g is None else g.ctypes.data_as(dp)))
         return val.value, g
+
+    def log_marginal_likelihood_bbmm(self, m: int, log_hyp=None, n_probes: int = 8, n_iter: int = 100,
+                                     seed: int = 0, want_grad: bool = True):
+        """BBMM estimate (reading R39) of (log p(y_m | X, phi), d/dphi, log|Khat|): one batched CG of
+        exactly n_iter iterations on [y | z_1 .. z_t] (Rademacher Philox probes), SLQ log-det, Hutchinson trace."""
+        dp = C.POINTER(C.c_double)
+        h = None if log_hyp is None else np.ascontiguousarray(log_hyp, dtype=np.float64)
+        if h is not None and h.shape != (self.d + 2,):
+            raise ValueError(f"log_hyp must have d + 2 = {self.d + 2} entries")
+        val, ld = C.c_double(0.0), C.c_double(0.0)
+        g = np.zeros(self.d + 2) if want_grad else None
+        self._check(self.L.gp_log_marginal_likelihood_bbmm(
+            self.h, int(m), None if h is None else h.ctypes.data_as(dp), int(n_probes), int(n_iter),
+            int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(val), None if g is None else g.ctypes.data_as(dp), C.byref(ld)))
+        return val.value, g, ld.value
 
     # ------------------------------------------------------------ Algorithm 1 around the path
     def sample_states(self, seed: int, traj_offset: int, B: int, lo, hi, which: int = 0, out=None):

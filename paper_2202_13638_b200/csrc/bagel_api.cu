@@ -446,6 +446,8 @@ extern "C" int bagel_destroy(bagel_ctx* c) {
   dev_free(c->mll_K);
   dev_free(c->mll_Li);
   dev_free(c->mll_vec);
+  dev_free(c->bbmm_ws);
+  dev_free(c->bbmm_its);
   delete c;
   return BAGEL_OK;
 }
@@ -1110,6 +1112,52 @@ extern "C" int gp_log_marginal_likelihood(bagel_ctx* c, int m, const double* log
     *mll = -0.5 * hs[1] - hs[0] - 0.5 * N * log(2.0 * M_PI);
     if (grad)
       for (int i = 0; i < d + 2; ++i) grad[i] = hs[2 + i];
+  });
+}
+
+extern "C" int gp_log_marginal_likelihood_bbmm(bagel_ctx* c, int m, const double* log_hyp, int n_probes, int n_iter,
+                                               uint64_t seed, double* mll, double* grad, double* logdet) {
+  return guarded(c, [&] {
+    REQUIRE(c->N > 0, BAGEL_E_STATE, "gp_log_marginal_likelihood_bbmm: no GP loaded (call gp_load first)");
+    REQUIRE(m >= 0 && m < c->p, BAGEL_E_ARG, "gp_log_marginal_likelihood_bbmm: output m=%d out of range [0, %d)", m, c->p);
+    REQUIRE(mll, BAGEL_E_ARG, "gp_log_marginal_likelihood_bbmm: mll must be non-NULL");
+    REQUIRE(n_probes >= 1 && n_probes <= 16, BAGEL_E_ARG, "gp_log_marginal_likelihood_bbmm: n_probes=%d not in [1, 16]",
+            n_probes);
+    const int N = c->N, d = c->d;
+    REQUIRE(n_iter >= 1 && n_iter <= N && n_iter <= 4096, BAGEL_E_ARG,
+            "gp_log_marginal_likelihood_bbmm: n_iter=%d not in [1, min(N=%d, 4096)]", n_iter, N);
+    const size_t need = bbmm_workspace_doubles(N, n_probes + 1, n_iter);
+    REQUIRE((double)need * 8.0 < 120e9, BAGEL_E_ARG,
+            "gp_log_marginal_likelihood_bbmm: N=%d needs %.1f GB of float64 workspace, above the 120 GB limit", N,
+            (double)need * 8.0 / 1e9);
+    double h[BAGEL_MAX_D + 2];
+    for (int i = 0; i < d; ++i) h[i] = log_hyp ? log_hyp[i] : log((double)c->ell[(size_t)m * d + i]);
+    h[d] = log_hyp ? log_hyp[d] : log((double)c->s[m]);
+    h[d + 1] = log_hyp ? log_hyp[d + 1] : log((double)c->noise[m]);
+    for (int i = 0; i < d + 2; ++i)
+      REQUIRE(isfinite(h[i]) && fabs(h[i]) < 700.0, BAGEL_E_ARG,
+              "gp_log_marginal_likelihood_bbmm: log_hyp[%d] = %g out of range", i, h[i]);
+    REQUIRE(exp(h[d + 1]) >= 1e-8, BAGEL_E_ARG,
+            "gp_log_marginal_likelihood_bbmm: noise exp(log_hyp[%d]) = %g must be >= 1e-8", d + 1, exp(h[d + 1]));
+    if (c->bbmm_ws_n < need) {
+      dev_free(c->bbmm_ws);
+      c->bbmm_ws_n = 0;
+      dev_alloc(c, c->bbmm_ws, need);
+      c->bbmm_ws_n = need;
+    }
+    if (!c->bbmm_its) dev_alloc(c, c->bbmm_its, 32);
+    double ld = 0.0, quad = 0.0;
+    const int rc = bbmm_launch(c->X, c->Y + m, c->p, N, d, h, n_probes, n_iter, seed, c->bbmm_ws, c->bbmm_its, &ld,
+                               &quad, grad, c->stream);
+    CK(cudaGetLastError());
+    REQUIRE(rc != -2, BAGEL_E_CUDA, "gp_log_marginal_likelihood_bbmm: cuTensorMapEncodeTiled failed for the Khat tiles");
+    REQUIRE(rc == 0, BAGEL_E_CUDA, "gp_log_marginal_likelihood_bbmm: stream error");
+    REQUIRE(isfinite(ld) && isfinite(quad), BAGEL_E_NUMERIC,
+            "gp_log_marginal_likelihood_bbmm: non-finite estimate (log-det %g, quadratic form %g): Khat too "
+            "ill-conditioned for %d CG iterations",
+            ld, quad, n_iter);
+    *mll = -0.5 * quad - 0.5 * ld - 0.5 * N * log(2.0 * M_PI);
+    if (logdet) *logdet = ld;
   });
 }
 

@@ -171,6 +171,9 @@ struct bagel_ctx {
   double* mll_Li = nullptr;   // N x N: L^-1
   double* mll_vec = nullptr;  // alpha (N) | scalars (2) | grad (MAX_D + 2) | tile partials
   int mll_N = 0;
+  double* bbmm_ws = nullptr;  // BBMM workspace (bbmm.cu): Khat | rhs, u, r, p, q columns | CG coefficients | partials
+  size_t bbmm_ws_n = 0;
+  int* bbmm_its = nullptr;     // CG iterations per column
   int abs_target = 0;         // gp_target_mode
   int gp_kernel = 1;  // 1: tcgen05 path (default), 0: v0 FFMA path (reference / A-B tests)
   int last_launches = 0;
@@ -288,6 +291,9 @@ int op_sample_uniform(uint64_t seed, long long traj_offset, int B, int p, int wh
 int op_adam(float* theta, const float* g, float* m1, float* m2, int n, float lr, float b1, float b2, float eps,
             float bc1, float bc2, int* flag, cudaStream_t st);
 int mll_part_count(int N);
+size_t bbmm_workspace_doubles(int N, int nc, int J);
+int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const double* log_hyp, int t, int J,
+                uint64_t seed, double* ws, int* its_dev, double* logdet, double* quad, double* grad, cudaStream_t st);
 int exact_launch(const float* X, const float* Y, int ystride, int N, int d, const float* ell, float s, float noise,
                  double* K, double* Li, double* alpha, int* pivot_flag, cudaStream_t st);
 int mll_launch(const float* X, const float* Y, int ystride, int N, int d, const double* log_hyp, double* K,
