@@ -32,7 +32,6 @@ namespace bbmm {
 constexpr int MAXC = 17;      // t + 1 <= 17 columns (probes <= 16)
 constexpr int LDV = 256;      // vector / Khat row stride granularity (pads are zero)
 constexpr int RED = 256;      // threads of the reduction kernels
-constexpr int MW = 8;         // MVM warps (warp 0 also issues the copies)
 constexpr int GC = 4;         // columns per CTA of the gradient pass
 constexpr int GT = 64;        // gradient pair tile
 
@@ -83,13 +82,14 @@ __global__ void k_rhs(const float* __restrict__ Y, int ystride, int N, int ld, i
 // Khat tile and the NC x TC direction slice) into one ring stage, NST - 1 units ahead of the compute; consumer warp w owns rows R w .. R w + R - 1 of the unit
 // and lanes cover column pairs (16-byte shared loads, each direction pair reused for R rows, each
 // Khat pair for NC columns).  Shared-memory wavefronts per unit (reads + TMA writes) bound the rate:
-// R = 8 for NC <= 9 keeps them under the HBM time.  A row block's sums are flushed (fixed butterfly)
+// R = 4 rows per warp; 16 warps (latency hiding) for NC <= 9, 8 warps (fewer direction re-reads) above.  A row block's sums are flushed (fixed butterfly)
 // when its last chunk or the CTA's range ends, into partial slot rb + g (unique: the ranges are
 // monotone); k_mvm_fixup adds a row block's slots in CTA order (deterministic for a given SM count)
 // and emits the CTA partials of p.q for the CG step.
 template <int NC>
 struct MvmCfg {
-  static constexpr int R = NC <= 9 ? 8 : 4;        // rows per consumer warp
+  static constexpr int MW = NC <= 9 ? 16 : 8;      // warps (warp 0 also issues the copies)
+  static constexpr int R = 4;                      // rows per warp
   static constexpr int TR = MW * R;                // rows per unit
   static constexpr int TC = NC <= 9 ? 64 : 128;    // columns per unit
   static constexpr int KD = TR * TC;               // Khat doubles per stage
@@ -108,10 +108,10 @@ struct MvmMaps {
 };
 
 template <int NC>
-__global__ void __launch_bounds__(32 * MW, 1)
+__global__ void __launch_bounds__(32 * MvmCfg<NC>::MW, 1)
     k_mvm(const __grid_constant__ MvmMaps maps, double* __restrict__ part, int NRB, int NCH) {
   using Cfg = MvmCfg<NC>;
-  constexpr int R = Cfg::R, TR = Cfg::TR, TC = Cfg::TC, NST = Cfg::NST;
+  constexpr int R = Cfg::R, TR = Cfg::TR, TC = Cfg::TC, NST = Cfg::NST, MW = Cfg::MW;
   extern __shared__ __align__(128) uint8_t smraw[];
   double* stg = reinterpret_cast<double*>(smraw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)NST * Cfg::SD * 8);
@@ -130,13 +130,17 @@ __global__ void __launch_bounds__(32 * MW, 1)
   }
   __syncthreads();
   // warp 0 doubles as the producer: unit i's copies are issued NST - 1 units ahead
+  int prb = (int)(u0 / NCH), pch = (int)(u0 % NCH);  // next unit to load
   auto produce = [&](int i) {
     const int s = i % NST;
     tc::mbar_wait(&empty[s], ((uint32_t)(i / NST) & 1u) ^ 1u);
+    const int rb = prb, ch = pch;
+    if (++pch == NCH) {
+      pch = 0;
+      ++prb;
+    }
     if (lane == 0) {
       tc::mbar_arrive_expect_tx(&full[s], (uint32_t)(Cfg::SD * 8));
-      const long long u = u0 + i;
-      const int rb = (int)(u / NCH), ch = (int)(u % NCH);
       double* dst = stg + (size_t)s * Cfg::SD;
       const uint32_t bar = tc::smem_u32(&full[s]);
       asm volatile(
@@ -156,6 +160,7 @@ __global__ void __launch_bounds__(32 * MW, 1)
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[r][c] = 0.0;
+  int rb = (int)(u0 / NCH), ch = (int)(u0 % NCH);  // unit being consumed
   for (int i = 0; i < nu; ++i) {
     if (warp == 0 && i + NST - 1 < nu) produce(i + NST - 1);
     const int s = i % NST;
@@ -176,8 +181,6 @@ __global__ void __launch_bounds__(32 * MW, 1)
     }
     __syncwarp();
     if (lane == 0) tc::mbar_arrive(&empty[s]);
-    const long long u = u0 + i;
-    const int rb = (int)(u / NCH), ch = (int)(u % NCH);
     if (ch == NCH - 1 || i == nu - 1) {
       double* dst = part + (size_t)(rb + g) * NC * TR;
 #pragma unroll
@@ -190,6 +193,10 @@ __global__ void __launch_bounds__(32 * MW, 1)
           if (lane == 0) dst[c * TR + warp * R + r] = v;
           acc[r][c] = 0.0;
         }
+    }
+    if (++ch == NCH) {
+      ch = 0;
+      ++rb;
     }
   }
 }
@@ -273,7 +280,7 @@ static bool mvm_launch(const double* K, int N, int ld, const double* P, double* 
   if (!tmap_f64(&maps.k, K, ld, N, ld, MvmCfg<NC>::TC, MvmCfg<NC>::TR) ||
       !tmap_f64(&maps.p, P, ld, NC, ld, MvmCfg<NC>::TC, NC))
     return false;
-  k_mvm<NC><<<pl.G, 32 * MW, MvmCfg<NC>::SMEM, st>>>(maps, part, pl.NRB, pl.NCH);
+  k_mvm<NC><<<pl.G, 32 * MvmCfg<NC>::MW, MvmCfg<NC>::SMEM, st>>>(maps, part, pl.NRB, pl.NCH);
   k_mvm_fixup<<<(N + RED - 1) / RED, RED, 0, st>>>(part, N, ld, NC, pl.TR, pl.NCH, (long long)pl.NRB * pl.NCH, pl.G,
                                                    P, Q, pq_part);
   return true;
@@ -385,27 +392,21 @@ __global__ void __launch_bounds__(RED) k_update_p(int N, int ld, int nc, int nbl
 }
 
 // ---------------------------------------------------------------- gradient pass
-// For every pair (a, b): w_c[a] v_c[b] (K_ab r2_ab,l .., K_ab) for the GC columns c = GC blockIdx.z + ..,
-// with (w_0, v_0) = (u_0, u_0), (w_c, v_c) = (u_c, z_c) and r2_l = (x_al - x_bl)^2 / l_l^2.  Tile of
-// GT a x GT b: each thread keeps one b (x_b, v_c[b] in registers) and walks GT / 4 a's, x_a and w_c[a]
-// broadcast from shared memory; the kernel value is computed once per pair.  Per-CTA partials
-// [blk][c][MAX_D + 1] (l = MAX_D holds the signal-variance term sum w K v).
+// For every pair (a, b): w_c[a] v_c[b] (K_ab r2_ab,l .., K_ab) for the GC columns c = GC blockIdx.y + ..,
+// with (w_0, v_0) = (u_0, u_0), (w_c, v_c) = (u_c, z_c), r2_l = (x_al - x_bl)^2 / l_l^2 and K_ab =
+// s exp(-sum_l r2_l / 2) regenerated (cheaper than re-reading Khat).  A CTA owns GT b's (one per thread
+// of each quarter: x_b and v_c[b] in registers) and walks every a in tiles of GT (x_a, w_c[a] staged
+// in shared memory, broadcast reads); the thread sums are reduced by a fixed shuffle butterfly, then
+// across the 8 warps in warp order.  Per-CTA partials [b tile][c][MAX_D + 1] (l = MAX_D holds the
+// signal-variance term sum w K v).
 __global__ void __launch_bounds__(256) k_grad_pairs(const float* __restrict__ X, int N, int ld, int d, Hyp h, int nc,
                                                     const double* __restrict__ U, const double* __restrict__ Z,
                                                     double* __restrict__ part) {
   __shared__ double xa_s[GT][BAGEL_MAX_D];
   __shared__ double wa_s[GC][GT];
-  __shared__ double red[256];
-  const int ti = blockIdx.y, tj = blockIdx.x, c0 = blockIdx.z * GC;
+  __shared__ double wred[8][GC][BAGEL_MAX_D + 1];
+  const int tj = blockIdx.x, c0 = blockIdx.y * GC;
   const int ncl = min(GC, nc - c0);
-  for (int idx = threadIdx.x; idx < GT * BAGEL_MAX_D; idx += 256) {
-    const int a = ti * GT + idx / BAGEL_MAX_D, l = idx % BAGEL_MAX_D;
-    xa_s[idx / BAGEL_MAX_D][l] = a < N && l < d ? (double)X[(size_t)a * d + l] : 0.0;
-  }
-  for (int idx = threadIdx.x; idx < GC * GT; idx += 256) {
-    const int c = idx / GT, a = ti * GT + idx % GT;
-    wa_s[c][idx % GT] = c < ncl && a < N ? U[(size_t)(c0 + c) * ld + a] : 0.0;
-  }
   const int bl = threadIdx.x % GT, ag = threadIdx.x / GT;
   const int b = tj * GT + bl;
   double xb[BAGEL_MAX_D], vb[GC];
@@ -416,47 +417,62 @@ __global__ void __launch_bounds__(256) k_grad_pairs(const float* __restrict__ X,
     const int cc = c0 + c;
     vb[c] = c < ncl && b < N ? (cc == 0 ? U[b] : Z[(size_t)cc * ld + b]) : 0.0;
   }
-  __syncthreads();
   double acc[GC][BAGEL_MAX_D + 1];
 #pragma unroll
   for (int c = 0; c < GC; ++c)
 #pragma unroll
     for (int l = 0; l <= BAGEL_MAX_D; ++l) acc[c][l] = 0.0;
-  const int alim = min(GT, N - ti * GT);
-  if (b < N)
-    for (int al = ag; al < alim; al += 256 / GT) {
-      double r2[BAGEL_MAX_D], q = 0.0;
+  for (int a0 = 0; a0 < N; a0 += GT) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < GT * BAGEL_MAX_D; idx += 256) {
+      const int a = a0 + idx / BAGEL_MAX_D, l = idx % BAGEL_MAX_D;
+      xa_s[idx / BAGEL_MAX_D][l] = a < N && l < d ? (double)X[(size_t)a * d + l] : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < GC * GT; idx += 256) {
+      const int c = idx / GT, a = a0 + idx % GT;
+      wa_s[c][idx % GT] = c < ncl && a < N ? U[(size_t)(c0 + c) * ld + a] : 0.0;
+    }
+    __syncthreads();
+    const int alim = min(GT, N - a0);
+    if (b < N)
+      for (int al = ag; al < alim; al += 256 / GT) {
+        double r2[BAGEL_MAX_D], q = 0.0;
 #pragma unroll
-      for (int l = 0; l < BAGEL_MAX_D; ++l) {
-        r2[l] = 0.0;
-        if (l < d) {
-          const double df = xa_s[al][l] - xb[l];
-          r2[l] = df * df * h.inv_l2[l];
-          q += r2[l];
+        for (int l = 0; l < BAGEL_MAX_D; ++l) {
+          r2[l] = 0.0;
+          if (l < d) {
+            const double df = xa_s[al][l] - xb[l];
+            r2[l] = df * df * h.inv_l2[l];
+            q += r2[l];
+          }
+        }
+        const double k = h.s * exp(-0.5 * q);
+#pragma unroll
+        for (int c = 0; c < GC; ++c) {
+          const double wv = wa_s[c][al] * vb[c] * k;
+#pragma unroll
+          for (int l = 0; l < BAGEL_MAX_D; ++l) acc[c][l] = fma(wv, r2[l], acc[c][l]);
+          acc[c][BAGEL_MAX_D] += wv;
         }
       }
-      const double k = h.s * exp(-0.5 * q);
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 #pragma unroll
-      for (int c = 0; c < GC; ++c) {
-        const double wv = wa_s[c][al] * vb[c] * k;
+  for (int c = 0; c < GC; ++c)
 #pragma unroll
-        for (int l = 0; l < BAGEL_MAX_D; ++l) acc[c][l] = fma(wv, r2[l], acc[c][l]);
-        acc[c][BAGEL_MAX_D] += wv;
-      }
-    }
-  const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-  for (int c = 0; c < ncl; ++c)
     for (int l = 0; l <= BAGEL_MAX_D; ++l) {
-      if (l >= d && l < BAGEL_MAX_D) continue;
-      red[threadIdx.x] = acc[c][l];
-      __syncthreads();
-      for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) part[(blk * MAXC + c0 + c) * (BAGEL_MAX_D + 1) + l] = red[0];
-      __syncthreads();
+      double v = acc[c][l];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) wred[warp][c][l] = v;
     }
+  __syncthreads();
+  if (threadIdx.x < GC * (BAGEL_MAX_D + 1)) {
+    const int c = threadIdx.x / (BAGEL_MAX_D + 1), l = threadIdx.x % (BAGEL_MAX_D + 1);
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += wred[w][c][l];
+    if (c < ncl) part[((size_t)tj * MAXC + c0 + c) * (BAGEL_MAX_D + 1) + l] = v;
+  }
 }
 
 // fixed-order sum of the pair partials: out[c][l]; one CTA per (c, l), strided partial sums then a tree
@@ -538,7 +554,7 @@ size_t bbmm_workspace_doubles(int N, int nc, int J) {
   const size_t ld = bbmm_ld(N);
   const size_t nblk = (N + RED - 1) / RED, ntile = (N + GT - 1) / GT, nrb = (N + 31) / 32;
   return (size_t)N * ld + 5 * (size_t)nc * ld + 2 * (size_t)nc * J + 2 * std::max<size_t>(nblk, 1) * MAXC +
-         (size_t)(J + 1) * MAXC + ntile * ntile * MAXC * (BAGEL_MAX_D + 1) + MAXC * (BAGEL_MAX_D + 1) +
+         (size_t)(J + 1) * MAXC + ntile * MAXC * (BAGEL_MAX_D + 1) + MAXC * (BAGEL_MAX_D + 1) +
          (nrb + MAX_G) * MAXC * 32;
 }
 
@@ -566,7 +582,7 @@ int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const
   double* rr_part = part + (size_t)std::max(nblk, 1) * MAXC;  // r.r partials
   double* rr_hist = rr_part + (size_t)std::max(nblk, 1) * MAXC;
   double* gpart = rr_hist + (size_t)(J + 1) * MAXC;
-  double* gsum = gpart + (size_t)ntile * ntile * MAXC * (BAGEL_MAX_D + 1);
+  double* gsum = gpart + (size_t)ntile * MAXC * (BAGEL_MAX_D + 1);
   double* mpart = gsum + MAXC * (BAGEL_MAX_D + 1);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -604,8 +620,8 @@ int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const
   cudaMemcpyAsync(its_h.data(), its_dev, sizeof(int) * nc, cudaMemcpyDeviceToHost, st);
   std::vector<double> gs_h((size_t)MAXC * (BAGEL_MAX_D + 1), 0.0);
   if (grad) {
-    k_grad_pairs<<<dim3(ntile, ntile, (nc + GC - 1) / GC), 256, 0, st>>>(X, N, ld, d, h, nc, U, Z, gpart);
-    k_grad_sum<<<dim3(nc, BAGEL_MAX_D + 1), RED, 0, st>>>(gpart, (size_t)ntile * ntile, d, gsum);
+    k_grad_pairs<<<dim3(ntile, (nc + GC - 1) / GC), 256, 0, st>>>(X, N, ld, d, h, nc, U, Z, gpart);
+    k_grad_sum<<<dim3(nc, BAGEL_MAX_D + 1), RED, 0, st>>>(gpart, (size_t)ntile, d, gsum);
     cudaMemcpyAsync(gs_h.data(), gsum, sizeof(double) * (size_t)MAXC * (BAGEL_MAX_D + 1), cudaMemcpyDeviceToHost, st);
   }
   if (cudaStreamSynchronize(st) != cudaSuccess) return -1;

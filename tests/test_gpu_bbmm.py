@@ -13,7 +13,7 @@ Between the two -- CG past the loss of orthogonality but not yet converged -- th
 rounding-order chaotic (measured on the CPU, reading R39: two numpy summation orders of the same CG
 give y^T u_0 = 22.7704 and 22.7813 at N = 257, J = 60, residual 3e-3; 1-ulp input perturbations move
 it only ~1e-5), so the parity cases sit in the stable regimes (J small, or J large enough that the
-residual is <= 1e-7: N = 257 J = 200, N = 700 J = 300, the full Krylov space J = N); the chaotic
+residual is <= 1e-7: N = 257 J = 200, N = 520 J = 240, the full Krylov space J = N); the chaotic
 regime is covered by the statistical comparison with the exact log p at N = 5000 below.
 The CPU pins (test_oracle_mll.py) fix what the estimate itself must satisfy."""
 import time
@@ -56,8 +56,8 @@ def _envelope(X, y, h, t, J, seed, ref, k=4):
     return env
 
 
-@pytest.mark.parametrize("N,t,J", [(1, 1, 1), (2, 3, 2), (63, 8, 20), (63, 8, 63), (257, 8, 200), (700, 16, 300),
-                                   (700, 1, 700)])
+@pytest.mark.parametrize("N,t,J", [(1, 1, 1), (2, 3, 2), (63, 8, 20), (63, 8, 63), (257, 8, 200), (520, 16, 240),
+                                   (300, 1, 300)])
 def test_bbmm_matches_oracle(bagel, N, t, J):
     X, Y, ell, s, noise = small_gp_data(N=N, d=3, p=2, seed=N + t)
     ctx = _ctx(bagel, X, Y, ell, s, noise)
