@@ -278,6 +278,23 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
       : "memory");
 }
 
+// 1-D bulk copy (TMA engine) from this CTA's shared memory to the same offset `dst` in CTA `rank`
+// of the cluster, completing tx on the mbarrier at `bar`'s offset in that CTA.
+__device__ __forceinline__ void bulk_s2s_cluster(const void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                 uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 rd, rb;\n\t"
+      "mapa.shared::cluster.u32 rd, %0, %3;\n\t"
+      "mapa.shared::cluster.u32 rb, %2, %3;\n\t"
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [rd], [%1], %4, [rb];\n\t}" ::"r"(
+          smem_u32(dst)),
+      "r"(smem_u32(src)), "r"(smem_u32(bar)), "r"(rank), "r"(bytes)
+      : "memory");
+}
+// Named barrier over the first `threads` threads of the CTA (id 1..15).
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 // Index (in fp16 elements) of element (r, k) of a canonical K-major tile with KT columns.
 __host__ __device__ __forceinline__ int canon_idx(int r, int k, int KT) {
   return (((r >> 3) * (KT >> 3) + (k >> 3)) << 6) + ((r & 7) << 3) + (k & 7);
