@@ -92,6 +92,13 @@ def lib():
             L.orc_mll_bbmm.restype = C.c_int
             L.orc_bbmm_probe.argtypes = [C.c_uint64, C.c_int, C.c_int]
             L.orc_bbmm_probe.restype = C.c_double
+            L.orc_mll_bbmm_pc.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp,
+                                          _dp, _dp, _dp, C.POINTER(C.c_int)]
+            L.orc_mll_bbmm_pc.restype = C.c_int
+            L.orc_bbmm_gauss.argtypes = [C.c_uint64, C.c_int, C.c_int]
+            L.orc_bbmm_gauss.restype = C.c_double
+            L.orc_pivoted_cholesky.argtypes = [_dp, C.c_int, C.c_int, _dp, C.POINTER(C.c_int)]
+            L.orc_pivoted_cholesky.restype = C.c_int
             L.orc_num_threads.restype = C.c_int
             L.orc_set_num_threads.argtypes = [C.c_int]
             _lib = L
@@ -297,6 +304,37 @@ def log_marginal_likelihood_bbmm(X, y, log_hyp, n_probes, n_iter, seed, want_gra
     if rc != 0:
         raise MemoryError("oracle BBMM: allocation failed")
     return val.value, g, ld.value, qd.value
+
+
+def log_marginal_likelihood_bbmm_pc(X, y, log_hyp, n_probes, n_iter, precond_rank, seed, want_grad=True):
+    """BBMM with GPyTorch's rank-k pivoted-Cholesky preconditioner (reading R40): probes z ~ N(0, P),
+    preconditioned CG of exactly n_iter iterations, log|P| + SLQ log-det, Hutchinson trace with P^-1 z.
+    precond_rank 0 is log_marginal_likelihood_bbmm.  Returns (mll, grad or None, logdet, y^T u_0, rank)."""
+    X, y, h = _d(X), _d(y).reshape(-1), _d(log_hyp).reshape(-1)
+    N, d = X.shape
+    assert h.shape == (d + 2,) and y.shape == (N,)
+    val, ld, qd, rk = C.c_double(0.0), C.c_double(0.0), C.c_double(0.0), C.c_int(0)
+    g = np.zeros(d + 2) if want_grad else None
+    rc = lib().orc_mll_bbmm_pc(_ptr(X), N, d, _ptr(y), _ptr(h), int(n_probes), int(n_iter), int(precond_rank),
+                               int(seed), C.byref(val), _ptr(g), C.byref(ld), C.byref(qd), C.byref(rk))
+    if rc != 0:
+        raise ArithmeticError(f"oracle preconditioned BBMM failed ({rc})")
+    return val.value, g, ld.value, qd.value, rk.value
+
+
+def pivoted_cholesky(Kf, k):
+    """(L (N x rank), pivots) of the oracle's greedy pivoted Cholesky of a PSD matrix (reading R40)."""
+    Kf = _d(Kf)
+    N = Kf.shape[0]
+    L = np.zeros((N, k))
+    piv = (C.c_int * k)()
+    r = lib().orc_pivoted_cholesky(_ptr(Kf), N, int(k), _ptr(L), piv)
+    return L[:, :r], np.array(piv[:r])
+
+
+def bbmm_gauss(seed, i, j) -> float:
+    """Gaussian g_i[j] of the preconditioned probes (Philox, Box-Muller, reading R40)."""
+    return lib().orc_bbmm_gauss(int(seed), int(i), int(j))
 
 
 def bbmm_probes(seed, n_probes, N) -> np.ndarray:

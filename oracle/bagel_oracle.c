@@ -1067,3 +1067,256 @@ int orc_mll_bbmm(const double* X, int N, int d, const double* y, const double* l
     free(ta); free(tb); free(its); free(be); free(al); free(Q); free(P); free(Rr); free(U); free(Z); free(K);
     return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-1 at large N with GPyTorch's preconditioner (reading R40):     */
+/* BBMM with a rank-k pivoted-Cholesky preconditioner [gardner2018],    */
+/*   K_f ~ L L^T (k greedy pivots of the noise-free kernel matrix:     */
+/*     d_n = K_f[n][n]; per step m: pivot pi = argmax over the unpivoted */
+/*     n of d_n (lowest index on ties); L[n][m] = (K_f[n][pi] -          */
+/*     sum_{j<m} L[n][j] L[pi][j]) / sqrt(d_pi); d_n -= L[n][m]^2;       */
+/*     stop early once max d_n <= 0),                                    */
+/*   P = L L^T + sn2 I, applied as P^-1 v = (v - L C^-1 L^T v) / sn2,     */
+/*   C = sn2 I_k + L^T L (Woodbury), log|P| = log|C| + (N - k) log sn2;  */
+/* probes z_i = L g_i[0..k) + sqrt(sn2) g_i[k..k+N) ~ N(0, P), g from     */
+/* Philox (key = seed, ctr = (i, j >> 2, 0x4242424E, 5), Box-Muller word  */
+/* j & 3, fp64); preconditioned CG (exactly J iterations; a column stops  */
+/* once r^T P^-1 r is exactly 0) on [y z_1 .. z_t]; each probe's PCG      */
+/* coefficients give the Lanczos tridiagonal T_i of P^-1/2 Khat P^-1/2,   */
+/*   log|Khat| ~ log|P| + (1/t) sum_i (z_i^T P^-1 z_i) e1^T log(T_i) e1,  */
+/*   tr(Khat^-1 dK) ~ (1/t) sum_i u_i^T dK (P^-1 z_i),                    */
+/* quadratic term y^T u_0.  k = 0 is orc_mll_bbmm exactly.              */
+/* ------------------------------------------------------------------ */
+double orc_bbmm_gauss(uint64_t seed, int i, int j)
+{
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {(uint32_t)i, (uint32_t)(j >> 2), 0x4242424Eu, 5u};
+    uint32_t o[4];
+    double e[4];
+    orc_philox4x32_10(ctr, key, o);
+    orc_box_muller4(o, e);
+    return e[j & 3];
+}
+
+/* rank-k pivoted Cholesky of K_f (row-major N x N); L is N x k row-major (L[n*k + m]); returns the
+ * rank reached (<= k) */
+int orc_pivoted_cholesky(const double* Kf, int N, int k, double* L, int* piv)
+{
+    double* dg = (double*)malloc(sizeof(double) * N);
+    char* used = (char*)calloc(N, 1);
+    for (int n = 0; n < N; ++n) dg[n] = Kf[(size_t)n * N + n];
+    memset(L, 0, sizeof(double) * (size_t)N * k);
+    int m = 0;
+    for (; m < k; ++m) {
+        int p = -1;
+        for (int n = 0; n < N; ++n)
+            if (!used[n] && (p < 0 || dg[n] > dg[p])) p = n;
+        if (p < 0 || !(dg[p] > 0.0)) break;
+        used[p] = 1;
+        piv[m] = p;
+        const double sq = sqrt(dg[p]);
+        for (int n = 0; n < N; ++n) {
+            double v = Kf[(size_t)n * N + p];
+            for (int j = 0; j < m; ++j) v -= L[(size_t)n * k + j] * L[(size_t)p * k + j];
+            L[(size_t)n * k + m] = v / sq;
+        }
+        for (int n = 0; n < N; ++n) dg[n] -= L[(size_t)n * k + m] * L[(size_t)n * k + m];
+    }
+    free(dg);
+    free(used);
+    return m;
+}
+
+/* in-place Cholesky of a k x k SPD matrix (lower), returns 0 or pivot+1 */
+static int orc_chol_small(double* A, int k)
+{
+    for (int j = 0; j < k; ++j) {
+        double s = A[(size_t)j * k + j];
+        for (int m = 0; m < j; ++m) s -= A[(size_t)j * k + m] * A[(size_t)j * k + m];
+        if (!(s > 0.0)) return j + 1;
+        A[(size_t)j * k + j] = sqrt(s);
+        for (int i = j + 1; i < k; ++i) {
+            double v = A[(size_t)i * k + j];
+            for (int m = 0; m < j; ++m) v -= A[(size_t)i * k + m] * A[(size_t)j * k + m];
+            A[(size_t)i * k + j] = v / A[(size_t)j * k + j];
+        }
+    }
+    return 0;
+}
+
+/* w = P^-1 v = (v - L C^-1 L^T v) / sn2 with C = R R^T (R lower, k x k) */
+static void orc_precond_apply(const double* L, const double* R, int N, int k, double sn2, const double* v, double* w,
+                              double* tmp)
+{
+    for (int m = 0; m < k; ++m) {
+        double a = 0.0;
+        for (int n = 0; n < N; ++n) a += L[(size_t)n * k + m] * v[n];
+        tmp[m] = a;
+    }
+    for (int i = 0; i < k; ++i) { /* R x = tmp */
+        double a = tmp[i];
+        for (int m = 0; m < i; ++m) a -= R[(size_t)i * k + m] * tmp[m];
+        tmp[i] = a / R[(size_t)i * k + i];
+    }
+    for (int i = k - 1; i >= 0; --i) { /* R^T y = x */
+        double a = tmp[i];
+        for (int m = i + 1; m < k; ++m) a -= R[(size_t)m * k + i] * tmp[m];
+        tmp[i] = a / R[(size_t)i * k + i];
+    }
+    for (int n = 0; n < N; ++n) {
+        double a = v[n];
+        for (int m = 0; m < k; ++m) a -= L[(size_t)n * k + m] * tmp[m];
+        w[n] = a / sn2;
+    }
+}
+
+int orc_mll_bbmm_pc(const double* X, int N, int d, const double* y, const double* log_hyp, int t, int J, int kp,
+                    uint64_t seed, double* mll, double* grad, double* logdet_out, double* quad_out, int* rank_out)
+{
+    if (kp <= 0) {
+        if (rank_out) *rank_out = 0;
+        return orc_mll_bbmm(X, N, d, y, log_hyp, t, J, seed, mll, grad, logdet_out, quad_out);
+    }
+    double ell[16];
+    for (int c = 0; c < d; ++c) ell[c] = exp(log_hyp[c]);
+    double s = exp(log_hyp[d]), sn2 = exp(log_hyp[d + 1]);
+    double* K = orc_khat(X, N, d, ell, s, sn2);
+    if (!K) return -1;
+    /* pivoted Cholesky of K_f = Khat - sn2 I */
+    double* Kf = (double*)malloc(sizeof(double) * (size_t)N * N);
+    memcpy(Kf, K, sizeof(double) * (size_t)N * N);
+    for (int n = 0; n < N; ++n) Kf[(size_t)n * N + n] -= sn2;
+    double* L0 = (double*)malloc(sizeof(double) * (size_t)N * kp);
+    int* piv = (int*)malloc(sizeof(int) * kp);
+    const int k = orc_pivoted_cholesky(Kf, N, kp, L0, piv);
+    free(Kf);
+    /* compact L to N x k, C = sn2 I + L^T L, R = chol(C), log|P| */
+    double* L = (double*)malloc(sizeof(double) * (size_t)N * (k > 0 ? k : 1));
+    for (int n = 0; n < N; ++n)
+        for (int m = 0; m < k; ++m) L[(size_t)n * k + m] = L0[(size_t)n * kp + m];
+    free(L0);
+    double* R = (double*)calloc((size_t)(k > 0 ? k * k : 1), sizeof(double));
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) {
+            double a = (i == j) ? sn2 : 0.0;
+            for (int n = 0; n < N; ++n) a += L[(size_t)n * k + i] * L[(size_t)n * k + j];
+            R[(size_t)i * k + j] = a;
+        }
+    if (orc_chol_small(R, k) != 0) return -2;
+    double logdetP = (double)(N - k) * log(sn2);
+    for (int i = 0; i < k; ++i) logdetP += 2.0 * log(R[(size_t)i * k + i]);
+    const int nc = t + 1;
+    double* Z = (double*)malloc(sizeof(double) * (size_t)nc * N);  /* rhs: y, z_1..z_t */
+    double* W0 = (double*)malloc(sizeof(double) * (size_t)nc * N); /* P^-1 rhs */
+    double* U = (double*)calloc((size_t)nc * N, sizeof(double));
+    double* Rr = (double*)malloc(sizeof(double) * (size_t)N);
+    double* Wv = (double*)malloc(sizeof(double) * (size_t)N);
+    double* Pp = (double*)malloc(sizeof(double) * (size_t)N);
+    double* Q = (double*)malloc(sizeof(double) * (size_t)N);
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)(k > 0 ? k : 1));
+    double* al = (double*)malloc(sizeof(double) * (size_t)nc * J);
+    double* be = (double*)malloc(sizeof(double) * (size_t)nc * J);
+    double* nz = (double*)malloc(sizeof(double) * nc);
+    int* its = (int*)malloc(sizeof(int) * nc);
+    for (int n = 0; n < N; ++n) Z[n] = y[n];
+    for (int i = 1; i <= t; ++i)
+        for (int n = 0; n < N; ++n) {
+            double v = sqrt(sn2) * orc_bbmm_gauss(seed, i - 1, k + n);
+            for (int m = 0; m < k; ++m) v += L[(size_t)n * k + m] * orc_bbmm_gauss(seed, i - 1, m);
+            Z[(size_t)i * N + n] = v;
+        }
+    for (int c = 0; c < nc; ++c) {
+        const double* b = Z + (size_t)c * N;
+        double* u = U + (size_t)c * N;
+        double* w0 = W0 + (size_t)c * N;
+        for (int n = 0; n < N; ++n) Rr[n] = b[n];
+        orc_precond_apply(L, R, N, k, sn2, Rr, w0, tmp);
+        double rz = 0.0;
+        for (int n = 0; n < N; ++n) {
+            Pp[n] = w0[n];
+            rz += Rr[n] * w0[n];
+        }
+        nz[c] = rz;
+        its[c] = 0;
+        for (int j = 0; j < J && rz > 0.0; ++j) {
+#pragma omp parallel for schedule(static)
+            for (int a = 0; a < N; ++a) {
+                double acc = 0.0;
+                for (int n = 0; n < N; ++n) acc += K[(size_t)a * N + n] * Pp[n];
+                Q[a] = acc;
+            }
+            double pq = 0.0;
+            for (int n = 0; n < N; ++n) pq += Pp[n] * Q[n];
+            const double alpha = rz / pq;
+            for (int n = 0; n < N; ++n) {
+                u[n] += alpha * Pp[n];
+                Rr[n] -= alpha * Q[n];
+            }
+            orc_precond_apply(L, R, N, k, sn2, Rr, Wv, tmp);
+            double rz2 = 0.0;
+            for (int n = 0; n < N; ++n) rz2 += Rr[n] * Wv[n];
+            const double beta = rz2 / rz;
+            for (int n = 0; n < N; ++n) Pp[n] = Wv[n] + beta * Pp[n];
+            al[(size_t)c * J + j] = alpha;
+            be[(size_t)c * J + j] = beta;
+            rz = rz2;
+            its[c] = j + 1;
+        }
+    }
+    double logdet = 0.0;
+    double* ta = (double*)malloc(sizeof(double) * J);
+    double* tb = (double*)malloc(sizeof(double) * J);
+    for (int i = 1; i <= t; ++i) {
+        const int n = its[i];
+        const double* a_ = al + (size_t)i * J;
+        const double* b_ = be + (size_t)i * J;
+        for (int j = 0; j < n; ++j) {
+            ta[j] = 1.0 / a_[j] + (j > 0 ? b_[j - 1] / a_[j - 1] : 0.0);
+            if (j + 1 < n) tb[j] = sqrt(b_[j]) / a_[j];
+        }
+        logdet += nz[i] * orc_tridiag_e1_log_e1(ta, tb, n);
+    }
+    logdet = logdetP + logdet / (double)t;
+    double quad = 0.0;
+    for (int n = 0; n < N; ++n) quad += y[n] * U[n];
+    *mll = -0.5 * quad - 0.5 * logdet - 0.5 * N * log(2.0 * 3.14159265358979323846);
+    if (logdet_out) *logdet_out = logdet;
+    if (quad_out) *quad_out = quad;
+    if (rank_out) *rank_out = k;
+    if (grad) {
+        for (int jp = 0; jp < d + 2; ++jp) {
+            /* w^T dK_jp v for (w, v) = (u_0, u_0) and (u_i, P^-1 z_i) */
+            double q0 = 0.0, tr = 0.0;
+            for (int c = 0; c < nc; ++c) {
+                const double* w = U + (size_t)c * N;
+                const double* v = c == 0 ? U : W0 + (size_t)c * N;
+#pragma omp parallel for schedule(static)
+                for (int a = 0; a < N; ++a) {
+                    double row = 0.0;
+                    for (int b2 = 0; b2 < N; ++b2) {
+                        double dk;
+                        if (jp < d) {
+                            double diff = X[(size_t)a * d + jp] - X[(size_t)b2 * d + jp];
+                            dk = orc_kernel(X + (size_t)a * d, X + (size_t)b2 * d, d, ell, s) * diff * diff /
+                                 (ell[jp] * ell[jp]);
+                        } else if (jp == d) {
+                            dk = orc_kernel(X + (size_t)a * d, X + (size_t)b2 * d, d, ell, s);
+                        } else {
+                            dk = (a == b2) ? sn2 : 0.0;
+                        }
+                        row += dk * v[b2];
+                    }
+                    Q[a] = w[a] * row;
+                }
+                double acc = 0.0;
+                for (int a = 0; a < N; ++a) acc += Q[a];
+                if (c == 0) q0 = acc;
+                else tr += acc;
+            }
+            grad[jp] = 0.5 * q0 - 0.5 * tr / (double)t;
+        }
+    }
+    free(ta); free(tb); free(its); free(nz); free(be); free(al); free(tmp); free(Q); free(Pp); free(Wv); free(Rr);
+    free(U); free(W0); free(Z); free(R); free(L); free(piv); free(K);
+    return 0;
+}

@@ -171,3 +171,106 @@ def test_bbmm_fixed_iterations_and_thread_count_independent():
     finally:
         O.set_num_threads(n0)
     assert r1[0] == r2[0] and np.array_equal(r1[1], r2[1])
+
+
+# ------------------------------------------------------------ preconditioned BBMM (reading R40)
+def test_pivoted_cholesky_nystrom_properties():
+    """Greedy pivoted Cholesky (Harbrecht et al.; GPyTorch's preconditioner): with equal diagonals the
+    first pivot is index 0 and L[:, 0] = K[:, 0] / sqrt(K_00); L L^T reproduces K exactly on the
+    pivot columns (the Nystrom interpolation property); the residual diagonal is >= 0 and its trace
+    decreases with the rank; at the numerical rank of a smooth kernel L L^T = K."""
+    X, Y, ell, s, noise = small_gp_data(N=40, d=2, p=1, seed=12)
+    Kf = _khat(X, ell[0], float(s[0]), 0.0)
+    L, piv = O.pivoted_cholesky(Kf, 6)
+    assert piv[0] == 0 and len(set(piv)) == len(piv)
+    np.testing.assert_allclose(L[:, 0], Kf[:, 0] / np.sqrt(Kf[0, 0]), rtol=1e-15)
+    np.testing.assert_allclose((L @ L.T)[:, piv], Kf[:, piv], rtol=0, atol=1e-12 * Kf.max())
+    traces = []
+    for k in (1, 3, 6, 12, 24):
+        Lk, _ = O.pivoted_cholesky(Kf, k)
+        res = np.diag(Kf - Lk @ Lk.T)
+        assert res.min() >= -1e-12 * Kf.max()
+        traces.append(res.sum())
+    assert all(a >= b for a, b in zip(traces, traces[1:]))
+    Lf, _ = O.pivoted_cholesky(Kf, 40)
+    assert np.abs(Kf - Lf @ Lf.T).max() <= 1e-8 * Kf.max()
+
+
+def test_bbmm_gauss_is_box_muller_of_philox():
+    """g_i[j] = Box-Muller word j & 3 of Philox4x32-10(key = seed, ctr = (i, j >> 2, 0x4242424E, 5)),
+    uniforms ((o >> 9) + 0.5) 2^-23 (R29)."""
+    for i, j in [(0, 0), (0, 1), (1, 2), (3, 7), (2, 13)]:
+        o = O.philox4x32_10(np.array([i, j >> 2, 0x4242424E, 5], dtype=np.uint32), [0xBEEF, 0])
+        u = ((o >> 9).astype(np.float64) + 0.5) * 2.0 ** -23
+        r0, r1 = np.sqrt(-2 * np.log(u[0])), np.sqrt(-2 * np.log(u[2]))
+        e = [r0 * np.cos(2 * np.pi * u[1]), r0 * np.sin(2 * np.pi * u[1]),
+             r1 * np.cos(2 * np.pi * u[3]), r1 * np.sin(2 * np.pi * u[3])]
+        assert O.bbmm_gauss(0xBEEF, i, j) == pytest.approx(e[j & 3], rel=1e-14, abs=1e-15)
+
+
+def test_bbmm_pc_rank_zero_is_plain_bbmm():
+    X, Y, ell, s, noise = small_gp_data(N=50, d=3, p=1, seed=9)
+    h = np.log(np.r_[ell[0], float(s[0]), float(noise[0])])
+    a = O.log_marginal_likelihood_bbmm(X, Y[:, 0], h, 4, 20, 5)
+    b = O.log_marginal_likelihood_bbmm_pc(X, Y[:, 0], h, 4, 20, 0, 5)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1]) and a[2] == b[2] and b[4] == 0
+
+
+def test_bbmm_pc_full_krylov_is_exact_per_probe():
+    """J = N preconditioned CG: each probe's quadrature is exact for M = P^-1/2 Khat P^-1/2, so
+    logdet = log|P| + (1/t) sum_i w_i^T log(M) w_i with w_i = P^-1/2 z_i, z_i = L g_i[:k] + sn g_i[k:]
+    (numpy eigh of P and M); y^T u_0 = y^T Khat^-1 y; the Hutchinson term = (1/t) sum_i
+    (Khat^-1 z_i)^T dK (P^-1 z_i)."""
+    X, Y, ell, s, noise = small_gp_data(N=24, d=3, p=1, seed=5)
+    y = Y[:, 0]
+    s, sn2 = float(s[0]), 0.05 * float(s[0])
+    t, seed, k = 4, 91, 5
+    h = np.log(np.r_[ell[0], s, sn2])
+    N = len(y)
+    mll, g, logdet, quad, rank = O.log_marginal_likelihood_bbmm_pc(X, y, h, t, N, k, seed)
+    assert rank == k
+    Kh = _khat(X, ell[0], s, sn2)
+    L, _ = O.pivoted_cholesky(Kh - sn2 * np.eye(N), k)
+    P = L @ L.T + sn2 * np.eye(N)
+    lp, Vp = np.linalg.eigh(P)
+    Pm12 = (Vp / np.sqrt(lp)) @ Vp.T
+    lm, Vm = np.linalg.eigh(Pm12 @ Kh @ Pm12)
+    logM = (Vm * np.log(lm)) @ Vm.T
+    Z = np.array([[O.bbmm_gauss(seed, i, j) for j in range(k + N)] for i in range(t)])
+    Zs = np.array([L @ z[:k] + np.sqrt(sn2) * z[k:] for z in Z])
+    ref = np.sum(np.log(lp)) + np.mean([(Pm12 @ z) @ logM @ (Pm12 @ z) for z in Zs])
+    assert logdet == pytest.approx(ref, rel=1e-9)
+    assert quad == pytest.approx(y @ np.linalg.solve(Kh, y), rel=1e-9)
+    a = np.linalg.solve(Kh, y)
+    for j in range(X.shape[1] + 2):
+        D = _dK(X, ell[0], s, sn2, j)
+        tr = np.mean([np.linalg.solve(Kh, z) @ D @ np.linalg.solve(P, z) for z in Zs])
+        assert g[j] == pytest.approx(0.5 * a @ D @ a - 0.5 * tr, rel=1e-8, abs=1e-10 * np.abs(g).max())
+
+
+def test_bbmm_pc_is_unbiased_and_preconditioning_helps():
+    """(a) Many Gaussian probes: the log-det estimate is within 4 s.e. of the exact log|Khat| (Var of
+    w^T A w for w ~ N(0, I) is 2 ||A||_F^2, A = log M); (b) at a short CG run (J = 8) on an
+    ill-conditioned Khat the preconditioned estimate of log p is closer to the exact value than the
+    unpreconditioned one, for each of 3 probe seeds."""
+    X, Y, ell, s, noise = small_gp_data(N=40, d=2, p=1, seed=6)
+    y = Y[:, 0]
+    h = np.log(np.r_[ell[0], float(s[0]), float(noise[0]) * 10])
+    exact_ld = np.linalg.slogdet(_khat(X, ell[0], np.exp(h[2]), np.exp(h[3])))[1]
+    t, k = 400, 4
+    _, _, logdet, _, _ = O.log_marginal_likelihood_bbmm_pc(X, y, h, t, 40, k, 13, want_grad=False)
+    Kh = _khat(X, ell[0], np.exp(h[2]), np.exp(h[3]))
+    L, _ = O.pivoted_cholesky(Kh - np.exp(h[3]) * np.eye(40), k)
+    P = L @ L.T + np.exp(h[3]) * np.eye(40)
+    lp, Vp = np.linalg.eigh(P)
+    Pm12 = (Vp / np.sqrt(lp)) @ Vp.T
+    lm = np.linalg.eigvalsh(Pm12 @ Kh @ Pm12)
+    sd = np.sqrt(2 * np.sum(np.log(lm) ** 2) / t)
+    assert abs(logdet - exact_ld) <= 4 * sd + 1e-9
+    X2, Y2, ell2, s2, noise2 = small_gp_data(N=300, d=2, p=1, seed=14)
+    h2 = np.log(np.r_[ell2[0], float(s2[0]), float(noise2[0])])
+    exact, _ = O.log_marginal_likelihood(X2, Y2[:, 0], h2, want_grad=False)
+    for seed in (1, 2, 3):
+        plain = O.log_marginal_likelihood_bbmm(X2, Y2[:, 0], h2, 4, 8, seed, want_grad=False)[0]
+        pc = O.log_marginal_likelihood_bbmm_pc(X2, Y2[:, 0], h2, 4, 8, 30, seed, want_grad=False)[0]
+        assert abs(pc - exact) < abs(plain - exact), (seed, pc, plain, exact)
