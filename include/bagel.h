@@ -229,17 +229,26 @@ int gp_log_marginal_likelihood(bagel_ctx* ctx, int m, const double* log_hyp, dou
  *   mll = -1/2 y^T u_0 - 1/2 log|Khat| - N/2 log(2 pi);
  *   grad_j = 1/2 u_0^T dK_j u_0 - 1/2 (1/t) sum_i u_i^T dK_j z_i.
  * A column whose residual reaches exactly 0 stops early (its T_i is smaller).
+ * precond_rank k in [0, min(N, 64)]: k > 0 adds GPyTorch's preconditioner (reading
+ * R40): a greedy rank-k pivoted Cholesky L L^T of Khat - sn2 I (pivot = the largest
+ * residual diagonal, lowest index on ties; it stops early at a non-positive
+ * residual), P = L L^T + sn2 I applied by Woodbury; probes become Gaussian,
+ * z_i = L g_i[0..k) + sqrt(sn2) g_i[k..k+N), g_i[j] = Box-Muller word j & 3 of
+ * Philox4x32-10(key = seed, ctr = (i, j >> 2, 0x4242424E, 5)); the CG is
+ * preconditioned, log|Khat| ~ log|P| + (1/t) sum_i (z_i^T P^-1 z_i) e_1^T
+ * log(T_i) e_1 and tr(Khat^-1 dK) ~ (1/t) sum_i u_i^T dK P^-1 z_i.
  *   m, log_hyp, mll, grad  as gp_log_marginal_likelihood.
  *   n_probes t in [1, 16];  n_iter J in [1, min(N, 4096)];  seed  probe stream.
  *   logdet   [host, nullable] receives the log-det estimate.
  * Synchronous.  Cost O(J N^2) for the solves plus O(t N^2 d) for the gradient;
  * workspace N^2 + 5 (t + 1) N float64 (kept for later calls).  Deterministic:
  * every reduction runs in a fixed order.  Does not change the loaded model.
- * Errors: E_STATE without gp_load; E_ARG (m, t, J out of range, non-finite
+ * Errors: E_STATE without gp_load; E_ARG (m, t, J, k out of range, non-finite
  * log_hyp, noise < 1e-8, workspace > 120 GB); E_NUMERIC when the estimate is
- * non-finite (Khat too ill-conditioned for J iterations); E_CUDA. */
+ * non-finite (Khat too ill-conditioned for J iterations) or sn2 I + L^T L is not
+ * positive definite; E_CUDA. */
 int gp_log_marginal_likelihood_bbmm(bagel_ctx* ctx, int m, const double* log_hyp, int n_probes, int n_iter,
-                                    uint64_t seed, double* mll, double* grad, double* logdet);
+                                    int precond_rank, uint64_t seed, double* mll, double* grad, double* logdet);
 
 /* Number of kernel launches the last rollout_cost_and_grad enqueued: launches [host]
  * (the bench's gpu_launches count).  Errors: E_ARG for NULL pointers. */

@@ -88,8 +88,8 @@ def lib() -> C.CDLL:
             L.gp_log_marginal_likelihood.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                                      C.POINTER(C.c_double)]
             L.gp_log_marginal_likelihood_bbmm.argtypes = [_vp, C.c_int, C.POINTER(C.c_double), C.c_int, C.c_int,
-                                                          C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                                          C.POINTER(C.c_double)]
+                                                          C.c_int, C.c_uint64, C.POINTER(C.c_double),
+                                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
             L.policy_adam_step.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_longlong, C.c_float, C.c_float,
                                            C.c_float, C.c_float, C.POINTER(C.c_int)]
             _lib = L
@@ -232,9 +232,10 @@ class Context:
         return val.value, g
 
     def log_marginal_likelihood_bbmm(self, m: int, log_hyp=None, n_probes: int = 8, n_iter: int = 100,
-                                     seed: int = 0, want_grad: bool = True):
-        """BBMM estimate (reading R39) of (log p(y_m | X, phi), d/dphi, log|Khat|): one batched CG of
-        exactly n_iter iterations on [y | z_1 .. z_t] (Rademacher Philox probes), SLQ log-det, Hutchinson trace."""
+                                     seed: int = 0, want_grad: bool = True, precond_rank: int = 0):
+        """BBMM estimate (readings R39 / R40) of (log p(y_m | X, phi), d/dphi, log|Khat|): one batched
+        (preconditioned) CG of exactly n_iter iterations on [y | z_1 .. z_t], SLQ log-det, Hutchinson trace;
+        precond_rank k > 0 adds GPyTorch's rank-k pivoted-Cholesky preconditioner (Gaussian probes)."""
         dp = C.POINTER(C.c_double)
         h = None if log_hyp is None else np.ascontiguousarray(log_hyp, dtype=np.float64)
         if h is not None and h.shape != (self.d + 2,):
@@ -243,7 +244,7 @@ class Context:
         g = np.zeros(self.d + 2) if want_grad else None
         self._check(self.L.gp_log_marginal_likelihood_bbmm(
             self.h, int(m), None if h is None else h.ctypes.data_as(dp), int(n_probes), int(n_iter),
-            int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(val), None if g is None else g.ctypes.data_as(dp), C.byref(ld)))
+            int(precond_rank), int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(val), None if g is None else g.ctypes.data_as(dp), C.byref(ld)))
         return val.value, g, ld.value
 
     # ------------------------------------------------------------ Algorithm 1 around the path

@@ -1116,7 +1116,8 @@ extern "C" int gp_log_marginal_likelihood(bagel_ctx* c, int m, const double* log
 }
 
 extern "C" int gp_log_marginal_likelihood_bbmm(bagel_ctx* c, int m, const double* log_hyp, int n_probes, int n_iter,
-                                               uint64_t seed, double* mll, double* grad, double* logdet) {
+                                               int precond_rank, uint64_t seed, double* mll, double* grad,
+                                               double* logdet) {
   return guarded(c, [&] {
     REQUIRE(c->N > 0, BAGEL_E_STATE, "gp_log_marginal_likelihood_bbmm: no GP loaded (call gp_load first)");
     REQUIRE(m >= 0 && m < c->p, BAGEL_E_ARG, "gp_log_marginal_likelihood_bbmm: output m=%d out of range [0, %d)", m, c->p);
@@ -1126,6 +1127,8 @@ extern "C" int gp_log_marginal_likelihood_bbmm(bagel_ctx* c, int m, const double
     const int N = c->N, d = c->d;
     REQUIRE(n_iter >= 1 && n_iter <= N && n_iter <= 4096, BAGEL_E_ARG,
             "gp_log_marginal_likelihood_bbmm: n_iter=%d not in [1, min(N=%d, 4096)]", n_iter, N);
+    REQUIRE(precond_rank >= 0 && precond_rank <= 64 && precond_rank <= N, BAGEL_E_ARG,
+            "gp_log_marginal_likelihood_bbmm: precond_rank=%d not in [0, min(N=%d, 64)]", precond_rank, N);
     const size_t need = bbmm_workspace_doubles(N, n_probes + 1, n_iter);
     REQUIRE((double)need * 8.0 < 120e9, BAGEL_E_ARG,
             "gp_log_marginal_likelihood_bbmm: N=%d needs %.1f GB of float64 workspace, above the 120 GB limit", N,
@@ -1147,10 +1150,12 @@ extern "C" int gp_log_marginal_likelihood_bbmm(bagel_ctx* c, int m, const double
     }
     if (!c->bbmm_its) dev_alloc(c, c->bbmm_its, 32);
     double ld = 0.0, quad = 0.0;
-    const int rc = bbmm_launch(c->X, c->Y + m, c->p, N, d, h, n_probes, n_iter, seed, c->bbmm_ws, c->bbmm_its, &ld,
-                               &quad, grad, c->stream);
+    int rank = 0;
+    const int rc = bbmm_launch(c->X, c->Y + m, c->p, N, d, h, n_probes, n_iter, precond_rank, seed, c->bbmm_ws,
+                               c->bbmm_its, &ld, &quad, grad, &rank, c->stream);
     CK(cudaGetLastError());
     REQUIRE(rc != -2, BAGEL_E_CUDA, "gp_log_marginal_likelihood_bbmm: cuTensorMapEncodeTiled failed for the Khat tiles");
+    REQUIRE(rc != -3, BAGEL_E_NUMERIC, "gp_log_marginal_likelihood_bbmm: sn2 I + L^T L of the preconditioner is not SPD");
     REQUIRE(rc == 0, BAGEL_E_CUDA, "gp_log_marginal_likelihood_bbmm: stream error");
     REQUIRE(isfinite(ld) && isfinite(quad), BAGEL_E_NUMERIC,
             "gp_log_marginal_likelihood_bbmm: non-finite estimate (log-det %g, quadratic form %g): Khat too "

@@ -293,7 +293,8 @@ int op_adam(float* theta, const float* g, float* m1, float* m2, int n, float lr,
 int mll_part_count(int N);
 size_t bbmm_workspace_doubles(int N, int nc, int J);
 int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const double* log_hyp, int t, int J,
-                uint64_t seed, double* ws, int* its_dev, double* logdet, double* quad, double* grad, cudaStream_t st);
+                int kp, uint64_t seed, double* ws, int* its_dev, double* logdet, double* quad, double* grad,
+                int* rank_out, cudaStream_t st);
 int exact_launch(const float* X, const float* Y, int ystride, int N, int d, const float* ell, float s, float noise,
                  double* K, double* Li, double* alpha, int* pivot_flag, cudaStream_t st);
 int mll_launch(const float* X, const float* Y, int ystride, int N, int d, const double* log_hyp, double* K,

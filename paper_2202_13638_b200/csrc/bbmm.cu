@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(RED) k_update_ur(int N, int ld, int nc, int nb
                                                    int j, int J, const double* __restrict__ P,
                                                    const double* __restrict__ Qv, double* __restrict__ U,
                                                    double* __restrict__ R, double* __restrict__ rr_part) {
+  // rr_part == nullptr (preconditioned CG): no r.r partials, r^T P^-1 r comes from k_apply_w
   __shared__ double alpha_s[MAXC];
   __shared__ double red[RED];
   if (threadIdx.x < nc) {
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(RED) k_update_ur(int N, int ld, int nc, int nb
         R[o] = rv;
       }
     }
+    if (!rr_part) continue;
     red[threadIdx.x] = rv * rv;
     __syncthreads();
     for (int o = RED / 2; o > 0; o >>= 1) {
@@ -358,8 +360,9 @@ __global__ void __launch_bounds__(RED) k_update_ur(int N, int ld, int nc, int nb
   }
 }
 
-// step 2: beta = rr_{j+1} / rr_j, p = r + beta p; CTA 0 records beta, the iteration count and rr_{j+1}
-// (0 when the column stopped, so it stays stopped)
+// step 2: beta = rr_{j+1} / rr_j, p = r + beta p (preconditioned: rr = r^T P^-1 r, R = the
+// preconditioned residual P^-1 r); CTA 0 records beta, the iteration count and rr_{j+1} (0 when the
+// column stopped, so it stays stopped)
 __global__ void __launch_bounds__(RED) k_update_p(int N, int ld, int nc, int nblk, const double* __restrict__ rr_part,
                                                   double* __restrict__ rr_hist, double* __restrict__ be_hist,
                                                   int* __restrict__ its, int j, int J, const double* __restrict__ R,
@@ -388,6 +391,190 @@ __global__ void __launch_bounds__(RED) k_update_p(int N, int ld, int nc, int nbl
   for (int c = 0; c < nc; ++c) {
     const size_t o = (size_t)c * ld + n;
     P[o] = fma(beta_s[c], P[o], R[o]);
+  }
+}
+
+// ---------------------------------------------------------------- preconditioner (reading R40)
+constexpr int KMAX = 64;  // preconditioner rank bound
+
+// greedy pivoted Cholesky of K_f = Khat - sn2 I, step m: the pivot = argmax of the residual diagonal
+// over the unpivoted rows (lowest index on ties), one CTA; stop[0] = 1 (rank m) once it is <= 0
+__global__ void __launch_bounds__(1024) k_pchol_argmax(int N, const double* __restrict__ dg, int* __restrict__ used,
+                                                       int m, int* __restrict__ piv, double* __restrict__ dmax,
+                                                       int* __restrict__ stop) {
+  __shared__ double bv[1024];
+  __shared__ int bi[1024];
+  if (stop[0]) return;
+  double v = 0.0;
+  int idx = -1;
+  for (int n = threadIdx.x; n < N; n += 1024)
+    if (!used[n] && (idx < 0 || dg[n] > v)) {
+      v = dg[n];
+      idx = n;
+    }
+  bv[threadIdx.x] = v;
+  bi[threadIdx.x] = idx;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v2 = bv[threadIdx.x + o];
+      const int i2 = bi[threadIdx.x + o];
+      const int i1 = bi[threadIdx.x];
+      if (i2 >= 0 && (i1 < 0 || v2 > bv[threadIdx.x] || (v2 == bv[threadIdx.x] && i2 < i1))) {
+        bv[threadIdx.x] = v2;
+        bi[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (bi[0] < 0 || !(bv[0] > 0.0)) {
+      stop[0] = 1;
+      stop[1] = m;
+    } else {
+      piv[m] = bi[0];
+      dmax[0] = bv[0];
+      used[bi[0]] = 1;
+      stop[1] = m + 1;
+    }
+  }
+}
+
+// column m: L[m][n] = (K_f[p][n] - sum_{j<m} L[j][n] L[j][p]) / sqrt(d_p); d_n -= L[m][n]^2
+__global__ void k_pchol_col(int N, int ld, const double* __restrict__ K, double sn2, double* __restrict__ L,
+                            double* __restrict__ dg, int m, const int* __restrict__ piv,
+                            const double* __restrict__ dmax, const int* __restrict__ stop) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N || stop[0]) return;
+  const int p = piv[m];
+  double v = K[(size_t)p * ld + n];
+  if (n == p) v -= sn2;
+  for (int j = 0; j < m; ++j) v -= L[(size_t)j * ld + n] * L[(size_t)j * ld + p];
+  const double l = v / sqrt(dmax[0]);
+  L[(size_t)m * ld + n] = l;
+  dg[n] -= l * l;
+}
+
+__global__ void k_pchol_init(int N, int ld, const double* __restrict__ K, double sn2, double* __restrict__ dg,
+                             int* __restrict__ used) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  dg[n] = K[(size_t)n * ld + n] - sn2;
+  used[n] = 0;
+}
+
+// G[i][j] = sum_n L[i][n] L[j][n] (one CTA per pair, fixed-order tree)
+__global__ void __launch_bounds__(RED) k_gram(int N, int ld, int k, const double* __restrict__ L, double* __restrict__ G) {
+  __shared__ double red[RED];
+  const int i = blockIdx.x, j = blockIdx.y;
+  double v = 0.0;
+  for (int n = threadIdx.x; n < N; n += RED) v += L[(size_t)i * ld + n] * L[(size_t)j * ld + n];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = RED / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) G[i * k + j] = red[0];
+}
+
+// Gaussian probes z_i = L g_i[0..k) + sn g_i[k..k+N): g_i[j] = Box-Muller word j & 3 of
+// Philox(key = seed, ctr = (i, j >> 2, 0x4242424E, 5)); column 0 = y
+__device__ __forceinline__ double bbmm_gauss(uint64_t seed, int i, int j) {
+  const uint4 o = bagel_philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(j >> 2), 0x4242424Eu, 5u),
+                                      (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+  return bagel_normal_d(o, j & 3);
+}
+__global__ void k_rhs_pc(const float* __restrict__ Y, int ystride, int N, int ld, int t, int k, uint64_t seed,
+                         const double* __restrict__ L, double sn, double* __restrict__ Z) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  Z[n] = (double)Y[(size_t)n * ystride];
+  for (int i = 0; i < t; ++i) {
+    double v = sn * bbmm_gauss(seed, i, k + n);
+    for (int m = 0; m < k; ++m) v += L[(size_t)m * ld + n] * bbmm_gauss(seed, i, m);
+    Z[(size_t)(i + 1) * ld + n] = v;
+  }
+}
+
+// Woodbury apply W = P^-1 V = (V - L C^-1 L^T V) / sn2 for the nc columns, in three steps.
+// (a) CTA partials of L^T V: part[blk][m][c] (RED rows per CTA: the k_dots partition; per (m, c) a
+//     fixed shuffle butterfly per warp, then the 8 warps in order)
+__global__ void __launch_bounds__(RED) k_lt_part(int N, int ld, int nc, int k, const double* __restrict__ L,
+                                                 const double* __restrict__ V, double* __restrict__ part) {
+  __shared__ double red[RED / 32][MAXC];
+  const int n = blockIdx.x * RED + threadIdx.x, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  double v[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) v[c] = c < nc && n < N ? V[(size_t)c * ld + n] : 0.0;
+  for (int m = 0; m < k; ++m) {
+    const double l = n < N ? L[(size_t)m * ld + n] : 0.0;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      if (c >= nc) break;
+      double x = l * v[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) red[warp][c] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      double x = 0.0;
+      for (int w = 0; w < RED / 32; ++w) x += red[w][threadIdx.x];
+      part[((size_t)blockIdx.x * KMAX + m) * MAXC + threadIdx.x] = x;
+    }
+    __syncthreads();
+  }
+}
+// (b) one CTA: T[m][c] = sum over the CTAs in order; Yk[c][i] = sum_m Cinv[i][m] T[m][c]
+__global__ void __launch_bounds__(1024) k_lt_fin(int nblk, int nc, int k, const double* __restrict__ part,
+                                                 const double* __restrict__ Cinv, double* __restrict__ Yk) {
+  __shared__ double T[KMAX][MAXC];
+  for (int idx = threadIdx.x; idx < k * nc; idx += blockDim.x) {
+    const int m = idx / nc, c = idx % nc;
+    double x = 0.0;
+    for (int b = 0; b < nblk; ++b) x += part[((size_t)b * KMAX + m) * MAXC + c];
+    T[m][c] = x;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < k * nc; idx += blockDim.x) {
+    const int i = idx / nc, c = idx % nc;
+    double x = 0.0;
+    for (int m = 0; m < k; ++m) x += Cinv[i * k + m] * T[m][c];
+    Yk[c * KMAX + i] = x;
+  }
+}
+// (c) W = (V - L Yk) / sn2 (and copies into W2 when given), the CTA partials of V^T W per column
+__global__ void __launch_bounds__(RED) k_apply_w(int N, int ld, int nc, int k, const double* __restrict__ L,
+                                                 const double* __restrict__ Yk, double sn2,
+                                                 const double* __restrict__ V, double* __restrict__ W,
+                                                 double* __restrict__ W2, double* __restrict__ W3,
+                                                 double* __restrict__ rz_part) {
+  __shared__ double red[RED];
+  __shared__ double ys[MAXC][KMAX];
+  for (int idx = threadIdx.x; idx < nc * k; idx += RED) ys[idx / k][idx % k] = Yk[(idx / k) * KMAX + idx % k];
+  __syncthreads();
+  const int n = blockIdx.x * RED + threadIdx.x;
+  for (int c = 0; c < nc; ++c) {
+    double x = 0.0;
+    if (n < N) {
+      const size_t o = (size_t)c * ld + n;
+      double a = V[o];
+      for (int m = 0; m < k; ++m) a -= L[(size_t)m * ld + n] * ys[c][m];
+      const double w = a / sn2;
+      W[o] = w;
+      if (W2) W2[o] = w;
+      if (W3) W3[o] = w;
+      x = V[o] * w;
+    }
+    red[threadIdx.x] = x;
+    __syncthreads();
+    for (int o = RED / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) rz_part[(size_t)blockIdx.x * MAXC + c] = red[0];
+    __syncthreads();
   }
 }
 
@@ -553,15 +740,56 @@ constexpr int MAX_G = 1024;  // bound on the MVM grid (SM count) for the partial
 size_t bbmm_workspace_doubles(int N, int nc, int J) {
   const size_t ld = bbmm_ld(N);
   const size_t nblk = (N + RED - 1) / RED, ntile = (N + GT - 1) / GT, nrb = (N + 31) / 32;
-  return (size_t)N * ld + 5 * (size_t)nc * ld + 2 * (size_t)nc * J + 2 * std::max<size_t>(nblk, 1) * MAXC +
+  return (size_t)N * ld + 7 * (size_t)nc * ld + 2 * (size_t)nc * J + 2 * std::max<size_t>(nblk, 1) * MAXC +
          (size_t)(J + 1) * MAXC + ntile * MAXC * (BAGEL_MAX_D + 1) + MAXC * (BAGEL_MAX_D + 1) +
-         (nrb + MAX_G) * MAXC * 32;
+         (nrb + MAX_G) * MAXC * 32 +
+         /* preconditioner: L, residual diagonal, pivot flags, L^T V partials, Yk, C^-1, pivots */
+         (size_t)KMAX * ld + 2 * ld + std::max<size_t>(nblk, 1) * KMAX * MAXC + MAXC * KMAX + KMAX * KMAX +
+         2 * KMAX + 8;
+}
+
+// Cholesky (lower, in place) and inverse of the k x k matrix C = sn2 I + L^T L (host, k <= 64);
+// returns log|C| or NaN if C is not positive definite.
+static double small_spd_inverse(std::vector<double>& C, int k, std::vector<double>& Cinv) {
+  double ld = 0.0;
+  for (int j = 0; j < k; ++j) {
+    double a = C[(size_t)j * k + j];
+    for (int m = 0; m < j; ++m) a -= C[(size_t)j * k + m] * C[(size_t)j * k + m];
+    if (!(a > 0.0)) return NAN;
+    const double r = sqrt(a);
+    C[(size_t)j * k + j] = r;
+    ld += 2.0 * log(r);
+    for (int i = j + 1; i < k; ++i) {
+      double v = C[(size_t)i * k + j];
+      for (int m = 0; m < j; ++m) v -= C[(size_t)i * k + m] * C[(size_t)j * k + m];
+      C[(size_t)i * k + j] = v / r;
+    }
+  }
+  Cinv.assign((size_t)k * k, 0.0);
+  std::vector<double> e(k);
+  for (int col = 0; col < k; ++col) {  // C^-1 e_col by forward / back substitution
+    for (int i = 0; i < k; ++i) {
+      double v = i == col ? 1.0 : 0.0;
+      for (int m = 0; m < i; ++m) v -= C[(size_t)i * k + m] * e[m];
+      e[i] = v / C[(size_t)i * k + i];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double v = e[i];
+      for (int m = i + 1; m < k; ++m) v -= C[(size_t)m * k + i] * e[m];
+      e[i] = v / C[(size_t)i * k + i];
+    }
+    for (int i = 0; i < k; ++i) Cinv[(size_t)i * k + col] = e[i];
+  }
+  return ld;
 }
 
 // Runs the BBMM estimate on the stream and returns it on the host: logdet, quad (y^T u_0) and, when
-// grad is non-NULL, d mll / d phi (d + 2).  ws: bbmm_workspace_doubles(N, t + 1, J) doubles; its: nc ints.
+// grad is non-NULL, d mll / d phi (d + 2).  kp > 0: GPyTorch's rank-kp pivoted-Cholesky preconditioner
+// (reading R40); *rank_out = the rank reached.  ws: bbmm_workspace_doubles(N, t + 1, J) doubles;
+// its: nc ints.
 int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const double* log_hyp, int t, int J,
-                uint64_t seed, double* ws, int* its_dev, double* logdet, double* quad, double* grad, cudaStream_t st) {
+                int kp, uint64_t seed, double* ws, int* its_dev, double* logdet, double* quad, double* grad,
+                int* rank_out, cudaStream_t st) {
   const int nc = t + 1;
   Hyp h{};
   for (int c = 0; c < d; ++c) h.inv_l2[c] = exp(-2.0 * log_hyp[c]);
@@ -576,14 +804,25 @@ int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const
   double* R = U + (size_t)nc * ld;
   double* P = R + (size_t)nc * ld;
   double* Qv = P + (size_t)nc * ld;
-  double* al = Qv + (size_t)nc * ld;
+  double* W = Qv + (size_t)nc * ld;   // preconditioned residual P^-1 r
+  double* W0 = W + (size_t)nc * ld;   // P^-1 rhs (the gradient's second vectors)
+  double* al = W0 + (size_t)nc * ld;
   double* be = al + (size_t)nc * J;
   double* part = be + (size_t)nc * J;                       // p.q partials / general dot partials
-  double* rr_part = part + (size_t)std::max(nblk, 1) * MAXC;  // r.r partials
+  double* rr_part = part + (size_t)std::max(nblk, 1) * MAXC;  // r.r (r^T P^-1 r) partials
   double* rr_hist = rr_part + (size_t)std::max(nblk, 1) * MAXC;
   double* gpart = rr_hist + (size_t)(J + 1) * MAXC;
   double* gsum = gpart + (size_t)ntile * MAXC * (BAGEL_MAX_D + 1);
   double* mpart = gsum + MAXC * (BAGEL_MAX_D + 1);
+  double* Lp = mpart + ((size_t)(N + 31) / 32 + MAX_G) * MAXC * 32;
+  double* dg = Lp + (size_t)KMAX * ld;
+  int* used = reinterpret_cast<int*>(dg + ld);
+  double* ltp = dg + 2 * (size_t)ld;
+  double* Yk = ltp + (size_t)std::max(nblk, 1) * KMAX * MAXC;
+  double* Cinv_d = Yk + MAXC * KMAX;
+  double* dmax = Cinv_d + KMAX * KMAX;
+  int* piv = reinterpret_cast<int*>(dmax + 1);   // KMAX ints
+  int* stop = piv + KMAX;                        // [stop, rank]
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -591,25 +830,68 @@ int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const
 
   k_khat<<<dim3(ld / 256, N), 256, 0, st>>>(X, N, ld, d, h, K);
   const MvmFn mvm = mvm_fn(nc);
-  cudaMemsetAsync(Z, 0, sizeof(double) * 5 * (size_t)nc * ld, st);  // Z U R P Q, pads stay 0
-  k_rhs<<<(N + 255) / 256, 256, 0, st>>>(Y, ystride, N, ld, t, seed, Z);
-  cudaMemcpyAsync(R, Z, sizeof(double) * (size_t)nc * ld, cudaMemcpyDeviceToDevice, st);
-  cudaMemcpyAsync(P, Z, sizeof(double) * (size_t)nc * ld, cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(Z, 0, sizeof(double) * 7 * (size_t)nc * ld, st);  // Z U R P Q W W0, pads stay 0
   cudaMemsetAsync(its_dev, 0, sizeof(int) * nc, st);
-  // rr_0 = r.r (fixed order: CTA partials, then CTA order on the host)
-  k_dots<<<nblk, RED, 0, st>>>(R, R, N, ld, nc, part);
+  int k = 0;
+  double logdetP = 0.0;
+  std::vector<double> rr0(MAXC, 0.0);
   std::vector<double> part_h((size_t)nblk * MAXC);
+  if (kp > 0) {
+    // rank-kp pivoted Cholesky of K_f (2 launches per pivot), then C = sn2 I + L^T L on the host
+    cudaMemsetAsync(stop, 0, 2 * sizeof(int), st);
+    k_pchol_init<<<(N + 255) / 256, 256, 0, st>>>(N, ld, K, h.noise, dg, used);
+    for (int m = 0; m < kp; ++m) {
+      k_pchol_argmax<<<1, 1024, 0, st>>>(N, dg, used, m, piv, dmax, stop);
+      k_pchol_col<<<(N + 255) / 256, 256, 0, st>>>(N, ld, K, h.noise, Lp, dg, m, piv, dmax, stop);
+    }
+    int stop_h[2] = {0, 0};
+    cudaMemcpyAsync(stop_h, stop, sizeof(stop_h), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+    k = stop_h[1];
+    if (k > 0) {
+      k_gram<<<dim3(k, k), RED, 0, st>>>(N, ld, k, Lp, Cinv_d);  // L^T L, staged in the C^-1 slot
+      std::vector<double> C((size_t)k * k), Ci;
+      cudaMemcpyAsync(C.data(), Cinv_d, sizeof(double) * (size_t)k * k, cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+      for (int i = 0; i < k; ++i) C[(size_t)i * k + i] += h.noise;
+      const double ldC = small_spd_inverse(C, k, Ci);
+      if (!(ldC == ldC)) return -3;
+      logdetP = ldC;
+      cudaMemcpyAsync(Cinv_d, Ci.data(), sizeof(double) * (size_t)k * k, cudaMemcpyHostToDevice, st);
+    }
+    logdetP += (double)(N - k) * log(h.noise);
+    // Gaussian probes z ~ N(0, P); W0 = P^-1 [y z_1 ..], P = R = rhs, rz_0 = rhs^T W0
+    k_rhs_pc<<<(N + 255) / 256, 256, 0, st>>>(Y, ystride, N, ld, t, k, seed, Lp, sqrt(h.noise), Z);
+    cudaMemcpyAsync(R, Z, sizeof(double) * (size_t)nc * ld, cudaMemcpyDeviceToDevice, st);
+    k_lt_part<<<nblk, RED, 0, st>>>(N, ld, nc, k, Lp, Z, ltp);
+    k_lt_fin<<<1, 1024, 0, st>>>(nblk, nc, k, ltp, Cinv_d, Yk);
+    k_apply_w<<<nblk, RED, 0, st>>>(N, ld, nc, k, Lp, Yk, h.noise, Z, W0, P, W, part);
+  } else {
+    k_rhs<<<(N + 255) / 256, 256, 0, st>>>(Y, ystride, N, ld, t, seed, Z);
+    cudaMemcpyAsync(R, Z, sizeof(double) * (size_t)nc * ld, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(P, Z, sizeof(double) * (size_t)nc * ld, cudaMemcpyDeviceToDevice, st);
+    k_dots<<<nblk, RED, 0, st>>>(R, R, N, ld, nc, part);
+  }
+  // rr_0 (r.r, or r^T P^-1 r): CTA partials summed in CTA order on the host
   cudaMemcpyAsync(part_h.data(), part, sizeof(double) * (size_t)nblk * MAXC, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
-  std::vector<double> rr0(MAXC, 0.0);
   for (int c = 0; c < nc; ++c)
     for (int b = 0; b < nblk; ++b) rr0[c] += part_h[(size_t)b * MAXC + c];
   cudaMemcpyAsync(rr_hist, rr0.data(), sizeof(double) * MAXC, cudaMemcpyHostToDevice, st);
   for (int j = 0; j < J; ++j) {
     if (!mvm(K, N, ld, P, mpart, Qv, part, sms, st)) return -2;
-    k_update_ur<<<nblk, RED, 0, st>>>(N, ld, nc, nblk, part, rr_hist, al, j, J, P, Qv, U, R, rr_part);
-    k_update_p<<<nblk, RED, 0, st>>>(N, ld, nc, nblk, rr_part, rr_hist, be, its_dev, j, J, R, P);
+    if (kp > 0) {
+      k_update_ur<<<nblk, RED, 0, st>>>(N, ld, nc, nblk, part, rr_hist, al, j, J, P, Qv, U, R, nullptr);
+      k_lt_part<<<nblk, RED, 0, st>>>(N, ld, nc, k, Lp, R, ltp);
+      k_lt_fin<<<1, 1024, 0, st>>>(nblk, nc, k, ltp, Cinv_d, Yk);
+      k_apply_w<<<nblk, RED, 0, st>>>(N, ld, nc, k, Lp, Yk, h.noise, R, W, nullptr, nullptr, rr_part);
+      k_update_p<<<nblk, RED, 0, st>>>(N, ld, nc, nblk, rr_part, rr_hist, be, its_dev, j, J, W, P);
+    } else {
+      k_update_ur<<<nblk, RED, 0, st>>>(N, ld, nc, nblk, part, rr_hist, al, j, J, P, Qv, U, R, rr_part);
+      k_update_p<<<nblk, RED, 0, st>>>(N, ld, nc, nblk, rr_part, rr_hist, be, its_dev, j, J, R, P);
+    }
   }
+  const double* Vg = kp > 0 ? W0 : Z;  // the gradient's second vectors: P^-1 z_i (or z_i)
   // y^T u_0 (column 0 of the rhs is y)
   k_dots<<<nblk, RED, 0, st>>>(Z, U, N, ld, 1, part);
   std::vector<double> al_h((size_t)nc * J), be_h((size_t)nc * J);
@@ -620,7 +902,7 @@ int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const
   cudaMemcpyAsync(its_h.data(), its_dev, sizeof(int) * nc, cudaMemcpyDeviceToHost, st);
   std::vector<double> gs_h((size_t)MAXC * (BAGEL_MAX_D + 1), 0.0);
   if (grad) {
-    k_grad_pairs<<<dim3(ntile, (nc + GC - 1) / GC), 256, 0, st>>>(X, N, ld, d, h, nc, U, Z, gpart);
+    k_grad_pairs<<<dim3(ntile, (nc + GC - 1) / GC), 256, 0, st>>>(X, N, ld, d, h, nc, U, Vg, gpart);
     k_grad_sum<<<dim3(nc, BAGEL_MAX_D + 1), RED, 0, st>>>(gpart, (size_t)ntile, d, gsum);
     cudaMemcpyAsync(gs_h.data(), gsum, sizeof(double) * (size_t)MAXC * (BAGEL_MAX_D + 1), cudaMemcpyDeviceToHost, st);
   }
@@ -638,17 +920,18 @@ int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const
       ta[j] = 1.0 / a_[j] + (j > 0 ? b_[j - 1] / a_[j - 1] : 0.0);
       if (j + 1 < n) tb[j] = sqrt(b_[j]) / a_[j];
     }
-    lds += (double)N * tridiag_e1_log_e1(ta, tb);  // ||z||^2 = N for a Rademacher probe
+    lds += rr0[i] * tridiag_e1_log_e1(ta, tb);  // z^T P^-1 z (= ||z||^2 = N for Rademacher, kp = 0)
   }
-  *logdet = lds / (double)t;
+  *logdet = logdetP + lds / (double)t;
+  if (rank_out) *rank_out = k;
   if (grad) {
-    // noise derivative: dKhat / dlog sn2 = sn2 I -> w^T v sums (u_0.u_0 and u_c.z_c)
+    // noise derivative: dKhat / dlog sn2 = sn2 I -> w^T v sums (u_0.u_0 and u_c.v_c)
     std::vector<double> dots(nc, 0.0);
     k_dots<<<nblk, RED, 0, st>>>(U, U, N, ld, 1, part);
     cudaMemcpyAsync(part_h.data(), part, sizeof(double) * (size_t)nblk * MAXC, cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
     for (int b = 0; b < nblk; ++b) dots[0] += part_h[(size_t)b * MAXC];
-    k_dots<<<nblk, RED, 0, st>>>(U + ld, Z + ld, N, ld, t, part);
+    k_dots<<<nblk, RED, 0, st>>>(U + ld, Vg + ld, N, ld, t, part);
     cudaMemcpyAsync(part_h.data(), part, sizeof(double) * (size_t)nblk * MAXC, cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
     for (int c = 1; c < nc; ++c)
