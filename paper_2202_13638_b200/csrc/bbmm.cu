@@ -43,22 +43,23 @@ struct Hyp {
 // Khat row-major with row stride ld (pad columns 0)
 __global__ void k_khat(const float* __restrict__ X, int N, int ld, int d, Hyp h, double* __restrict__ K) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
   if (j >= ld) return;
-  if (j >= N) {
-    K[(size_t)i * ld + j] = 0.0;
-    return;
-  }
-  double q = 0.0;
-#pragma unroll
-  for (int c = 0; c < BAGEL_MAX_D; ++c)
-    if (c < d) {
-      const double df = (double)X[(size_t)i * d + c] - (double)X[(size_t)j * d + c];
-      q += df * df * h.inv_l2[c];
+  for (int i = blockIdx.y; i < N; i += gridDim.y) {  // grid.y is capped at 65535 rows per pass
+    if (j >= N) {
+      K[(size_t)i * ld + j] = 0.0;
+      continue;
     }
-  double v = h.s * exp(-0.5 * q);
-  if (i == j) v += h.noise;
-  K[(size_t)i * ld + j] = v;
+    double q = 0.0;
+#pragma unroll
+    for (int c = 0; c < BAGEL_MAX_D; ++c)
+      if (c < d) {
+        const double df = (double)X[(size_t)i * d + c] - (double)X[(size_t)j * d + c];
+        q += df * df * h.inv_l2[c];
+      }
+    double v = h.s * exp(-0.5 * q);
+    if (i == j) v += h.noise;
+    K[(size_t)i * ld + j] = v;
+  }
 }
 
 // rhs columns [y | z_1 .. z_t] (stride ld): the Rademacher probes from Philox
@@ -828,7 +829,7 @@ int bbmm_launch(const float* X, const float* Y, int ystride, int N, int d, const
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   sms = std::min(sms, MAX_G);
 
-  k_khat<<<dim3(ld / 256, N), 256, 0, st>>>(X, N, ld, d, h, K);
+  k_khat<<<dim3(ld / 256, std::min(N, 65535)), 256, 0, st>>>(X, N, ld, d, h, K);
   const MvmFn mvm = mvm_fn(nc);
   cudaMemsetAsync(Z, 0, sizeof(double) * 7 * (size_t)nc * ld, st);  // Z U R P Q W W0, pads stay 0
   cudaMemsetAsync(its_dev, 0, sizeof(int) * nc, st);

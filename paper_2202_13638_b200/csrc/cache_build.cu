@@ -22,16 +22,17 @@ struct EllD {
 __global__ void k_khat(const float* __restrict__ X, int N, int d, EllD e, double s, double noise,
                        double* __restrict__ K) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
   if (j >= N) return;
-  double q = 0.0;
-  for (int c = 0; c < d; ++c) {
-    const double df = (double)X[(size_t)i * d + c] - (double)X[(size_t)j * d + c];
-    q += df * df * e.inv_l2[c];
+  for (int i = blockIdx.y; i < N; i += gridDim.y) {  // grid.y is capped at 65535 rows per pass
+    double q = 0.0;
+    for (int c = 0; c < d; ++c) {
+      const double df = (double)X[(size_t)i * d + c] - (double)X[(size_t)j * d + c];
+      q += df * df * e.inv_l2[c];
+    }
+    double v = s * exp(-0.5 * q);
+    if (i == j) v += noise;
+    K[(size_t)i * N + j] = v;
   }
-  double v = s * exp(-0.5 * q);
-  if (i == j) v += noise;
-  K[(size_t)i * N + j] = v;
 }
 
 constexpr int NB = 64;  // Cholesky block
@@ -314,7 +315,7 @@ int cb_build_khat(const float* X, int N, int d, const float* ell_host, double s,
                   double* K, cudaStream_t st) {
   EllD e{};
   for (int c = 0; c < d; ++c) e.inv_l2[c] = 1.0 / ((double)ell_host[c] * (double)ell_host[c]);
-  dim3 grid(cdiv(N, 256), N);
+  dim3 grid(cdiv(N, 256), N < 65535 ? N : 65535);
   k_khat<<<grid, 256, 0, st>>>(X, N, d, e, s, noise, K);
   return 1;
 }

@@ -12,6 +12,8 @@
 // Roofline: fp64 FMA bound -- Cholesky N^3/3, triangular inverse N^3/3, Khat^-1 tiles N^3/3 flops.
 #include <math.h>
 
+#include <algorithm>
+
 #include "bagel_internal.h"
 
 namespace {
@@ -25,16 +27,17 @@ struct Hyp64 {
 
 __global__ void k_khat64(const float* __restrict__ X, int N, int d, Hyp64 h, double* __restrict__ K) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
   if (j >= N) return;
-  double q = 0.0;
-  for (int c = 0; c < d; ++c) {
-    const double df = (double)X[(size_t)i * d + c] - (double)X[(size_t)j * d + c];
-    q += df * df * h.inv_l2[c];
+  for (int i = blockIdx.y; i < N; i += gridDim.y) {  // grid.y is capped at 65535 rows per pass
+    double q = 0.0;
+    for (int c = 0; c < d; ++c) {
+      const double df = (double)X[(size_t)i * d + c] - (double)X[(size_t)j * d + c];
+      q += df * df * h.inv_l2[c];
+    }
+    double v = h.s * exp(-0.5 * q);
+    if (i == j) v += h.noise;
+    K[(size_t)i * N + j] = v;
   }
-  double v = h.s * exp(-0.5 * q);
-  if (i == j) v += h.noise;
-  K[(size_t)i * N + j] = v;
 }
 
 // out[0] = sum_i log L_ii, out[1] = y^T alpha (one CTA, fixed order)
@@ -260,7 +263,7 @@ int exact_launch(const float* X, const float* Y, int ystride, int N, int d, cons
   h.s = (double)s;
   h.noise = (double)noise;
   int launches = 0;
-  k_khat64<<<dim3(cdiv(N, 256), N), 256, 0, st>>>(X, N, d, h, K);
+  k_khat64<<<dim3(cdiv(N, 256), std::min(N, 65535)), 256, 0, st>>>(X, N, d, h, K);
   ++launches;
   launches += cb_cholesky(K, N, pivot_flag, st);
   launches += cb_cholesky_solve(K, N, Y, ystride, alpha, nullptr, st);
@@ -290,7 +293,7 @@ int mll_launch(const float* X, const float* Y, int ystride, int N, int d, const 
   h.s = exp(log_hyp[d]);
   h.noise = exp(log_hyp[d + 1]);
   int launches = 0;
-  k_khat64<<<dim3(cdiv(N, 256), N), 256, 0, st>>>(X, N, d, h, K);
+  k_khat64<<<dim3(cdiv(N, 256), std::min(N, 65535)), 256, 0, st>>>(X, N, d, h, K);
   ++launches;
   launches += cb_cholesky(K, N, pivot_flag, st);
   launches += cb_cholesky_solve(K, N, Y, ystride, alpha, nullptr, st);

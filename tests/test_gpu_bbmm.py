@@ -232,3 +232,26 @@ def test_fit_with_bbmm_objective_improves_exact_likelihood(bagel):
     gain_bbmm = ctx.log_marginal_likelihood(1, ph_bbmm, want_grad=False)[0] - start
     assert gain_exact > 0 and gain_bbmm > 0.8 * gain_exact, (gain_exact, gain_bbmm)
     ctx.close()
+
+
+def test_more_rows_than_the_grid_y_limit(bagel):
+    """N = 66,000 > 65,535 (the grid.y limit the Khat builders loop over): with y = e_i0 at a row past
+    the limit, one CG iteration gives y^T u = (y^T y)^2 / (y^T Khat y) = 1 / (s + sn2) exactly; and the
+    exact Cholesky log p (value only) and the rank-32 preconditioned BBMM estimate agree to 2 %."""
+    X = W.make_dataset("boom", 66000, seed=5)[0]
+    N = X.shape[0]
+    i0 = 65800
+    Y = np.zeros((N, 1), dtype=np.float32)
+    Y[i0, 0] = 1.0
+    ell, s, sn = np.array([[1.0, 1.5, 0.8]], np.float32), np.array([0.5], np.float32), np.array([0.01], np.float32)
+    ctx = bagel.Context(0)
+    ctx.gp_load(X.astype(np.float32), Y, ell, s, sn)
+    v, _, ld = ctx.log_marginal_likelihood_bbmm(0, None, 1, 1, 0, want_grad=False)
+    quad = -2.0 * (v + 0.5 * ld + 0.5 * N * np.log(2 * np.pi))
+    assert quad == pytest.approx(1.0 / (float(s[0]) + float(sn[0])), rel=1e-6)
+    Yr = np.random.default_rng(3).standard_normal((N, 1)).astype(np.float32)
+    ctx.gp_load(X.astype(np.float32), Yr, ell, s, sn)
+    exact, _ = ctx.log_marginal_likelihood(0, None, want_grad=False)
+    est, _, _ = ctx.log_marginal_likelihood_bbmm(0, None, 8, 100, 1, want_grad=False, precond_rank=32)
+    assert np.isfinite(exact) and est == pytest.approx(exact, rel=0.02)
+    ctx.close()
