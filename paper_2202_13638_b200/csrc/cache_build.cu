@@ -107,47 +107,74 @@ __global__ void __launch_bounds__(TR) k_trsm_panel(double* __restrict__ A, int N
   }
 }
 
-// Trailing update A22 -= L21 L21^T on lower 64x64 tiles (16x16 threads, 4x4 each).
-__global__ void __launch_bounds__(256) k_syrk(double* __restrict__ A, int N, int kb,
+// Deferred trailing update A[i][j] -= sum_{l < nbk} A[i][kb + l] A[j][kb + l] for base <= j <= i < N,
+// j < col_end (lower triangle), on 128 x 128 tiles: 16 x 16 threads, 8 x 8 accumulators each; the two
+// 128 x 8 slices of the L columns per K step are double-buffered in shared memory (the next slice's
+// global loads are in flight while the current one is multiplied).
+constexpr int ST = 128, SK = 8;
+__global__ void __launch_bounds__(256) k_syrk(double* __restrict__ A, int N, int kb, int nbk, int base, int col_end,
                                               const int* __restrict__ pivot_flag) {
   if (*pivot_flag) return;
-  const int ti = blockIdx.y, tj = blockIdx.x;
-  if (tj > ti) return;
-  const int nb = min(NB, N - kb);
-  const int base = kb + nb;
-  const int i0 = base + ti * 64, j0 = base + tj * 64;
-  __shared__ double As[16][64];
-  __shared__ double Bs[16][64];
+  const int i0 = base + blockIdx.y * ST, j0 = base + blockIdx.x * ST;
+  if (j0 >= col_end || j0 > i0 + ST - 1) return;  // past the columns, or entirely above the diagonal
+  __shared__ double As[2][SK][ST];
+  __shared__ double Bs[2][SK][ST];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[4][4] = {};
-  for (int l0 = 0; l0 < nb; l0 += 16) {
-    for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
-      const int r = idx / 16, l = idx % 16;
-      As[l][r] = (i0 + r < N && l0 + l < nb) ? A[(size_t)(i0 + r) * N + kb + l0 + l] : 0.0;
-      Bs[l][r] = (j0 + r < N && l0 + l < nb) ? A[(size_t)(j0 + r) * N + kb + l0 + l] : 0.0;
+  // staging: thread -> (row r = threadIdx.x / 2, K elements 4 (threadIdx.x % 2) .. + 3) of both slices
+  const int sr = threadIdx.x / 2, sl = 4 * (threadIdx.x % 2);
+  const bool ai = i0 + sr < N, bj = j0 + sr < N;
+  const double* arow = A + (size_t)(i0 + sr) * N + kb;
+  const double* brow = A + (size_t)(j0 + sr) * N + kb;
+  double ra[4], rb[4];
+  auto fetch = [&](int l0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int l = l0 + sl + q;
+      ra[q] = ai && l < nbk ? arow[l] : 0.0;
+      rb[q] = bj && l < nbk ? brow[l] : 0.0;
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
 #pragma unroll
-    for (int l = 0; l < 16; ++l) {
-      double a[4], b[4];
+    for (int q = 0; q < 4; ++q) {
+      As[buf][sl + q][sr] = ra[q];
+      Bs[buf][sl + q][sr] = rb[q];
+    }
+  };
+  double acc[8][8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = As[l][ty + 16 * u];
-        b[u] = Bs[l][tx + 16 * u];
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  const int nch = (nbk + SK - 1) / SK;
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) fetch((c + 1) * SK);
+#pragma unroll
+    for (int l = 0; l < SK; ++l) {
+      double a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] = As[buf][l][ty + 16 * u];
+        b[u] = Bs[buf][l][tx + 16 * u];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
     }
+    if (c + 1 < nch) stash(buf ^ 1);
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 8; ++v) {
       const int i = i0 + ty + 16 * u, j = j0 + tx + 16 * v;
-      if (i < N && j < N && j <= i) A[(size_t)i * N + j] -= acc[u][v];
+      if (i < N && j < col_end && j <= i) A[(size_t)i * N + j] -= acc[u][v];
     }
 }
 
@@ -320,18 +347,33 @@ int cb_build_khat(const float* X, int N, int d, const float* ell_host, double s,
   return 1;
 }
 
+// Blocked right-looking Cholesky with deferred trailing updates: super-panels of NB2 = 256 columns are
+// factored block by block (NB = 64: diagonal block, panel solve over all rows below, update of the
+// super-panel's remaining columns only); the trailing matrix right of the super-panel is updated
+// once per super-panel with K = 256, so it is streamed N / 256 instead of N / 64 times.
+constexpr int NB2 = 256;
 int cb_cholesky(double* K, int N, int* pivot_flag, cudaStream_t st) {
   int launches = 0;
-  for (int kb = 0; kb < N; kb += NB) {
-    const int nb = (N - kb < NB) ? N - kb : NB;
-    k_potrf_diag<<<1, 256, 0, st>>>(K, N, kb, pivot_flag);
-    ++launches;
-    const int rem = N - kb - nb;
-    if (rem > 0) {
-      k_trsm_panel<<<cdiv(rem, TR), TR, 0, st>>>(K, N, kb, pivot_flag);
-      const int t2 = cdiv(rem, 64);
-      k_syrk<<<dim3(t2, t2), 256, 0, st>>>(K, N, kb, pivot_flag);
-      launches += 2;
+  for (int KB = 0; KB < N; KB += NB2) {
+    const int pe = (N - KB < NB2) ? N : KB + NB2;
+    for (int kb = KB; kb < pe; kb += NB) {
+      const int nb = (N - kb < NB) ? N - kb : NB;
+      k_potrf_diag<<<1, 256, 0, st>>>(K, N, kb, pivot_flag);
+      ++launches;
+      const int rem = N - kb - nb;
+      if (rem > 0) {
+        k_trsm_panel<<<cdiv(rem, TR), TR, 0, st>>>(K, N, kb, pivot_flag);
+        ++launches;
+        const int base = kb + nb;
+        if (base < pe) {  // the super-panel's remaining columns, all rows below
+          k_syrk<<<dim3(cdiv(pe - base, ST), cdiv(N - base, ST)), 256, 0, st>>>(K, N, kb, nb, base, pe, pivot_flag);
+          ++launches;
+        }
+      }
+    }
+    if (pe < N) {  // everything right of the super-panel, K = its width
+      k_syrk<<<dim3(cdiv(N - pe, ST), cdiv(N - pe, ST)), 256, 0, st>>>(K, N, KB, pe - KB, pe, N, pivot_flag);
+      ++launches;
     }
   }
   return launches;
