@@ -32,7 +32,7 @@ namespace bbmm {
 constexpr int MAXC = 17;      // t + 1 <= 17 columns (probes <= 16)
 constexpr int LDV = 256;      // vector / Khat row stride granularity (pads are zero)
 constexpr int RED = 256;      // threads of the reduction kernels
-constexpr int GC = 4;         // columns per CTA of the gradient pass
+constexpr int GC = 9;         // columns per CTA of the gradient pass (t = 8: one pass)
 constexpr int GT = 64;        // gradient pair tile
 
 struct Hyp {
