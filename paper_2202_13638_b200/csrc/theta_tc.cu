@@ -98,21 +98,25 @@ __device__ __forceinline__ void split8(const float* v, float sc, uint4& hi, uint
 
 // Per K block: max |delta| of every adjoint-tape column and max |phi| (the layer-0 input) -- the
 // power-of-two operand scales of k_theta_grad_tc.  Streams whole tape rows (coalesced float4).
+// float4 column groups of the adjoint tape a CTA covers: every layer's delta segment (<= 8 layers of
+// <= 256 outputs, each padded to a multiple of 4) -- d_ld / 4 <= 520
+constexpr int CM_U = (BAGEL_MAX_LAYERS * (BAGEL_MAX_WIDTH + 4) / 4 + 31) / 32;
 __global__ void __launch_bounds__(256) k_theta_colmax(long long K, int d_ld, int act_ld, int phi_w,
                                                        const float* __restrict__ delta,
                                                        const float* __restrict__ act, float* __restrict__ colmax) {
-  __shared__ float red[8][MAXNP * 4 + 4];
+  __shared__ float red[8][32 * CM_U];
+  __shared__ float red_phi[8];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long k0 = (long long)blockIdx.x * RPB, k1 = min(K, k0 + RPB);
   const int n4 = d_ld / 4;
-  float mx[8];
+  float mx[CM_U];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) mx[u] = 0.0f;
+  for (int u = 0; u < CM_U; ++u) mx[u] = 0.0f;
   float pm = 0.0f;
   for (long long k = k0 + warp; k < k1; k += 8) {
     const float4* row = reinterpret_cast<const float4*>(delta + k * d_ld);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < CM_U; ++u) {
       const int c4 = lane + 32 * u;
       if (c4 < n4) {
         const float4 v = __ldg(row + c4);
@@ -124,10 +128,10 @@ __global__ void __launch_bounds__(256) k_theta_colmax(long long K, int d_ld, int
   // per float4 column group (the scale of an output is the max over its group of 4 columns: a
   // power-of-two scale only needs an upper bound)
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < CM_U; ++u)
     if (lane + 32 * u < n4) red[warp][lane + 32 * u] = mx[u];
   for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
-  if (lane == 0) red[warp][MAXNP * 4] = pm;
+  if (lane == 0) red_phi[warp] = pm;
   __syncthreads();
   float* out = colmax + (size_t)blockIdx.x * (d_ld + 1);
   for (int c = threadIdx.x; c < d_ld; c += 256) {
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(256) k_theta_colmax(long long K, int d_ld, int
   }
   if (threadIdx.x == 0) {
     float m = 0.0f;
-    for (int w = 0; w < 8; ++w) m = fmaxf(m, red[w][MAXNP * 4]);
+    for (int w = 0; w < 8; ++w) m = fmaxf(m, red_phi[w]);
     out[d_ld] = m;
   }
 }

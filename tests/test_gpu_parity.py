@@ -541,3 +541,19 @@ def test_wide_policy_ragged_widths(bagel):
     seed = W.rollout_seed(9)
     cost, grad = _rollout_gpu(ctx, wl, goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "ragged wide policy")
+
+
+def test_wide_policy_narrow_middle_layer(bagel):
+    """The cluster MLP kernels (mlp_tc.cu) with a 16-wide layer between 256-wide ones: that layer's
+    16 output columns are one 16-column unit, so three of the four CTAs of each cluster compute no
+    columns there and hand over empty regions, forward and backward (the path whose unconsumed
+    barrier phases once let a CTA exit with a peer's copy in flight)."""
+    wl = W.make_workload(plant="boom", N=600, rank=64, hidden=(256, 256, 16, 256, 256), B=200, T=4)
+    assert W.n_params(wl.sizes) > 100000
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    goals = (wl.x0 + np.array([0.3, -0.1], dtype=np.float32)).astype(np.float32)
+    seed = W.rollout_seed(12)
+    cost, grad = _rollout_gpu(ctx, wl, goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "narrow middle layer")
