@@ -557,3 +557,17 @@ def test_wide_policy_narrow_middle_layer(bagel):
     seed = W.rollout_seed(12)
     cost, grad = _rollout_gpu(ctx, wl, goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, goals, seed), "narrow middle layer")
+
+
+@pytest.mark.parametrize("plant,hidden,phi", [("boom", (128,) * 7, "xgd"), ("hydraulic4", (256, 192), "xg")])
+def test_wide_policy_shapes(bagel, plant, hidden, phi):
+    """More wide-policy shapes through the cluster MLP kernels and the tensor-core theta gradient:
+    the maximum depth (8 layers, 7 hidden of 128) with the [x, g, g - x] input, and the hydraulic
+    plant (p = 4 outputs, q = 2 actions: a 2-wide output layer) with 256/192-wide layers; ragged B."""
+    wl = W.make_workload(plant=plant, N=700, rank=64, hidden=hidden, B=130, T=3, phi_mode=phi)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    seed = W.rollout_seed(13)
+    cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), f"{plant} {hidden} {phi}")
