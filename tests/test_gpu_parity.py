@@ -571,3 +571,16 @@ def test_wide_policy_shapes(bagel, plant, hidden, phi):
     seed = W.rollout_seed(13)
     cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), f"{plant} {hidden} {phi}")
+
+
+@pytest.mark.parametrize("B", [1, 129])
+def test_wide_policy_tiny_and_ragged_batches(bagel, B):
+    """Cluster MLP kernels with a single trajectory (one cluster, 127 empty rows) and with 129 (a
+    second cluster holding one row), C3's policy shape."""
+    wl = W.make_workload(plant="boom", N=500, rank=64, hidden=(256, 256, 256), B=B, T=3)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    ctx = _ctx(bagel, wl, build_cache=False)
+    _inject(ctx, mdl)
+    seed = W.rollout_seed(14)
+    cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
+    _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), f"wide B={B}")
