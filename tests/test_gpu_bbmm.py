@@ -157,7 +157,8 @@ def _envelope_pc(X, y, h, t, J, k, seed, ref, n=4):
     return env
 
 
-@pytest.mark.parametrize("N,t,J,k", [(40, 4, 40, 5), (63, 8, 12, 8), (257, 8, 100, 16), (520, 8, 150, 32)])
+@pytest.mark.parametrize("N,t,J,k", [(40, 4, 40, 5), (63, 8, 12, 8), (257, 8, 100, 16), (520, 8, 150, 32),
+                                     (300, 16, 80, 64)])
 def test_bbmm_preconditioned_matches_oracle(bagel, N, t, J, k):
     """GPyTorch's rank-k pivoted-Cholesky preconditioner (reading R40) against the oracle's
     orc_mll_bbmm_pc, same probes and iterations, within 8 oracle-only envelopes + 1e-11 relative (as
