@@ -584,3 +584,24 @@ def test_wide_policy_tiny_and_ragged_batches(bagel, B):
     seed = W.rollout_seed(14)
     cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
     _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), f"wide B={B}")
+
+
+def test_context_reuse_across_models_and_batches(bagel):
+    """One context, reconfigured: a small model and batch, then a larger N / rank / B and a wider
+    policy, then back to the small one -- every rollout against the oracle (workspaces sized for one
+    shape must be re-derived, not reused stale)."""
+    ctx = bagel.Context(0)
+    shapes = [dict(N=300, rank=40, hidden=(32, 32), B=64, T=4),
+              dict(N=1400, rank=200, hidden=(256, 256), B=300, T=3),
+              dict(N=300, rank=40, hidden=(32, 32), B=64, T=4)]
+    for i, sh in enumerate(shapes):
+        wl = W.make_workload(plant="boom", data_seed=i % 2, **sh)
+        mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+        ctx.gp_load(wl.X, wl.Y, wl.ell, wl.s, wl.noise)
+        ctx.policy_configure(wl.sizes)
+        ctx.reward_configure(wl.Q, wl.sigma_r)
+        _inject(ctx, mdl)
+        seed = W.rollout_seed(20 + i)
+        cost, grad = _rollout_gpu(ctx, wl, wl.goals, seed)
+        _assert_cost_grad(cost, grad, _rollout_oracle(mdl, wl, wl.goals, seed), f"reuse {i}")
+    ctx.close()
