@@ -246,14 +246,15 @@ static MvmPlan mvm_plan(int N, int ld, int sms) {
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {  // thread-safe one-time lookup
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&f), cudaEnableDefault, &q) !=
             cudaSuccess ||
         q != cudaDriverEntryPointSuccess)
-      encode = nullptr;
-  }
+      f = nullptr;
+    return f;
+  }();
   return encode;
 }
 

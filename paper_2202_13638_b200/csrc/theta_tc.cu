@@ -376,14 +376,16 @@ int theta_grad_tc(const PolicyDesc& P, long long K, const float* act, const floa
   k_theta_colmax<<<nblk, 256, 0, st>>>(K, P.d_ld, P.act_ld, P.sizes[0], delta, act, colmax);
   const dim3 grid(nblk, nj);
   // tensor maps: the adjoint / activation tapes as 2-D (columns, rows) fp32 arrays
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {  // thread-safe one-time lookup
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&f), cudaEnableDefault, &q) !=
             cudaSuccess || q != cudaDriverEntryPointSuccess)
-      return -1;
-  }
-  static Maps maps;
+      f = nullptr;
+    return f;
+  }();
+  if (!encode) return -1;
+  Maps maps;  // per call (no shared host state between contexts)
   for (int j = 0; j < nj; ++j) {
     for (int t = 0; t < 2; ++t) {
       const bool isd = t == 0;
