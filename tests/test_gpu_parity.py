@@ -403,6 +403,23 @@ def test_batch_invariance_bitwise(c2):
         assert torch.equal(sub["ret"].cpu(), full["ret"][off:off + n]), ("ret", off, n)
 
 
+def test_batch_invariance_across_reduce_modes(c2):
+    """A doubled C2 batch (2048 trajectories: 288 CTA pairs, more than one resident wave) runs
+    reduce 1 as the separate k_r1a_tc / k_r1b_tc kernels instead of inside pass 1 after a grid
+    barrier; its first 1024 trajectories must replay the 1024-batch (fused) run bit for bit."""
+    wl, mdl, ctx = c2
+    seed = W.rollout_seed(1)
+    full = ctx.rollout_trace(wl.theta, wl.x0, wl.goals, wl.T, seed)
+    full = {k: v.cpu() for k, v in full.items()}
+    x0 = np.concatenate([wl.x0, wl.x0[::-1]]).astype(np.float32)
+    g = np.concatenate([wl.goals, wl.goals[::-1]]).astype(np.float32)
+    big = ctx.rollout_trace(wl.theta, x0, g, wl.T, seed)
+    n = wl.B
+    for key in ("x", "mu", "var"):
+        assert torch.equal(big[key].cpu()[:, :n], full[key]), key
+    assert torch.equal(big["ret"].cpu()[:n], full["ret"])
+
+
 _C2_IT3_REASON = (
     "iteration 3: trajectory 240 carries 40% of the batch gradient norm and is the batch's most "
     "ill-conditioned row; the tensor-core accumulator's truncation (scripts/diag_tmem_acc.py: every MMA "
