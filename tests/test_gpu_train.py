@@ -112,6 +112,33 @@ def test_training_run_matches_oracle_sampled_goals(bagel):
     ctx.close()
 
 
+def test_training_run_wide_policy_matches_oracle(bagel):
+    """Algorithm 1 with a wide policy (the cluster MLP kernels, the tensor-core theta gradient and
+    the weight repacking every iteration): 4 iterations at lr 1e-2 with sampled goals."""
+    from paper_2202_13638_b200.train import train_policy
+
+    wl = W.make_workload(plant="boom", N=500, rank=64, hidden=(256, 256), B=96, T=6)
+    mdl = O.Model.build(wl.X, wl.Y, wl.ell, wl.s, wl.noise, wl.rank)
+    lo, hi = wl.X[:, :wl.p].min(0), wl.X[:, :wl.p].max(0)
+    ctx = bagel.setup(wl, device=0)
+    for m in range(mdl.p):
+        ctx.cache_set(m, mdl.alpha[m], mdl.R[m])
+    th, log = train_policy(ctx, wl.theta, wl.T, 4, wl.B, lo, hi, lr=1e-2, seed0=0x5EED2000)
+    th_o, costs_o = O.train(mdl, wl.sizes, "xg", wl.theta, wl.Q, wl.sigma_r, wl.T, 4, wl.B, lo, hi, 0x5EED2000,
+                            lr=1e-2)
+    np.testing.assert_allclose(log.cost, costs_o, rtol=1e-3)
+    # Adam normalises per coordinate (a step is lr m / sqrt(v)), so a coordinate's step error is lr
+    # times the RELATIVE error of its own gradient: tiny on the coordinates that matter, up to 2 lr
+    # where a gradient sits below the ~1e-4 (of the norm) gradient error (scripts/diag_train.py: the
+    # per-iteration costs agree to 7e-5; 2 of 67,329 first-iteration gradients differ in sign, both
+    # at 1.9e-7 of the largest; theta after 4 iterations 2.0e-3 relative L2, 3.7e-4 after 1).
+    # Asserted: the costs above, theta within 5e-3 relative L2, no coordinate beyond 2 lr per step.
+    t = th.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(t - th_o) <= 5e-3 * np.linalg.norm(th_o)
+    assert np.abs(t - th_o).max() <= 2 * 1e-2 * 4
+    ctx.close()
+
+
 def test_exp1_shape_reaches_the_spec_return_bar(bagel):
     """SPEC S:416's end-to-end bar on the Exp. 1 shape (workload E1: n = 2200, b = 100, H = 300,
     policy [8, 8], fixed start and goal, Adam lr 1e-2): the mean return per step
